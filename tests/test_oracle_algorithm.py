@@ -1,0 +1,449 @@
+"""Pins of the oracle's Algorithm-1 step against hand-worked trees,
+SPEC behaviours, brute force over all subsets/subtrees, and invariants."""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from inputs import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "toy_cfg1.json")
+
+
+@pytest.fixture(scope="module")
+def toy():
+    with open(GOLD) as f:
+        return json.load(f)
+
+
+def toy_pool(toy, T):
+    V = toy["V"]
+    rows = {name: synth.logits_from_probs(V, {int(t): p for t, p in spec.items()})
+            for name, spec in toy["rows"].items()}
+    pool = np.stack([rows[toy["node_rows"][min(i, len(toy["node_rows"]) - 1)]] for i in range(T)])
+    return pool[None].astype(np.float32)
+
+
+def toy_target(toy, T, tok_fill=0):
+    V = toy["V"]
+    tg = np.zeros((1, T, V), np.float32)
+    for node, t in toy["verify"]["argmax"].items():
+        tg[0, int(node), t] = 5.0
+    for i in range(T):
+        if str(i) not in toy["verify"]["argmax"]:
+            tg[0, i, 31] = 5.0  # a token that is never drafted
+    return tg
+
+
+def run_toy(orc, toy, preset, **over):
+    c = toy["cost"]
+    if preset == "hotpath":
+        P = toy["hotpath"]
+        cfg = orc.Config(V=toy["V"], k=toy["k"], d=toy["d"], W=0, b=1, B_verify=P["B_verify"],
+                         alpha=P["alpha"], omega=1, selection=orc.PREFIX,
+                         accept_model=orc.NODE_SUM, dtype=orc.FP32)
+        cost = orc.Cost(lam=c["lam"], eta=P["eta"], c_T=c["c_T"])
+    else:
+        P = toy["paper"]
+        cfg = orc.Config(V=toy["V"], k=toy["k"], d=toy["d"], W=0, b=1, B_verify=P["B_verify"],
+                         alpha=P["alpha"], omega=0, selection=orc.FROZEN,
+                         accept_model=orc.PATH_MEAN, dtype=orc.FP32)
+        cost = orc.Cost(lam=c["lam"], c_T=c["c_T"])
+    for kk, v in over.items():
+        setattr(cfg, kk, v)
+    T = cfg.tmax()
+    return orc.step(cfg, cost, toy_pool(toy, T), toy_target(toy, T), root_tok=[-1], root_pos=[100])
+
+
+def test_toy_hotpath_tree(orc, toy):
+    """SURVEY §8(c) toy example, HOTPATH preset: hand-traced layer decisions and final tree."""
+    H = toy["hotpath"]
+    res = run_toy(orc, toy, "hotpath")
+    n = res.n_nodes[0]
+    assert n == len(H["tokens"])
+    assert list(res.tok[0, :n]) == H["tokens"]
+    assert list(res.parent[0, :n]) == H["parent"]
+    assert list(res.depth[0, :n]) == H["depth"]
+    assert [int(w) for w in res.mask[0, :n, 0]] == H["mask_words"]
+    assert list(res.trace[:, 3].astype(int)) == H["layer_admits"]
+    np.testing.assert_allclose(res.trace[:, 7], H["layer_S_after"], rtol=1e-6)
+    assert res.trace[1, 8] == H["layer2_argmax_j"]  # argmax_j S_j == first-failure cut
+    assert res.E == pytest.approx(H["E"], rel=1e-6)
+    assert res.N == H["N"]
+    assert res.S == pytest.approx(H["S"], rel=1e-6)
+    # position ids = root_pos + depth (Q21)
+    assert list(res.pos[0, :n]) == [100 + d for d in H["depth"]]
+    # alpha = 0.8 gives the same tree (SURVEY note)
+    res8 = run_toy(orc, toy, "hotpath", alpha=0.8)
+    assert list(res8.tok[0, :res8.n_nodes[0]]) == H["tokens"]
+
+
+def test_toy_hotpath_prefix_S_sequence(orc, toy):
+    """Layer-2 prefix speedups S_1..S_4 (hand values) recomputed from the oracle's own
+    candidate dump with Eq.(1): S_j = c_T*(1 + E0 + sum b)/(c_T + N0 + j)."""
+    H = toy["hotpath"]
+    res = run_toy(orc, toy, "hotpath")
+    L2 = res.layer_cands(2)
+    bs = np.sort(L2["b"])[::-1]
+    E0, N0 = res.trace[1, 5], res.trace[1, 4]
+    S = [10 * (1 + E0 + bs[:j].sum()) / (10 + N0 + j) for j in range(1, 5)]
+    np.testing.assert_allclose(S, H["layer2_prefix_S"], rtol=1e-6)
+
+
+def test_toy_budget_binds(orc, toy):
+    """B_verify = 3: layer-2 eligibility min(B - n, W) = 1 (Q3) -> tree {u1, u2, u1c1}."""
+    H = toy["hotpath_budget3"]
+    res = run_toy(orc, toy, "hotpath", B_verify=H["B_verify"])
+    n = res.n_nodes[0]
+    assert list(res.tok[0, :n]) == H["tokens"]
+    assert list(res.parent[0, :n]) == H["parent"]
+
+
+def test_toy_verify_walk(orc, toy):
+    """Greedy walk: target argmax 5, 7, 4 -> accept [u1, u1c1], bonus 4."""
+    V = toy["verify"]
+    res = run_toy(orc, toy, "hotpath")
+    assert res.accept_len[0] == V["accept_len"]
+    assert list(res.accept_path[0, :2]) == V["accept_path"]
+    assert res.bonus[0] == V["bonus"]
+
+
+def test_toy_paper_preset(orc, toy):
+    """PAPER preset (Algorithm 1 literally, Eq.(2) path mean, S(empty)=0): tree {u1, u2},
+    R = 2.25, stops with an empty active set."""
+    P = toy["paper"]
+    res = run_toy(orc, toy, "paper")
+    n = res.n_nodes[0]
+    assert list(res.tok[0, :n]) == P["tokens"]
+    assert res.S == pytest.approx(P["S"], rel=1e-6)
+    assert res.E == pytest.approx(P["E"], rel=1e-6)
+    assert res.trace[1, 3] == 0 and res.trace[2, 12] == 0  # layer 2 admits nothing, layer 3 not run
+
+
+def _pool_from_fn(b, T, V, fn):
+    return np.stack([np.stack([fn(r, u) for u in range(T)]) for r in range(b)]).astype(np.float32)
+
+
+def test_spec_deterministic_chain(orc):
+    """deterministic draft (top-1 p = 1), B = 5, d = 7 -> chain of 5, budget exhausted."""
+    V = 16
+    def fn(r, u):
+        x = np.full(V, -np.inf, np.float32)
+        x[(u * 3) % V] = 0.0
+        return x
+    # HOTPATH preset (omega = 1, eta = c_T): alpha*c_T/dc = 8 > S_n = 10(1+n)/(10+n) for n < 35
+    cfg = orc.Config(V=V, k=2, d=7, W=0, b=1, B_verify=5, alpha=0.8, omega=1, selection=orc.PREFIX,
+                     accept_model=orc.NODE_SUM, dtype=orc.FP32)
+    cost = orc.Cost(lam=1.0, gamma=0.01, delta=0.01, rho=1.0, eta=10.0, c_T=10.0)
+    pool = _pool_from_fn(1, cfg.tmax(), V, fn)
+    res = orc.step(cfg, cost, pool)
+    assert res.n_nodes[0] == 6
+    assert list(res.depth[0, :6]) == [0, 1, 2, 3, 4, 5]
+    assert res.trace[4, 12] == 1 and res.trace[5, 12] == 0  # stopped by the budget after layer 5
+    # PAPER preset (omega = 0, beta = eta = 0): for a chain of all-ones S_n = c_T*n/cost(n) and the
+    # marginal ratio alpha*c_T/dc(n) <= c_T*n/cost(n) for any convex cost through the origin, so
+    # the strict rule (Q8) stops after layer 1.  SPEC's S:297 expectation holds only for the
+    # HOTPATH reading above (Q27).
+    cfgp = orc.Config(V=V, k=2, d=7, W=0, b=1, B_verify=5, alpha=0.8, omega=0, selection=orc.FROZEN,
+                      accept_model=orc.PATH_MEAN, dtype=orc.FP32)
+    resp = orc.step(cfgp, orc.Cost(lam=1.0, gamma=0.01, delta=0.01, rho=1.0, c_T=10.0), pool)
+    assert resp.n_nodes[0] == 2
+
+
+def test_spec_uniform_stops_early(orc):
+    """near-uniform draft over V = 1000: layer-2 Delta J < 0 -> empty active set."""
+    V = 1000
+    cfg = orc.Config(V=V, k=4, d=6, W=0, b=1, B_verify=60, alpha=0.8, omega=0, selection=orc.FROZEN,
+                     accept_model=orc.PATH_MEAN, dtype=orc.FP32)
+    cost = orc.Cost(lam=1.0, c_T=10.0)
+    res = orc.step(cfg, cost, _pool_from_fn(1, cfg.tmax(), V, lambda r, u: np.zeros(V, np.float32)))
+    assert res.trace[0, 3] == 4            # layer 1 admits everything with p > 0 (S(empty)=0)
+    assert res.trace[1, 3] == 0            # layer 2: 0.8*10*(1e-6/4) < S -> nothing
+    assert res.n_nodes[0] == 5
+
+
+def test_spec_depth_zero(orc):
+    """d = 0 -> root-only tree."""
+    cfg = orc.Config(V=8, k=2, d=0, b=1, B_verify=4, dtype=orc.FP32)
+    res = orc.step(cfg, orc.Cost(lam=1, eta=1, c_T=1), np.zeros((1, cfg.tmax(), 8), np.float32))
+    assert res.n_nodes[0] == 1 and res.N == 0
+
+
+# ---------------------------------------------------------------------------------------
+# brute-force pins
+# ---------------------------------------------------------------------------------------
+
+def _S_tilde(cost, omega, b, E, N):
+    """Eq.(1) generalised (Q13/Q19) times b: c_T*(omega*b+E)/cost(N)."""
+    C = cost.lam * N + cost.beta + cost.gamma * (math.exp(min(cost.delta * N ** cost.rho, 700)) - 1) + cost.eta
+    return 0.0 if C <= 0 else cost.c_T * (omega * b + E) / C
+
+
+def _kary_pool(rng, b, k, d, V, dtype=np.float32):
+    n = sum(k ** l for l in range(d + 1))
+    x = rng.standard_normal((b, n, V)).astype(np.float32) * 1.5
+    heads = rng.integers(0, V, size=(b, n, 3))
+    for r in range(b):
+        for f in range(n):
+            x[r, f, heads[r, f]] += rng.uniform(1, 4, 3).astype(np.float32)
+    return x
+
+
+def test_prefix_is_argmax_over_all_subsets(orc):
+    """SURVEY §8(c) 'PREFIX == argmax over prefixes': with alpha = 1, DIFFERENCE, NODE_SUM and a
+    convex cost, the greedy prefix cut of each layer maximises S over ALL subsets of that layer's
+    eligible candidates (mediant argument), and equals argmax_j S_j."""
+    rng = np.random.default_rng(11)
+    checked = 0
+    for seed in range(60):
+        b = int(rng.integers(1, 3))
+        k, d, V = 2, 3, 12
+        cost = orc.Cost(lam=float(rng.uniform(0.05, 0.5)), gamma=float(rng.uniform(0.0, 0.5)),
+                        delta=float(rng.uniform(0.01, 0.2)), rho=float(rng.uniform(1.0, 1.6)),
+                        eta=1.0, c_T=1.0)
+        cfg = orc.Config(V=V, k=k, d=d, W=0, b=b, B_verify=64 * b, alpha=1.0, omega=1,
+                         selection=orc.PREFIX, accept_model=orc.NODE_SUM, marginal=orc.DIFFERENCE,
+                         dtype=orc.FP32, row_mode=orc.ROWS_KARY)
+        res = orc.step(cfg, cost, _kary_pool(rng, b, k, d, V))
+        for l in range(1, d + 1):
+            if not res.trace[l - 1, 12]:
+                break
+            c = res.layer_cands(l)
+            bvals, adm = c["b"], c["admitted"]
+            E0, N0 = res.trace[l - 1, 5], int(res.trace[l - 1, 4])
+            best, best_set = -1.0, None
+            for m in range(len(bvals) + 1):
+                for sub in itertools.combinations(range(len(bvals)), m):
+                    s = _S_tilde(cost, 1, b, E0 + bvals[list(sub)].sum(), N0 + m)
+                    if s > best * (1 + 1e-12):
+                        best, best_set = s, set(sub)
+            got = _S_tilde(cost, 1, b, E0 + bvals[adm].sum(), N0 + int(adm.sum()))
+            assert got == pytest.approx(best, rel=1e-12), (seed, l)
+            assert int(adm.sum()) == int(res.trace[l - 1, 8])  # first failure == argmax_j S_j
+            # the admitted set is the top-|adm| by benefit
+            order = np.lexsort((c["c"], c["r"], -bvals))
+            assert set(np.nonzero(adm)[0]) == set(order[: int(adm.sum())])
+            checked += 1
+    assert checked > 100
+
+
+def _enumerate_subtrees(children, root=0):
+    """All ancestor-closed subsets (as frozensets of non-root nodes) of a tree."""
+    def rec(u):
+        opts = [frozenset()]
+        for v in children[u]:
+            sub = [frozenset([v]) | s for s in rec(v)]
+            opts = [a | s for a in opts for s in [frozenset()] + sub]
+        return opts
+    return rec(root)
+
+
+def test_subtree_count_k2_d3():
+    """676 ancestor-closed subtrees (incl. empty) of the k=2, d=3 candidate tree."""
+    ch = {f: ([2 * f + 1, 2 * f + 2] if f < 7 else []) for f in range(15)}
+    assert len(_enumerate_subtrees(ch)) == 676
+
+
+# Regression floors pinned from the first oracle run (S:317 asks the implementer to pin them):
+# HOTPATH (NODE_SUM, omega=1) observed min 0.945 / mean 0.996 -> SPEC's floor (0.9, 0.97) holds.
+# PAPER (Algorithm 1 literally: S(empty)=0 seed admits every positive layer-1 candidate, and
+# Eq.(13)'s 1/|P| dilution over-credits siblings under the Eq.(2) path mean) observed
+# min 0.235 / mean 0.351: the paper's greedy is far from the path-mean optimum ("not
+# globally optimal"); recorded in DESIGN.md §3 (Q28).
+FLOORS = {"paper": (0.20, 0.33), "hotpath": (0.90, 0.97)}
+
+
+@pytest.mark.parametrize("preset", ["paper", "hotpath"])
+def test_greedy_vs_exhaustive_optimum(orc, preset):
+    """P:264-266 / P:365 'not globally optimal': greedy S over the exhaustive optimum of all 676
+    subtrees (k=2, d=3, n <= B), 200 seeds.  SPEC S:317/S:487 regression floor: mean >= 0.97;
+    the min is pinned from the first oracle run (ratio <= 1 always)."""
+    rng = np.random.default_rng(2024 if preset == "paper" else 77)
+    k, d, V = 2, 3, 16
+    ratios = []
+    ch = {f: ([2 * f + 1, 2 * f + 2] if f < 7 else []) for f in range(15)}
+    subtrees = _enumerate_subtrees(ch)
+    for seed in range(200):
+        B = int(rng.integers(3, 15))
+        if preset == "paper":
+            cfg = orc.Config(V=V, k=k, d=d, W=0, b=1, B_verify=B, alpha=0.8, omega=0,
+                             selection=orc.FROZEN, accept_model=orc.PATH_MEAN, dtype=orc.FP32,
+                             row_mode=orc.ROWS_KARY)
+            cost = orc.Cost(lam=float(rng.uniform(0.05, 0.3)), gamma=float(rng.uniform(0.01, 0.3)),
+                            delta=float(rng.uniform(0.02, 0.2)), rho=float(rng.uniform(1.0, 1.5)), c_T=1.0)
+        else:
+            cfg = orc.Config(V=V, k=k, d=d, W=0, b=1, B_verify=B, alpha=0.8, omega=1,
+                             selection=orc.PREFIX, accept_model=orc.NODE_SUM, dtype=orc.FP32,
+                             row_mode=orc.ROWS_KARY)
+            cost = orc.Cost(lam=float(rng.uniform(0.02, 0.2)), gamma=float(rng.uniform(0.01, 0.3)),
+                            delta=float(rng.uniform(0.02, 0.2)), rho=float(rng.uniform(1.0, 1.5)),
+                            eta=1.0, c_T=1.0)
+        pool = _kary_pool(rng, 1, k, d, V)
+        res = orc.step(cfg, cost, pool)
+        # full candidate tree probabilities by heap index (library softmax + lexsort)
+        cum = np.zeros(15)
+        cum[0] = 1.0
+        par = [-1] + [(f - 1) // 2 for f in range(1, 15)]
+        for f in range(7):
+            x = pool[0, f].astype(np.float64)
+            e = np.exp(x - x.max()); pr = e / e.sum()
+            top = np.lexsort((np.arange(V), -x))[:2]
+            for j in range(2):
+                cum[2 * f + 1 + j] = cum[f] * pr[top[j]]
+        best = 0.0
+        for sub in subtrees:
+            if len(sub) > B:
+                continue
+            nodes = [0] + sorted(sub)
+            if preset == "paper":
+                idx = {u: i for i, u in enumerate(nodes)}
+                E = orc.l_tree_path_mean([-1] + [idx[par[u]] for u in nodes[1:]], [cum[u] for u in nodes])
+                s = _S_tilde(cost, 0, 1, E, len(sub))
+            else:
+                s = _S_tilde(cost, 1, 1, sum(cum[u] for u in sub), len(sub))
+            best = max(best, s)
+        assert res.S <= best * (1 + 1e-9)
+        ratios.append(res.S / best if best > 0 else 1.0)
+    ratios = np.array(ratios)
+    print(preset, "greedy/opt ratio: min %.4f mean %.4f" % (ratios.min(), ratios.mean()))
+    floor_min, floor_mean = FLOORS[preset]
+    assert ratios.min() >= floor_min and ratios.mean() >= floor_mean, (ratios.min(), ratios.mean())
+
+
+# ---------------------------------------------------------------------------------------
+# invariants on larger random instances
+# ---------------------------------------------------------------------------------------
+
+def _random_instance(orc, rng, V=64, dtype="fp32"):
+    b = int(rng.integers(1, 5))
+    k = int(rng.integers(2, 6))
+    d = int(rng.integers(1, 6))
+    W = int(rng.choice([0, k, 3]))
+    B_verify = int(rng.integers(b, 24 * b))
+    cfg = orc.Config(V=V, k=k, d=d, W=W, b=b, B_verify=B_verify, alpha=float(rng.choice([0.5, 0.8, 1.0])),
+                     omega=int(rng.integers(0, 2)), selection=int(rng.integers(0, 2)),
+                     accept_model=int(rng.integers(0, 2)), marginal=int(rng.integers(0, 2)),
+                     dtype=orc.FP32 if dtype == "fp32" else orc.BF16)
+    cost = orc.Cost(lam=float(rng.uniform(0.01, 0.3)), gamma=float(rng.uniform(0, 0.3)),
+                    delta=float(rng.uniform(0.001, 0.1)), rho=float(rng.uniform(0.8, 1.5)),
+                    eta=float(rng.uniform(0.5, 2.0)) if cfg.omega else 0.0, c_T=1.0)
+    T = cfg.tmax()
+    pool = synth.draft_pool(int(rng.integers(1 << 30)), b, T, V, dtype=dtype, a_lo=2, a_hi=8, sigma_bg=1.0)
+    return cfg, cost, pool
+
+
+def test_invariants_random(orc):
+    """Budget n_r <= B; O(kB) candidate count; admission re-scores
+    positive; cum = cum(parent)*p; A7 mask invariants; beta in [0,1]."""
+    rng = np.random.default_rng(99)
+    for it in range(150):
+        cfg, cost, pool = _random_instance(orc, rng)
+        T = cfg.tmax()
+        tgt = synth.target_pool(pool, 5, 0.5)
+        res = orc.step(cfg, cost, pool, tgt, root_tok=np.arange(cfg.b), root_pos=np.arange(cfg.b) * 7)
+        B, k = cfg.B, cfg.k
+        cand_per_req = np.zeros(cfg.b, int)
+        for l in range(1, cfg.d + 1):
+            if not res.trace[l - 1, 12]:
+                continue
+            c = res.layer_cands(l)
+            for r in range(cfg.b):
+                cand_per_req[r] += int((c["r"] == r).sum())
+            # admission: every admitted candidate satisfies the rule against its state
+            if cfg.selection == orc.FROZEN:
+                N0, E0 = int(res.trace[l - 1, 4]), res.trace[l - 1, 5]
+                dc0 = orc.dc(cost, N0, cfg.marginal)[0]
+                S0 = _S_tilde(cost, cfg.omega, cfg.b, E0, N0)
+                assert np.all(cfg.alpha * cost.c_T * c["b"][c["admitted"]] / dc0 > S0)
+        for r in range(cfg.b):
+            n = res.n_nodes[r]
+            assert n - 1 <= B
+            # O(kB): k * (1 + sum_{l<L} |A_l|) <= k * (B + 1)
+            assert cand_per_req[r] <= k * (B + 1)
+            for i in range(1, n):
+                pa = res.parent[r, i]
+                assert 0 <= pa < i and res.depth[r, i] == res.depth[r, pa] + 1
+                assert res.cum[r, i] == res.cum[r, pa] * res.p[r, i]
+            for i in range(T):
+                bits = int.from_bytes(res.mask[r, i].astype("<u4").tobytes(), "little")
+                if i >= n:
+                    assert bits == 0
+                    continue
+                assert bits >> i & 1 and bits & 1 and bits < (1 << (i + 1))
+                assert bin(bits).count("1") == res.depth[r, i] + 1
+                if i:
+                    pb = int.from_bytes(res.mask[r, res.parent[r, i]].astype("<u4").tobytes(), "little")
+                    assert bits == pb | (1 << i)
+                assert res.pos[r, i] == r * 7 + bin(bits).count("1") - 1
+            assert 0 <= res.accept_len[r] <= res.depth[r, :n].max()
+        assert 0.0 <= res.beta <= 1.0
+
+
+def test_alpha_nesting_frozen(orc):
+    """within a layer with fixed state, smaller alpha admits a subset (FROZEN, layer 1)."""
+    rng = np.random.default_rng(4)
+    for it in range(40):
+        cfg, cost, pool = _random_instance(orc, rng)
+        cfg.selection = orc.FROZEN
+        cfg.d = 1
+        prev = None
+        for a in (1.0, 0.9, 0.8, 0.7, 0.6, 0.5):
+            cfg.alpha = a
+            res = orc.step(cfg, cost, pool)
+            adm = set(map(tuple, np.argwhere(res.layer_cands(1)["admitted"])))
+            if prev is not None:
+                assert adm <= prev
+            prev = adm
+
+
+def test_verify_target_equals_draft_follows_top1_chain(orc):
+    """with target == draft (sigma_m = 0) the walk accepts exactly the longest chain of
+    top-1 children present in the tree (independent walk with numpy argmax)."""
+    rng = np.random.default_rng(8)
+    for it in range(60):
+        cfg, cost, pool = _random_instance(orc, rng, dtype="bf16")
+        res = orc.step(cfg, cost, pool, pool.copy())
+        for r in range(cfg.b):
+            cur, acc = 0, 0
+            while True:
+                t = int(np.argmax(synth.bf16_bits_to_f32(pool[r, cur])))
+                kids = [i for i in range(1, res.n_nodes[r]) if res.parent[r, i] == cur and res.tok[r, i] == t]
+                if not kids:
+                    break
+                cur, acc = kids[0], acc + 1
+            assert res.accept_len[r] == acc
+            assert res.bonus[r] == int(np.argmax(synth.bf16_bits_to_f32(pool[r, cur])))
+
+
+def test_replication_monotonicity(orc):
+    """SURVEY §8(c) batch structure: replicating a b = 1 instance m times (B_verify scaled by m, so
+    the per-request budget is unchanged) must not increase the mean tree size N/b, because the
+    batch-coupled marginal cost dc(N) grows with N while each request's benefit stays the same."""
+    rng = np.random.default_rng(21)
+    for it in range(20):
+        cfg, cost, _ = _random_instance(orc, rng)
+        cfg.b = 1
+        pool = synth.draft_pool(it, 1, cfg.tmax(), cfg.V, dtype="fp32", a_lo=2, a_hi=8, sigma_bg=1.0)
+        res1 = orc.step(cfg, cost, pool)
+        for m in (2, 3):
+            cfgm = orc.Config(**{**cfg.__dict__, "b": m, "B_verify": cfg.B_verify * m})
+            resm = orc.step(cfgm, cost, np.repeat(pool, m, 0))
+            assert resm.N / m <= res1.N + 1e-9
+
+
+def test_permutation_equivariance(orc):
+    """Permuting requests permutes the trees (instances without cross-request key ties)."""
+    rng = np.random.default_rng(31)
+    for it in range(30):
+        cfg, cost, pool = _random_instance(orc, rng)
+        if cfg.b < 2:
+            continue
+        perm = rng.permutation(cfg.b)
+        a = orc.step(cfg, cost, pool)
+        bb = orc.step(cfg, cost, pool[perm])
+        for i, r in enumerate(perm):
+            assert a.n_nodes[r] == bb.n_nodes[i]
+            assert (a.tok[r] == bb.tok[i]).all()
