@@ -274,7 +274,7 @@ def step(cfg: Config, cost: Cost, draft: np.ndarray, target: np.ndarray | None =
         trace=np.zeros(D * TRACE_F), summary=np.zeros(SUM_F))
     cand_i = np.zeros(D * capc * 5, np.int32) if dump else None
     cand_d = np.zeros(D * capc * 3) if dump else None
-    rt = np.ascontiguousarray(root_tok if root_tok is not None else np.zeros(b), np.int32)
+    rt = np.ascontiguousarray(root_tok if root_tok is not None else np.full(b, -1), np.int32)
     rp = np.ascontiguousarray(root_pos if root_pos is not None else np.zeros(b), np.int32)
     c_cfg, c_cost = cfg.c(), cost.c()
     rc = lib().orc_step(C.byref(c_cfg), C.byref(c_cost), _ptr(draft), ld, layer_stride,

@@ -1,0 +1,579 @@
+// api.cu — host side of the libsmart C-ABI (include/smart.h): validation, workspace,
+// launch sequencing, NCCL exchange for sharded batches, inspection.
+//
+// No torch, no oracle: this file links only the CUDA runtime (and dlopen()s libnccl.so.2 when
+// a context is attached to a multi-rank communicator).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "smart_internal.cuh"
+
+using namespace smart;
+
+struct smart_ctx {
+  smart_config cfg;
+  smart_cost cost;
+  int device = 0;
+  int num_sms = 0;
+  int grid_expand = 0, grid_verify = 0;
+  size_t select_smem = 0;
+  Params P{};
+  void* ws = nullptr;      // single device allocation
+  size_t ws_bytes = 0;
+  // host-side call order (graph-capture safe: no device reads)
+  int next_layer = 0;      // 0: no step begun
+  int phase = 0;           // 0 expect expand, 1 expect select
+  bool masked = false;
+  cudaStream_t last_stream = nullptr;
+  std::string err;
+  // NCCL
+  void* nccl_comm = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+smart_status fail(smart_ctx* c, smart_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return fail(ctx, SMART_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---- NCCL via dlopen ----
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllGather && CommDestroy && GetErrorString;
+  }
+} g_nccl;
+
+long long derive_T(const smart_config* c, int B) {
+  long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
+  long long t = 1 + std::min<long long>(B, (long long)c->max_depth * Wq);
+  return c->tree_capacity > 0 ? c->tree_capacity : t;
+}
+
+smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s, std::string& why) {
+  auto bad = [&](const char* m) {
+    why = m;
+    return SMART_EINVAL;
+  };
+  if (!c) return bad("null config");
+  if (c->vocab < 2 || c->vocab > (1 << 24)) return bad("vocab out of range [2, 2^24]");
+  if (c->top_k < 1 || c->top_k > 32 || c->top_k > c->vocab) return bad("top_k must be in [1, min(V, 32)]");
+  if (c->max_depth < 0 || c->max_depth > SMART_MAX_DEPTH) return bad("max_depth must be in [0, 16]");
+  if (c->max_frontier < 0) return bad("max_frontier must be >= 0");
+  if (c->batch_local < 1 || c->batch_global < c->batch_local) return bad("batch sizes invalid");
+  if (c->batch_offset < 0 || c->batch_offset + c->batch_local > c->batch_global) return bad("batch_offset invalid");
+  if (c->batch_global > 65535) return bad("batch_global > 65535");
+  if (c->batch_local > 4096) return bad("batch_local > 4096");
+  if (!(c->alpha > 0.0 && c->alpha <= 1.0)) return bad("alpha must be in (0, 1]");
+  if (c->bonus != 0 && c->bonus != 1) return bad("bonus must be 0 or 1");
+  if (c->selection < 0 || c->selection > 1 || c->accept_model < 0 || c->accept_model > 1 || c->marginal < 0 ||
+      c->marginal > 1 || c->cost_scope < 0 || c->cost_scope > 1 || c->logits_dtype < 0 || c->logits_dtype > 1 ||
+      c->row_mode < 0 || c->row_mode > 1)
+    return bad("enum field out of range");
+  int B = c->budget_verify / c->batch_global;
+  if (B < 1) return bad("per-request budget floor(budget_verify / batch_global) < 1");
+  if (k) {
+    if (!(k->c_T > 0)) return bad("c_T must be > 0");
+    if (k->lambda < 0 || k->gamma < 0 || k->delta < 0 || !(k->rho > 0)) return bad("cost constants out of domain");
+    if (!(k->lambda > 0 || (k->gamma > 0 && k->delta > 0))) return bad("marginal cost must be > 0 (lambda > 0 or gamma*delta > 0)");
+    if (c->bonus == 1 && k->beta + k->eta <= 0) return bad("bonus = 1 needs beta + eta > 0 (S(empty) finite)");
+  }
+  long long T = derive_T(c, B);
+  if (T < 1 || T > 1024) return bad("tree capacity T must be in [1, 1024]");
+  long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
+  long long wf = std::max<long long>(1, std::min<long long>(Wq, std::min<long long>(B, T - 1)));
+  long long cap_rows = (long long)c->batch_local * wf;
+  if (cap_rows * c->top_k > 65536ll * 8) return bad("frontier capacity too large");
+  if (wf * c->top_k > 65535) return bad("candidates per request exceed 16-bit index");
+  int esz = c->logits_dtype == SMART_BF16 ? 2 : 4;
+  int ce = kChunkBytes / esz;
+  int cpr = (c->vocab + ce - 1) / ce;
+  if (cpr > 256) return bad("vocab too large for the chunk scheduler (> 256 chunks per row)");
+  if (s) {
+    s->B = B;
+    s->T = (int)T;
+    s->mask_words = (int)((T + 31) / 32);
+    s->frontier_cap = (int)cap_rows;
+    s->chunk_elems = ce;
+  }
+  return SMART_OK;
+}
+
+int next_pow2(long long n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* smart_status_string(smart_status s) {
+  switch (s) {
+    case SMART_OK: return "ok";
+    case SMART_EINVAL: return "invalid argument";
+    case SMART_ECUDA: return "CUDA error";
+    case SMART_ENCCL: return "NCCL error";
+    case SMART_ECAPACITY: return "capacity exceeded";
+    case SMART_EDEVICE: return "device flag set (invalid logits)";
+    case SMART_ESTATE: return "call out of order";
+  }
+  return "unknown";
+}
+
+const char* smart_last_error(const smart_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+smart_status smart_query_sizes(const smart_config* cfg, smart_sizes* out) {
+  std::string why;
+  smart_status st = validate(cfg, nullptr, out, why);
+  if (st) return fail(nullptr, st, "%s", why.c_str());
+  return SMART_OK;
+}
+
+smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int device, smart_ctx** out) {
+  if (!out) return fail(nullptr, SMART_EINVAL, "null out");
+  *out = nullptr;
+  smart_sizes sz{};
+  std::string why;
+  smart_status st = validate(cfg, cost, &sz, why);
+  if (st) return fail(nullptr, st, "%s", why.c_str());
+  if (!cost) return fail(nullptr, SMART_EINVAL, "null cost");
+
+  smart_ctx* c = new smart_ctx();
+  c->cfg = *cfg;
+  c->cost = *cost;
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, SMART_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+
+  Params& P = c->P;
+  P.V = cfg->vocab;
+  P.k = cfg->top_k;
+  P.d = cfg->max_depth;
+  P.Wq = cfg->max_frontier > 0 ? cfg->max_frontier : (1 << 30);
+  P.b_loc = cfg->batch_local;
+  P.b_glob = cfg->batch_global;
+  P.b_off = cfg->batch_offset;
+  P.B = sz.B;
+  P.T = sz.T;
+  P.MW = sz.mask_words;
+  P.selection = cfg->selection;
+  P.accept_model = cfg->accept_model;
+  P.marginal = cfg->marginal;
+  P.cost_scope = cfg->cost_scope;
+  P.dtype = cfg->logits_dtype;
+  P.row_mode = cfg->row_mode;
+  P.omega = cfg->bonus;
+  P.esz = cfg->logits_dtype == SMART_BF16 ? 2 : 4;
+  P.chunk_elems = sz.chunk_elems;
+  P.cpr = (P.V + P.chunk_elems - 1) / P.chunk_elems;
+  P.cap_rows = sz.frontier_cap;
+  P.nranks = 1;
+  P.rank = 0;
+  P.alpha = cfg->alpha;
+  P.lambda = cost->lambda;
+  P.beta = cost->beta;
+  P.gamma = cost->gamma;
+  P.delta = cost->delta;
+  P.rho = cost->rho;
+  P.eta = cost->eta;
+  P.c_T = cost->c_T;
+
+  const long long b = P.b_loc, T = P.T, cap = P.cap_rows, k = P.k, cpr = P.cpr, d = std::max(P.d, 1);
+  const long long vrows = b * T;
+  const long long rd = std::max(cap, vrows);
+  // exchange sizing (used only with nranks > 1, allocated lazily in attach)
+  // workspace carve
+  struct Item {
+    void** ptr;
+    size_t bytes;
+  };
+  std::vector<Item> items;
+  auto add = [&](void* pp, size_t bytes) { items.push_back({reinterpret_cast<void**>(pp), bytes}); };
+  add(&P.n_nodes, b * 4);
+  add(&P.tok, b * T * 4);
+  add(&P.parent, b * T * 4);
+  add(&P.depth, b * T * 4);
+  add(&P.p, b * T * 4);
+  add(&P.cum, b * T * 4);
+  add(&P.path_sum, b * T * 8);
+  add(&P.E_r, b * 8);
+  add(&P.leaf_cnt, b * 4);
+  add(&P.leaf_sum, b * 8);
+  add(&P.finished, b * 4);
+  add(&P.root_pos, b * 4);
+  for (int q = 0; q < 2; ++q) {
+    add(&P.fr[q], cap * 8);
+    add(&P.fr_cnt[q], b * 4);
+    add(&P.fr_off[q], b * 4);
+    add(&P.fr_total[q], 4);
+  }
+  add(&P.ms, cap * cpr * kStreamWarps * 8);
+  add(&P.segv, cap * cpr * kStreamWarps * k * 4);
+  add(&P.segi, cap * cpr * kStreamWarps * k * 4);
+  add(&P.seglen, cap * cpr * 4);
+  add(&P.row_done, rd * 4);
+  add(&P.rowstat, cap * 8);
+  add(&P.cand, d * cap * k * sizeof(Cand));
+  add(&P.cand_b, d * cap * k * 4);
+  add(&P.cand_adm, d * cap * k * 4);
+  add(&P.cand_rs, d * cap * 8);
+  add(&P.trace, SMART_MAX_DEPTH * sizeof(DevTrace));
+  add(&P.err, 4);
+  add(&P.sum_accept, 8);
+  add(&P.E_glob, 8);
+  add(&P.N_glob, 4);
+  add(&P.vsegv, vrows * cpr * 4);
+  add(&P.vsegi, vrows * cpr * 4);
+  add(&P.vseglen, vrows * cpr * 4);
+  add(&P.vrow_arg, vrows * 4);
+  add(&P.vrow_off, (b + 1) * 4);
+  add(&P.req_done, b * 4);
+  size_t total = 0;
+  for (auto& it : items) total += (it.bytes + 255) & ~size_t(255);
+  e = cudaMalloc(&c->ws, total);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(nullptr, SMART_ECUDA, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
+  }
+  cudaMemset(c->ws, 0, total);
+  c->ws_bytes = total;
+  char* base = static_cast<char*>(c->ws);
+  for (auto& it : items) {
+    *it.ptr = base;
+    base += (it.bytes + 255) & ~size_t(255);
+  }
+  // launch geometry: persistent streaming grids sized to the SM count
+  c->grid_expand = c->num_sms * expand_occupancy();
+  c->grid_verify = c->num_sms * verify_occupancy();
+  // selection: dynamic smem = per-request ints + sort keys (single rank)
+  long long elig_cap = b * std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, T - 1)));
+  int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
+  c->select_smem = ((2 * b + 1) / 2 + 1) * 8 + (size_t)sort_cap * 8;
+  if (c->select_smem > 220 * 1024) {
+    cudaFree(c->ws);
+    delete c;
+    return fail(nullptr, SMART_ECAPACITY, "selection needs %zu B shared memory", (size_t)0);
+  }
+  e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
+  if (e != cudaSuccess) {
+    cudaFree(c->ws);
+    delete c;
+    return fail(nullptr, SMART_ECUDA, "select smem attribute: %s", cudaGetErrorString(e));
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(c->ws);
+    delete c;
+    return fail(nullptr, SMART_ECUDA, "init: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return SMART_OK;
+}
+
+smart_status smart_nccl_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(nullptr, SMART_EINVAL, "null id");
+  if (!g_nccl.load()) return fail(nullptr, SMART_ENCCL, "cannot dlopen libnccl.so.2");
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, SMART_ENCCL, "ncclGetUniqueId: %s", g_nccl.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(id_out, &id, 128);
+  return SMART_OK;
+}
+
+smart_status smart_attach_nccl(smart_ctx* c, const uint8_t id[128], int rank, int nranks) {
+  if (!c || !id) return fail(c, SMART_EINVAL, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, SMART_EINVAL, "bad rank/nranks");
+  if (c->cfg.batch_local * nranks != c->cfg.batch_global || c->cfg.batch_offset != rank * c->cfg.batch_local)
+    return fail(c, SMART_EINVAL, "sharding must be equal contiguous ranges: offset = rank * batch_local");
+  if (nranks == 1) return SMART_OK;
+  if (c->cfg.cost_scope != SMART_COST_GLOBAL) return fail(c, SMART_EINVAL, "LOCAL cost scope needs no communicator");
+  if (!g_nccl.load()) return fail(c, SMART_ENCCL, "cannot dlopen libnccl.so.2");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return fail(c, SMART_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+  c->nccl_comm = comm;
+  Params& P = c->P;
+  P.nranks = nranks;
+  P.rank = rank;
+  long long b = P.b_loc;
+  long long wf = std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, P.T - 1)));
+  P.m_cap = (int)(b * wf);
+  P.xstride = ((long long)P.m_cap * 8 + b * 8 + (b + 1) * 4 + 255) & ~255ll;
+  CUDA_TRY(c, cudaMalloc(&P.xs, P.xstride));
+  CUDA_TRY(c, cudaMalloc(&P.xr, P.xstride * nranks));
+  CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
+  int sort_cap = next_pow2((long long)P.m_cap * nranks);
+  size_t need = ((2 * b + 1) / 2 + 1) * 8 + (size_t)sort_cap * 8;
+  if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
+  c->select_smem = std::max(c->select_smem, need);
+  CUDA_TRY(c, select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024)));
+  return SMART_OK;
+}
+
+smart_status smart_destroy(smart_ctx* c) {
+  if (!c) return SMART_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->nccl_comm && g_nccl.h) g_nccl.CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
+  if (c->P.xs) cudaFree(c->P.xs);
+  if (c->P.xr) cudaFree(c->P.xr);
+  if (c->ws) cudaFree(c->ws);
+  delete c;
+  return SMART_OK;
+}
+
+smart_status smart_begin_step(smart_ctx* c, const int32_t* d_root_tok, const int32_t* d_root_pos, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int thr = 256, grid = (c->P.b_loc + thr - 1) / thr;
+  begin_step_kernel<<<grid, thr, 0, s>>>(c->P, d_root_tok, d_root_pos);
+  CUDA_TRY(c, cudaGetLastError());
+  c->next_layer = 1;
+  c->phase = 0;
+  c->masked = false;
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits, int64_t ld, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (!d_logits) return fail(c, SMART_EINVAL, "null logits");
+  if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld (%lld) < vocab (%d)", (long long)ld, c->cfg.vocab);
+  if (c->next_layer == 0) return fail(c, SMART_ESTATE, "expand before begin_step");
+  if (layer != c->next_layer || c->phase != 0 || layer > c->cfg.max_depth)
+    return fail(c, SMART_ESTATE, "expand layer %d out of order (expected %d, phase %d)", layer, c->next_layer, c->phase);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long ld_bytes = (long long)ld * c->P.esz;
+  bool aligned = ((reinterpret_cast<uintptr_t>(d_logits) & 15) == 0) && (ld_bytes % 16 == 0);
+  launch_expand(c->P, layer, d_logits, ld_bytes, aligned, c->grid_expand, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->phase = 1;
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int32_t* d_frontier_count, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (layer != c->next_layer || c->phase != 1)
+    return fail(c, SMART_ESTATE, "select layer %d out of order (expected %d after expand)", layer, c->next_layer);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P.nranks > 1) {
+    launch_select(c->P, layer, 0, c->select_smem, s);
+    CUDA_TRY(c, cudaGetLastError());
+    ncclResult_t r = g_nccl.AllGather(c->P.xs, c->P.xr, (size_t)c->P.xstride, ncclUint8,
+                                      static_cast<ncclComm_t>(c->nccl_comm), s);
+    if (r != ncclSuccess) return fail(c, SMART_ENCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
+    launch_select(c->P, layer, 1, c->select_smem, s);
+  } else {
+    launch_select(c->P, layer, 2, c->select_smem, s);
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  if (d_frontier || d_frontier_count) launch_export_frontier(c->P, layer & 1, d_frontier, d_frontier_count, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->next_layer = layer + 1;
+  c->phase = 0;
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_build_mask(smart_ctx* c, uint32_t* d_mask, int32_t* d_pos, int32_t* d_parent, int32_t* d_tok,
+                              int32_t* d_tree_len, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (c->next_layer == 0 || c->phase != 0) return fail(c, SMART_ESTATE, "build_mask needs a begun step between layers");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_mask(c->P, d_mask, d_pos, d_parent, d_tok, d_tree_len, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->masked = true;
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld, int32_t* d_accept_len,
+                                 int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (!d_target) return fail(c, SMART_EINVAL, "null target logits");
+  if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld < vocab");
+  if (!c->masked) return fail(c, SMART_ESTATE, "verify_accept must follow build_mask");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long ld_bytes = (long long)ld * c->P.esz;
+  bool aligned = ((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ld_bytes % 16 == 0);
+  launch_verify(c->P, d_target, ld_bytes, aligned, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32_t* d_root_pos, const void* d_draft,
+                            int64_t ld, const void* d_target, int64_t ld_t, uint32_t* d_mask, int32_t* d_pos,
+                            int32_t* d_parent, int32_t* d_tok, int32_t* d_tree_len, int32_t* d_accept_len,
+                            int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (c->cfg.row_mode != SMART_ROWS_NODE) return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE");
+  smart_status st = smart_begin_step(c, d_root_tok, d_root_pos, stream);
+  for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
+    st = smart_expand_step(c, l, d_draft, ld, stream);
+    if (!st) st = smart_select(c, l, nullptr, nullptr, stream);
+  }
+  if (!st) st = smart_build_mask(c, d_mask, d_pos, d_parent, d_tok, d_tree_len, stream);
+  if (!st && d_target) st = smart_verify_accept(c, d_target, ld_t, d_accept_len, d_accept_path, d_bonus, stream);
+  return st;
+}
+
+smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {
+  if (!c || !out) return fail(c, SMART_EINVAL, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
+  DevTrace tr[SMART_MAX_DEPTH];
+  int err = 0;
+  unsigned long long acc = 0;
+  double E = 0;
+  int N = 0;
+  CUDA_TRY(c, cudaMemcpy(tr, c->P.trace, sizeof tr, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(&err, c->P.err, 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(&acc, c->P.sum_accept, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(&E, c->P.E_glob, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(&N, c->P.N_glob, 4, cudaMemcpyDeviceToHost));
+  std::vector<int> nn(c->P.b_loc);
+  CUDA_TRY(c, cudaMemcpy(nn.data(), c->P.n_nodes, 4 * nn.size(), cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  out->error_flags = err;
+  out->accepted_local = (int64_t)acc;
+  long long nodes = 0;
+  for (int v : nn) nodes += v - 1;
+  out->nodes_local = nodes;
+  out->E_global = E;
+  int le = 0;
+  for (int l = 0; l < SMART_MAX_DEPTH; ++l) {
+    smart_layer_trace& t = out->layer[l];
+    t.executed = tr[l].executed;
+    t.n_rows = tr[l].n_rows;
+    t.n_cand = tr[l].n_cand;
+    t.n_elig = tr[l].n_elig;
+    t.n_admit = tr[l].n_admit;
+    t.argmax_j = tr[l].argmax_j;
+    t.N0 = tr[l].N0;
+    t.saturated = tr[l].saturated;
+    t.E0 = tr[l].E0;
+    t.S0 = tr[l].S0;
+    t.S_after = tr[l].S_after;
+    t.dc0 = tr[l].dc0;
+    if (t.executed) {
+      le = l + 1;
+      out->S_final = t.S_after;
+    }
+  }
+  out->layers_executed = le;
+  if (le == 0) {
+    // no layer ran: S of the root-only batch
+    int bc = c->cfg.cost_scope == SMART_COST_LOCAL ? c->P.b_loc : c->P.b_glob;
+    double C = c->cost.lambda * 0 + c->cost.beta + c->cost.eta;
+    out->S_final = C > 0 ? c->cost.c_T * (c->P.omega * bc) / (bc * C) : 0.0;
+  }
+  if (err & (kErrDraftNaN | kErrTargetNaN)) return fail(c, SMART_EDEVICE, "invalid logits (NaN/+inf) seen (flags %d)", err);
+  return SMART_OK;
+}
+
+smart_status smart_get_tree(smart_ctx* c, int32_t* n_nodes, int32_t* tok, int32_t* parent, int32_t* depth, float* p,
+                            float* cum) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
+  size_t bt = (size_t)c->P.b_loc * c->P.T;
+  if (n_nodes) CUDA_TRY(c, cudaMemcpy(n_nodes, c->P.n_nodes, 4 * c->P.b_loc, cudaMemcpyDeviceToHost));
+  if (tok) CUDA_TRY(c, cudaMemcpy(tok, c->P.tok, 4 * bt, cudaMemcpyDeviceToHost));
+  if (parent) CUDA_TRY(c, cudaMemcpy(parent, c->P.parent, 4 * bt, cudaMemcpyDeviceToHost));
+  if (depth) CUDA_TRY(c, cudaMemcpy(depth, c->P.depth, 4 * bt, cudaMemcpyDeviceToHost));
+  if (p) CUDA_TRY(c, cudaMemcpy(p, c->P.p, 4 * bt, cudaMemcpyDeviceToHost));
+  if (cum) CUDA_TRY(c, cudaMemcpy(cum, c->P.cum, 4 * bt, cudaMemcpyDeviceToHost));
+  return SMART_OK;
+}
+
+smart_status smart_get_candidates(smart_ctx* c, int32_t layer, int64_t cap, int32_t* count, int32_t* ints,
+                                  float* floats, int32_t* admitted) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (layer < 1 || layer > std::max(c->cfg.max_depth, 1)) return fail(c, SMART_EINVAL, "layer out of range");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
+  DevTrace tr;
+  CUDA_TRY(c, cudaMemcpy(&tr, c->P.trace + (layer - 1), sizeof tr, cudaMemcpyDeviceToHost));
+  int rows = tr.executed ? tr.n_rows : 0;
+  const int k = c->P.k;
+  long long n = (long long)rows * k;
+  if (count) *count = (int32_t)n;
+  if (n > cap) return fail(c, SMART_EINVAL, "cap %lld < %lld candidates", (long long)cap, n);
+  if (n == 0) return SMART_OK;
+  size_t lb = (size_t)(layer - 1) * c->P.cap_rows * k;
+  std::vector<Cand> cd(n);
+  std::vector<float> bb(n);
+  std::vector<int> adm(n);
+  CUDA_TRY(c, cudaMemcpy(cd.data(), c->P.cand + lb, n * sizeof(Cand), cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(bb.data(), c->P.cand_b + lb, n * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(adm.data(), c->P.cand_adm + lb, n * 4, cudaMemcpyDeviceToHost));
+  std::vector<int2> rs(rows);
+  CUDA_TRY(c, cudaMemcpy(rs.data(), c->P.cand_rs + (size_t)(layer - 1) * c->P.cap_rows, rows * sizeof(int2),
+                         cudaMemcpyDeviceToHost));
+  for (long long q = 0; q < n; ++q) {
+    const int2 e = rs[q / k];
+    if (ints) {
+      ints[q * 4 + 0] = e.x;
+      ints[q * 4 + 1] = cd[q].parent;
+      ints[q * 4 + 2] = cd[q].tok;
+      ints[q * 4 + 3] = e.y * k + (int)(q % k);
+    }
+    if (floats) {
+      floats[q * 3 + 0] = cd[q].p;
+      floats[q * 3 + 1] = cd[q].cum;
+      floats[q * 3 + 2] = bb[q];
+    }
+    if (admitted) admitted[q] = adm[q];
+  }
+  return SMART_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+// smart_internal.cuh — device-side layout and helpers of libsmart (B200, sm_100a).
+//
+// Everything here is product code; it shares nothing with oracle/ (the fp64 test oracle).
+// Citations: P:n = PAPER.md line n (arXiv 2604.09731); Q# = DESIGN.md §3 reading.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "smart.h"
+
+namespace smart {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kChunkBytes = 16384;       // streamed unit of a logit row (16 KiB)
+constexpr int kStreamThreads = 256;      // CTA size of the streaming kernels (8 warps)
+constexpr int kStreamWarps = kStreamThreads / kWarp;
+constexpr int kVecPerThread = kChunkBytes / 16 / kStreamThreads;  // 4 x 16 B per thread
+constexpr int kWarpBuf = 64;             // per-warp candidate staging (top-k filter)
+constexpr int kSelectThreads = 1024;     // single-CTA selection kernel
+constexpr int kMaxK = 32;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kIdxSentinel = 0x7fffffff;
+
+// error flag bits (smart_stats.error_flags)
+constexpr int kErrDraftNaN = 1;
+constexpr int kErrTargetNaN = 2;
+constexpr int kErrSaturated = 4;
+
+// one candidate produced by A1/A2 for (frontier row, rank j)
+struct Cand {
+  int32_t tok;
+  float p;
+  float cum;
+  int32_t parent;  // node index of the expanded frontier node
+};
+
+// device copy of one layer's trace (same fields as smart_layer_trace)
+struct DevTrace {
+  int32_t executed, n_rows, n_cand, n_elig, n_admit, argmax_j, N0, saturated;
+  double E0, S0, S_after, dc0;
+};
+
+// Everything a kernel needs: config scalars + workspace pointers.  Passed by value.
+struct Params {
+  // ---- config ----
+  int V, k, d, Wq, b_loc, b_glob, b_off, B, T, MW;
+  int selection, accept_model, marginal, cost_scope, dtype, row_mode, omega;
+  int esz;            // bytes per logit
+  int chunk_elems;    // elements per 16 KiB chunk
+  int cpr;            // chunks per row
+  int cap_rows;       // frontier rows per layer (local)
+  int nranks, rank;
+  double alpha, lambda, beta, gamma, delta, rho, eta, c_T;
+
+  // ---- per-request tree state [b_loc] / [b_loc*T] ----
+  int* n_nodes;       // incl. root
+  int* tok;
+  int* parent;
+  int* depth;
+  float* p;
+  float* cum;
+  double* path_sum;   // PATH_MEAN: sum of cum on root->node path
+  double* E_r;        // acceptance estimate of request r (Q11)
+  int* leaf_cnt;      // |P_r|
+  double* leaf_sum;   // sum over leaves of path_sum
+  int* finished;
+  int* root_pos;
+
+  // ---- frontier, ping-pong by layer parity ----
+  int2* fr[2];        // (local request, node)
+  int* fr_cnt[2];     // [b_loc]
+  int* fr_off[2];     // [b_loc] exclusive prefix
+  int* fr_total[2];   // [1]
+
+  // ---- A1 streaming scratch ----
+  float2* ms;         // [cap_rows*cpr*8] per (chunk, warp) softmax partial (max, sum)
+  float* segv;        // [cap_rows*cpr*8*k] per (segment start chunk, warp) top-k values
+  int* segi;          //   ... and indices
+  int* seglen;        // [cap_rows*cpr] segment length in chunks (at its first chunk)
+  int* row_done;      // [max(cap_rows, b_loc*T)] arrival counters (self-resetting)
+  float2* rowstat;    // [cap_rows] (M, Z) of the last expanded layer
+  Cand* cand;         // [d][cap_rows*k]
+  float* cand_b;      // [d][cap_rows*k] benefit
+  int* cand_adm;      // [d][cap_rows*k] admitted flag
+  int2* cand_rs;      // [d][cap_rows] (local request, frontier slot) of each candidate row
+
+  // ---- select / stats ----
+  DevTrace* trace;    // [SMART_MAX_DEPTH]
+  int* err;           // [1]
+  unsigned long long* sum_accept;  // [1]
+  double* E_glob;     // [1] sum_r E_r after the last select
+  int* N_glob;        // [1]
+
+  // ---- verify scratch ----
+  float* vsegv;       // [b_loc*T*cpr]
+  int* vsegi;         // [b_loc*T*cpr]
+  int* vseglen;       // [b_loc*T*cpr]
+  int* vrow_arg;      // [b_loc*T]
+  int* vrow_off;      // [b_loc+1]
+  int* req_done;      // [b_loc]
+
+  // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----
+  // per-rank record: keys[m_cap] u64 | E_r[b_loc] f64 | hdr[b_loc] n_r, hdr[b_loc] = count
+  int m_cap;
+  long long xstride;  // bytes per rank record
+  char* xs;           // send record
+  char* xr;           // [nranks] gathered records
+};
+
+// ------------------------------------------------------------------------------------------
+// small device helpers
+// ------------------------------------------------------------------------------------------
+
+// order of A1 top-k and of the verify argmax: larger value, then lower index (Q9)
+__device__ __forceinline__ bool better(float av, int ai, float bv, int bi) {
+  return av > bv || (av == bv && ai < bi);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t float_orderable(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---- cost model (fp64; Eqs.(4),(5),(15); clamp Q17) ----
+__device__ __forceinline__ double cost_spec(const Params& P, double N, int* sat) {
+  double a = P.delta * pow(N, P.rho);
+  if (a > 700.0) { a = 700.0; *sat = 1; }
+  return P.lambda * N + P.beta + P.gamma * (exp(a) - 1.0) + P.eta;
+}
+__device__ __forceinline__ double marginal_cost(const Params& P, long long N, int* sat) {
+  if (P.marginal == SMART_DIFFERENCE) return cost_spec(P, (double)(N + 1), sat) - cost_spec(P, (double)N, sat);
+  double M = (double)(N < 1 ? 1 : N);
+  double a = P.delta * pow(M, P.rho);
+  if (a > 700.0) { a = 700.0; *sat = 1; }
+  return P.lambda + P.gamma * P.delta * P.rho * pow(M, P.rho - 1.0) * exp(a);
+}
+// b * S: c_T*(omega*b + E)/cost(N); 0/0 := 0 (Q4)
+__device__ __forceinline__ double speed_b(const Params& P, double E, long long N, int b, int* sat) {
+  double C = cost_spec(P, (double)N, sat);
+  if (C <= 0.0) return 0.0;
+  return P.c_T * ((double)P.omega * b + E) / C;
+}
+
+// ---- kernels (host launchers in api.cu) ----
+__global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32_t* root_pos);
+void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool aligned,
+                   int grid, cudaStream_t s);
+int expand_occupancy();
+void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
+size_t select_smem_bytes(int sort_cap);
+cudaError_t select_set_smem(size_t bytes);
+void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok,
+                 int32_t* tree_len, cudaStream_t s);
+void launch_verify(const Params& P, const void* target, long long ld_bytes, bool aligned,
+                   int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s);
+int verify_occupancy();
+void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
+                            cudaStream_t s);
+
+}  // namespace smart

@@ -1,0 +1,171 @@
+"""Shared helpers of the GPU parity tests: run one decode step through the C-ABI (libsmart)
+and through the fp64 oracle on the SAME seeded inputs, then compare.
+
+Test infrastructure only.  Inputs come from inputs/synth.py (no method arithmetic); expected
+values come from oracle/ only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from inputs import synth
+
+REL_TOL = 1e-5  # north_star: 1e-5 relative on fp32 scores and speedup values
+
+
+@dataclass
+class Case:
+    V: int
+    k: int
+    d: int
+    W: int
+    b: int
+    B_verify: int
+    alpha: float = 0.8
+    omega: int = 1
+    selection: int = 0
+    accept_model: int = 0
+    marginal: int = 0
+    dtype: str = "bf16"
+    cost: tuple = (0.02, 0.0, 0.05, 0.01, 1.2, 1.0, 1.0)  # lam, beta, gamma, delta, rho, eta, c_T
+    seed: int = 0
+    sigma_m: float = 1.0
+    a_lo: float = 10.0
+    a_hi: float = 18.0
+    sigma_bg: float = 2.0
+    ld_pad: int = 0
+
+
+def make_inputs(case: Case, T: int):
+    ld = case.V + case.ld_pad
+    draft = synth.draft_pool(case.seed, case.b, T, case.V, ld=ld, dtype=case.dtype, a_lo=case.a_lo,
+                             a_hi=case.a_hi, sigma_bg=case.sigma_bg)
+    target = synth.target_pool(draft, case.seed + 1000, case.sigma_m, V=case.V)
+    rng = np.random.default_rng(case.seed)
+    root_tok = rng.integers(0, case.V, case.b).astype(np.int32)
+    root_pos = rng.integers(0, 4000, case.b).astype(np.int32)
+    return draft, target, root_tok, root_pos
+
+
+def run_oracle(case: Case, draft, target, root_tok, root_pos):
+    from oracle import oracle as O
+    lam, beta, gamma, delta, rho, eta, c_T = case.cost
+    cfg = O.Config(V=case.V, k=case.k, d=case.d, W=case.W, b=case.b, B_verify=case.B_verify,
+                   alpha=case.alpha, omega=case.omega, selection=case.selection,
+                   accept_model=case.accept_model, marginal=case.marginal,
+                   dtype=O.BF16 if case.dtype == "bf16" else O.FP32)
+    cost = O.Cost(lam=lam, beta=beta, gamma=gamma, delta=delta, rho=rho, eta=eta, c_T=c_T)
+    # the oracle reads rows [0, V) of each padded row (ld = last axis)
+    return O.step(cfg, cost, draft, target, root_tok=root_tok, root_pos=root_pos)
+
+
+def gpu_ctx(case: Case, row_mode=None):
+    from paper_2604_09731_b200 import smart as S
+    lam, beta, gamma, delta, rho, eta, c_T = case.cost
+    cfg = S.Config(vocab=case.V, top_k=case.k, max_depth=case.d, max_frontier=case.W,
+                   batch_local=case.b, budget_verify=case.B_verify, alpha=case.alpha, bonus=case.omega,
+                   selection=case.selection, accept_model=case.accept_model, marginal=case.marginal,
+                   logits_dtype=S.BF16 if case.dtype == "bf16" else S.FP32,
+                   row_mode=S.ROWS_NODE if row_mode is None else row_mode)
+    cost = S.Cost(lam=lam, beta=beta, gamma=gamma, delta=delta, rho=rho, eta=eta, c_T=c_T)
+    return S.Smart(cfg, cost, 0)
+
+
+def to_dev(a):
+    import torch
+    if a.dtype == np.uint16:
+        return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).cuda()
+    return torch.from_numpy(a).cuda()
+
+
+def run_gpu(case: Case, draft, target, root_tok, root_pos, use_run_step=False):
+    import torch
+    ctx = gpu_ctx(case)
+    dd, tt = to_dev(draft), to_dev(target)
+    rt, rp = to_dev(root_tok), to_dev(root_pos)
+    out = ctx.alloc_outputs()
+    if use_run_step:
+        ctx.run_step(dd, tt, out, root_tok=rt, root_pos=rp)
+    else:
+        ctx.begin_step(rt, rp)
+        for l in range(1, case.d + 1):
+            ctx.expand_step(l, dd)
+            ctx.select(l)
+        ctx.build_mask(out["mask"], out["pos"], out["parent"], out["tok"], out["tree_len"])
+        ctx.verify_accept(tt, out["accept_len"], out["accept_path"], out["bonus"])
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    res["stats"] = ctx.stats()
+    res["tree"] = ctx.tree()
+    res["cands"] = {l: ctx.candidates(l) for l in range(1, case.d + 1)
+                    if res["stats"]["layers"][l - 1]["executed"]}
+    res["ctx"] = ctx
+    return res
+
+
+def compare(case: Case, orc, gpu, check_scores=True):
+    """Assert parity.  Returns the number of layers compared (all, unless the oracle flags a
+    tie-ambiguous decision (Q24), in which case layers >= that one are not compared)."""
+    amb = orc.first_ambiguous_layer
+    L = case.d if amb == 0 else amb - 1
+    b, T = case.b, orc.T
+    st = gpu["stats"]
+    assert st["error_flags"] & 3 == 0, st["error_flags"]
+    # per-layer decisions
+    for l in range(1, L + 1):
+        tr = orc.trace[l - 1]
+        g = st["layers"][l - 1]
+        assert g["executed"] == int(tr[12]), (l, g, tr)
+        if not g["executed"]:
+            continue
+        assert g["n_rows"] == int(tr[0]) and g["n_elig"] == int(tr[2]), (l, g, tr)
+        assert g["n_admit"] == int(tr[3]), (l, g["n_admit"], tr[3])
+        assert g["N0"] == int(tr[4])
+        if check_scores:
+            np.testing.assert_allclose(g["E0"], tr[5], rtol=REL_TOL, atol=1e-9)
+            np.testing.assert_allclose(g["S0"], tr[6], rtol=REL_TOL, atol=1e-12)
+            np.testing.assert_allclose(g["S_after"], tr[7], rtol=REL_TOL, atol=1e-12)
+            np.testing.assert_allclose(g["dc0"], tr[9], rtol=1e-12)
+        # candidates: tokens/parents/c exact, p/cum/b within tolerance, admitted exact
+        oc = orc.layer_cands(l)
+        gc = gpu["cands"][l]
+        assert len(gc["tok"]) == len(oc["tok"])
+        np.testing.assert_array_equal(gc["r"], oc["r"])
+        np.testing.assert_array_equal(gc["parent"], oc["parent"])
+        np.testing.assert_array_equal(gc["tok"], oc["tok"])
+        np.testing.assert_array_equal(gc["c"], oc["c"])
+        np.testing.assert_array_equal(gc["admitted"], oc["admitted"])
+        if check_scores:
+            np.testing.assert_allclose(gc["p"], oc["p"], rtol=REL_TOL, atol=1e-30)
+            np.testing.assert_allclose(gc["cum"], oc["cum"], rtol=REL_TOL, atol=1e-30)
+            np.testing.assert_allclose(gc["b"], oc["b"], rtol=REL_TOL, atol=1e-30)
+    tree = gpu["tree"]
+    for r in range(b):
+        # nodes of depth <= L are decided by compared layers
+        on = orc.n_nodes[r]
+        gm = tree["depth"][r, : tree["n_nodes"][r]] <= L
+        om = orc.depth[r, :on] <= L
+        gi = np.nonzero(gm)[0]
+        oi = np.nonzero(om)[0]
+        assert len(gi) == len(oi), (r, gi, oi)
+        np.testing.assert_array_equal(tree["tok"][r, gi], orc.tok[r, oi])
+        np.testing.assert_array_equal(tree["parent"][r, gi], orc.parent[r, oi])
+        if check_scores:
+            np.testing.assert_allclose(tree["cum"][r, gi], orc.cum[r, oi], rtol=REL_TOL)
+    if amb == 0:
+        # whole step: masks, positions, parents, tokens, tree_len, verify — bit-exact
+        np.testing.assert_array_equal(gpu["tree_len"], orc.n_nodes)
+        np.testing.assert_array_equal(gpu["mask"].view(np.uint32), orc.mask)
+        np.testing.assert_array_equal(gpu["pos"], orc.pos)
+        np.testing.assert_array_equal(gpu["parent"], orc.parent)
+        np.testing.assert_array_equal(gpu["tok"], orc.tok)
+        np.testing.assert_array_equal(gpu["accept_len"], orc.accept_len)
+        np.testing.assert_array_equal(gpu["accept_path"], orc.accept_path)
+        np.testing.assert_array_equal(gpu["bonus"], orc.bonus)
+        assert st["accepted_local"] == int(orc.summary[3])
+        if check_scores:
+            np.testing.assert_allclose(st["S_final"], orc.S, rtol=REL_TOL)
+            np.testing.assert_allclose(st["E_global"], orc.E, rtol=REL_TOL)
+    return L

@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle, element by element,
+on the same seeded inputs.  Bit-exact on node sets, tokens, parents, masks,
+positions, accept lengths/paths and bonus tokens; 1e-5 relative on p, cum, b, E and S.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from smart_gpu_cases import Case, compare, make_inputs, run_gpu, run_oracle, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_09731_b200 import _build
+    _build.build()
+    from oracle import oracle as O
+    O.build()
+
+
+def _T(case):
+    from oracle import oracle as O
+    return O.Config(V=case.V, k=case.k, d=case.d, W=case.W, b=case.b, B_verify=case.B_verify).tmax()
+
+
+def _run(case, **kw):
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    orc = run_oracle(case, draft, target, rt, rp)
+    gpu = run_gpu(case, draft, target, rt, rp, **kw)
+    return orc, gpu, compare(case, orc, gpu)
+
+
+# ---- the toy worked example (cfg1) ----------------------------------------------------------
+
+def test_toy_cfg1_gpu():
+    """SURVEY §8(c) toy: GPU reproduces the hand-traced HOTPATH/PAPER trees and the walk."""
+    import torch
+    from smart_toy import toy_pool, toy_target
+    from paper_2604_09731_b200 import smart as S
+    toy = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "toy_cfg1.json")))
+    for preset in ("hotpath", "paper", "budget3"):
+        P = toy["hotpath"] if preset != "paper" else toy["paper"]
+        B_verify = toy["hotpath_budget3"]["B_verify"] if preset == "budget3" else P["B_verify"]
+        hot = preset != "paper"
+        cfg = S.Config(vocab=32, top_k=2, max_depth=3, max_frontier=0, batch_local=1, budget_verify=B_verify,
+                       alpha=P["alpha"], bonus=1 if hot else 0, selection=S.PREFIX if hot else S.FROZEN,
+                       accept_model=S.NODE_SUM if hot else S.PATH_MEAN, logits_dtype=S.FP32)
+        cost = S.Cost(lam=1.0, eta=10.0 if hot else 0.0, c_T=10.0)
+        ctx = S.Smart(cfg, cost)
+        T = ctx.sizes["T"]
+        draft = to_dev(toy_pool(toy, T))
+        target = to_dev(toy_target(toy, T))
+        out = ctx.alloc_outputs()
+        ctx.run_step(draft, target, out, root_tok=torch.tensor([-1], dtype=torch.int32, device="cuda"),
+                     root_pos=torch.tensor([100], dtype=torch.int32, device="cuda"))
+        torch.cuda.synchronize()
+        n = int(out["tree_len"][0])
+        want = toy["hotpath"] if preset == "hotpath" else (toy["hotpath_budget3"] if preset == "budget3" else toy["paper"])
+        assert out["tok"][0, :n].tolist() == want["tokens"], preset
+        assert out["parent"][0, :n].tolist() == want["parent"], preset
+        st = ctx.stats()
+        if preset == "hotpath":
+            assert out["mask"][0, :n, 0].tolist() == want["mask_words"]
+            assert out["pos"][0, :n].tolist() == [100 + d for d in want["depth"]]
+            assert [st["layers"][l]["n_admit"] for l in range(3)] == want["layer_admits"]
+            np.testing.assert_allclose([st["layers"][l]["S_after"] for l in range(3)], want["layer_S_after"], rtol=1e-5)
+            assert st["layers"][1]["argmax_j"] == want["layer2_argmax_j"]
+            np.testing.assert_allclose(st["S_final"], want["S"], rtol=1e-5)
+            v = toy["verify"]
+            assert int(out["accept_len"][0]) == v["accept_len"]
+            assert out["accept_path"][0, :2].tolist() == v["accept_path"]
+            assert int(out["bonus"][0]) == v["bonus"]
+        if preset == "paper":
+            np.testing.assert_allclose(st["S_final"], want["S"], rtol=1e-5)
+
+
+# ---- small random cases: several chunks, ragged tails, every preset ------------------------
+
+SMALL = []
+for seed in range(12):
+    rng = np.random.default_rng(seed)
+    SMALL.append(Case(V=int(rng.choice([1000, 20000, 40001, 70000])), k=int(rng.integers(2, 11)),
+                      d=int(rng.integers(1, 7)), W=int(rng.choice([0, 4, 8])), b=int(rng.integers(1, 9)),
+                      B_verify=int(rng.integers(8, 120)), alpha=float(rng.choice([0.5, 0.8, 1.0])),
+                      omega=int(seed % 2), selection=int(rng.integers(0, 2)), accept_model=int(rng.integers(0, 2)),
+                      marginal=int(rng.integers(0, 2)), dtype=["bf16", "fp32"][seed % 2], seed=seed,
+                      cost=(float(rng.uniform(0.01, 0.1)), 0.0, float(rng.uniform(0.0, 0.2)),
+                            float(rng.uniform(0.001, 0.05)), float(rng.uniform(0.9, 1.4)),
+                            1.0 if seed % 2 else 0.0, 1.0), sigma_m=0.5, a_lo=4.0, a_hi=12.0))
+
+
+@pytest.mark.parametrize("case", SMALL, ids=[f"small{i}" for i in range(len(SMALL))])
+def test_small_random(case):
+    _run(case)
+
+
+def test_run_step_equals_separate_calls():
+    case = Case(V=50000, k=6, d=5, W=6, b=5, B_verify=60, seed=3)
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    a = run_gpu(case, draft, target, rt, rp)
+    b = run_gpu(case, draft, target, rt, rp, use_run_step=True)
+    for key in ("mask", "pos", "parent", "tok", "tree_len", "accept_len", "accept_path", "bonus"):
+        np.testing.assert_array_equal(a[key], b[key])
+
+
+# ---- BASELINE.json configs at full size ------------------------------------------------------
+
+FULL = {
+    # cfg2: Llama-3.1-8B-shaped, b=1, d=6, k=10, EAGLE-style W=10, B_verify=60
+    "cfg2_llama8b_b1": Case(V=128256, k=10, d=6, W=10, b=1, B_verify=60, seed=11,
+                            cost=(0.0117, 0.0, 0.0, 0.0, 1.0, 2.4631, 2.4631)),
+    # cfg3: Llama-3.1-8B-shaped compute-bound regime, b=32, d=6, k=8, B_verify=200
+    "cfg3_llama8b_b32": Case(V=128256, k=8, d=6, W=8, b=32, B_verify=200, seed=12,
+                             cost=(0.0117, 0.0, 0.05, 0.02, 1.3, 2.4631, 2.4631)),
+    # cfg4: Qwen2-VL-7B-shaped MSD-style, b=12, d=8, k=10
+    "cfg4_qwen2vl_b12": Case(V=152064, k=10, d=8, W=10, b=12, B_verify=200, seed=13,
+                             cost=(0.0105, 0.0, 0.04, 0.02, 1.3, 2.20, 2.20)),
+}
+
+
+@pytest.mark.parametrize("name", list(FULL))
+def test_full_size_configs(name):
+    _run(FULL[name])
+
+
+def test_full_size_fp32_logits():
+    c = FULL["cfg3_llama8b_b32"]
+    _run(Case(**{**c.__dict__, "dtype": "fp32", "b": 8, "seed": 21}))
+
+
+# ---- edge cases ----------------------------------------------------------------------------
+
+def test_unaligned_rows_scalar_path():
+    """ld*esz not a multiple of 16 -> the scalar (non-vector) load path."""
+    _run(Case(V=9999, k=5, d=4, W=5, b=3, B_verify=30, dtype="bf16", ld_pad=3, seed=5))
+    _run(Case(V=9999, k=5, d=4, W=5, b=3, B_verify=30, dtype="fp32", ld_pad=1, seed=6))
+
+
+def test_tiny_vocab_single_chunk():
+    _run(Case(V=37, k=3, d=4, W=0, b=2, B_verify=20, dtype="fp32", seed=7, a_lo=1, a_hi=3, sigma_bg=1.0))
+
+
+def test_depth_zero_and_budget_one():
+    _run(Case(V=3000, k=4, d=0, W=4, b=2, B_verify=8, seed=8))
+    _run(Case(V=3000, k=4, d=5, W=4, b=4, B_verify=4, seed=9))   # B = 1
+
+
+def test_edge_rows_ties_and_neg_inf():
+    """all-equal rows, -inf entries, k-th/(k+1)-th ties: exact top-k order (Q9, Q23)."""
+    import torch
+    from inputs import synth
+    from oracle import oracle as O
+    for kind in ("all_equal", "neg_inf", "kth_tie"):
+        V, k = 20000, 6
+        case = Case(V=V, k=k, d=3, W=0, b=2, B_verify=40, dtype="bf16", seed=1)
+        T = _T(case)
+        draft, target, rt, rp = make_inputs(case, T)
+        row = synth.f32_to_bf16_bits(synth.edge_rows(kind, V, k, seed=3))
+        draft[:, :, :] = row[None, None, :]
+        orc = run_oracle(case, draft, target, rt, rp)
+        gpu = run_gpu(case, draft, target, rt, rp)
+        compare(case, orc, gpu)
+
+
+def test_nan_row_sets_device_flag():
+    from inputs import synth
+    from paper_2604_09731_b200 import smart as S
+    case = Case(V=5000, k=4, d=2, W=4, b=2, B_verify=20, seed=2)
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    draft[1, 0, :] = synth.f32_to_bf16_bits(synth.edge_rows("nan", 5000, 4))
+    gpu = run_gpu(case, draft, target, rt, rp)
+    assert gpu["stats"]["error_flags"] & 1
+    with pytest.raises(S.SmartError) as e:
+        gpu["ctx"].stats(raise_on_device_flag=True)
+    assert e.value.status == S.EDEVICE
+    with pytest.raises(ValueError):
+        run_oracle(case, draft, target, rt, rp)
+
+
+def test_frontier_row_mode_matches_node_mode():
+    """ROWS_FRONTIER (what a real draft forward produces) gives the same tree as ROWS_NODE."""
+    import torch
+    from paper_2604_09731_b200 import smart as S
+    from smart_gpu_cases import gpu_ctx
+    case = Case(V=30000, k=5, d=5, W=5, b=4, B_verify=60, seed=4)
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    ref = run_gpu(case, draft, target, rt, rp)
+    ctx = gpu_ctx(case, row_mode=S.ROWS_FRONTIER)
+    dd = to_dev(draft)
+    cap = ctx.sizes["frontier_cap"]
+    fr = torch.zeros((cap, 2), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    ctx.begin_step(to_dev(rt), to_dev(rp))
+    rows = dd[:, 0, :].contiguous()  # layer 1: the roots, one row per request
+    for l in range(1, case.d + 1):
+        ctx.expand_step(l, rows)
+        ctx.select(l, fr, cnt)
+        n = int(cnt.item())
+        if n == 0:
+            break
+        f = fr[:n].long()
+        rows = dd[f[:, 0], f[:, 1], :].contiguous()  # the "draft forward" over the frontier
+    out = ctx.alloc_outputs()
+    ctx.build_mask(out["mask"], out["pos"], out["parent"], out["tok"], out["tree_len"])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["tok"].cpu().numpy(), ref["tok"])
+    np.testing.assert_array_equal(out["parent"].cpu().numpy(), ref["parent"])
+    np.testing.assert_array_equal(out["mask"].cpu().numpy(), ref["mask"])
+
+
+def test_verify_draft_equals_target_accepts_top1_chain():
+    """sigma_m = 0 (target == draft): the walk accepts the longest top-1 chain."""
+    case = Case(V=40000, k=4, d=6, W=4, b=6, B_verify=120, seed=10, sigma_m=0.0)
+    orc, gpu, _ = _run(case)
+    assert gpu["accept_len"].sum() > 0
+
+
+def test_step_is_repeatable_and_graph_capturable():
+    """Same inputs -> bit-identical outputs; the step replays from a captured CUDA graph."""
+    import torch
+    case = FULL["cfg3_llama8b_b32"]
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    from smart_gpu_cases import gpu_ctx
+    ctx = gpu_ctx(case)
+    dd, tt, rtd, rpd = to_dev(draft), to_dev(target), to_dev(rt), to_dev(rp)
+    out = ctx.alloc_outputs()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.run_step(dd, tt, out, root_tok=rtd, root_pos=rpd, stream=s)
+    s.synchronize()
+    ref = {k: v.clone() for k, v in out.items()}
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.run_step(dd, tt, out, root_tok=rtd, root_pos=rpd, stream=s)
+    for _ in range(3):
+        for v in out.values():
+            v.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for k in ref:
+            assert torch.equal(ref[k], out[k]), k

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from inputs import synth
+from smart_toy import toy_pool, toy_target
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "toy_cfg1.json")
 
@@ -17,25 +18,6 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden", "toy_cfg1.json")
 def toy():
     with open(GOLD) as f:
         return json.load(f)
-
-
-def toy_pool(toy, T):
-    V = toy["V"]
-    rows = {name: synth.logits_from_probs(V, {int(t): p for t, p in spec.items()})
-            for name, spec in toy["rows"].items()}
-    pool = np.stack([rows[toy["node_rows"][min(i, len(toy["node_rows"]) - 1)]] for i in range(T)])
-    return pool[None].astype(np.float32)
-
-
-def toy_target(toy, T, tok_fill=0):
-    V = toy["V"]
-    tg = np.zeros((1, T, V), np.float32)
-    for node, t in toy["verify"]["argmax"].items():
-        tg[0, int(node), t] = 5.0
-    for i in range(T):
-        if str(i) not in toy["verify"]["argmax"]:
-            tg[0, i, 31] = 5.0  # a token that is never drafted
-    return tg
 
 
 def run_toy(orc, toy, preset, **over):
