@@ -29,7 +29,8 @@ def _stale(target, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
-    headers = [os.path.join(CSRC, "smart_internal.cuh"), os.path.join(ROOT, "include", "smart.h")]
+    headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
+    headers.append(os.path.join(ROOT, "include", "smart.h"))
     objs = []
     for s in SOURCES:
         src = os.path.join(CSRC, s)

@@ -6,13 +6,15 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
 
-#include "smart_internal.cuh"
+#include "stream.cuh"
 
 using namespace smart;
 
@@ -23,6 +25,8 @@ struct smart_ctx {
   int num_sms = 0;
   int grid_expand = 0, grid_verify = 0;
   size_t select_smem = 0;
+  bool fused_select = true;  // selection runs in the layer kernel's last CTA
+  double* cost_dev = nullptr;
   Params P{};
   void* ws = nullptr;      // single device allocation
   size_t ws_bytes = 0;
@@ -124,7 +128,7 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
   int esz = c->logits_dtype == SMART_BF16 ? 2 : 4;
   int ce = kChunkBytes / esz;
   int cpr = (c->vocab + ce - 1) / ce;
-  if (cpr > 256) return bad("vocab too large for the chunk scheduler (> 256 chunks per row)");
+  if (cpr > kMaxCpr) return bad("vocab too large for the chunk scheduler (> 64 chunks of 16 KiB per row)");
   if (s) {
     s->B = B;
     s->T = (int)T;
@@ -250,10 +254,10 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     add(&P.fr_total[q], 4);
   }
   add(&P.ms, cap * cpr * kStreamWarps * 8);
-  add(&P.segv, cap * cpr * kStreamWarps * k * 4);
-  add(&P.segi, cap * cpr * kStreamWarps * k * 4);
+  add(&P.segkey, cap * cpr * k * 8);
   add(&P.seglen, cap * cpr * 4);
   add(&P.row_done, rd * 4);
+  add(&P.layer_done, SMART_MAX_DEPTH * 4);
   add(&P.rowstat, cap * 8);
   add(&P.cand, d * cap * k * sizeof(Cand));
   add(&P.cand_b, d * cap * k * 4);
@@ -284,18 +288,67 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     *it.ptr = base;
     base += (it.bytes + 255) & ~size_t(255);
   }
+  // cost-model tables (fp64, Eqs.(4),(5),(15)): cost(N), marginal(N), N in [0, n_cost)
+  {
+    const long long wf2 = std::max<long long>(1, std::min<long long>(P.B, T - 1));
+    const long long n_cost = (long long)P.b_glob * wf2 + 2;
+    std::vector<double> tab(2 * n_cost);
+    long long sat_from = (1ll << 62);
+    auto costf = [&](double N, bool& sat) {
+      double a = cost->delta * std::pow(N, cost->rho);
+      if (a > 700.0) { a = 700.0; sat = true; }
+      return cost->lambda * N + cost->beta + cost->gamma * (std::exp(a) - 1.0) + cost->eta;
+    };
+    for (long long N = 0; N < n_cost; ++N) {
+      bool sat = false;
+      tab[N] = costf((double)N, sat);
+      double dcv;
+      if (cfg->marginal == SMART_DIFFERENCE) {
+        dcv = costf((double)(N + 1), sat) - costf((double)N, sat);
+      } else {
+        double M = (double)(N < 1 ? 1 : N);
+        double a = cost->delta * std::pow(M, cost->rho);
+        if (a > 700.0) { a = 700.0; sat = true; }
+        dcv = cost->lambda + cost->gamma * cost->delta * cost->rho * std::pow(M, cost->rho - 1.0) * std::exp(a);
+      }
+      tab[n_cost + N] = dcv;
+      if (sat && sat_from > N) sat_from = N;
+    }
+    e = cudaMalloc(&c->cost_dev, tab.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(c->cost_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(c->ws);
+      delete c;
+      return fail(nullptr, SMART_ECUDA, "cost table: %s", cudaGetErrorString(e));
+    }
+    P.cost_tab = c->cost_dev;
+    P.dc_tab = c->cost_dev + n_cost;
+    P.n_cost = (int)n_cost;
+    P.sat_from = sat_from;
+  }
+  P.min_units = getenv("SMART_MIN_UNITS") ? atoi(getenv("SMART_MIN_UNITS")) : 2;
+  if (P.min_units < 1) P.min_units = 1;
+  if (getenv("SMART_TIMING")) {
+    e = cudaMalloc(&P.dbg, 64 * sizeof(unsigned long long));
+    if (e != cudaSuccess) P.dbg = nullptr;
+  }
   // launch geometry: persistent streaming grids sized to the SM count
   c->grid_expand = c->num_sms * expand_occupancy();
   c->grid_verify = c->num_sms * verify_occupancy();
-  // selection: dynamic smem = per-request ints + sort keys (single rank)
+  // selection: fused into the layer kernel when its scratch fits the stream ring, else the
+  // standalone 1024-thread select kernel
   long long elig_cap = b * std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, T - 1)));
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
-  c->select_smem = ((2 * b + 1) / 2 + 1) * 8 + (size_t)sort_cap * 8;
+  P.sort_cap = sort_cap;
+  c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1);
+  c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes;
   if (c->select_smem > 220 * 1024) {
     cudaFree(c->ws);
+    cudaFree(c->cost_dev);
     delete c;
-    return fail(nullptr, SMART_ECAPACITY, "selection needs %zu B shared memory", (size_t)0);
+    return fail(nullptr, SMART_ECAPACITY, "selection needs more than 220 KiB of shared memory");
   }
+  mask_set_smem();
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {
     cudaFree(c->ws);
@@ -344,14 +397,16 @@ smart_status smart_attach_nccl(smart_ctx* c, const uint8_t id[128], int rank, in
   long long b = P.b_loc;
   long long wf = std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, P.T - 1)));
   P.m_cap = (int)(b * wf);
-  P.xstride = ((long long)P.m_cap * 8 + b * 8 + (b + 1) * 4 + 255) & ~255ll;
+  P.xstride = ((long long)P.m_cap * 8 + b * 8 + (b + 2) * 4 + 255) & ~255ll;
   CUDA_TRY(c, cudaMalloc(&P.xs, P.xstride));
   CUDA_TRY(c, cudaMalloc(&P.xr, P.xstride * nranks));
   CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
   int sort_cap = next_pow2((long long)P.m_cap * nranks);
-  size_t need = ((2 * b + 1) / 2 + 1) * 8 + (size_t)sort_cap * 8;
+  P.sort_cap = sort_cap;
+  size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks);
   if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
   c->select_smem = std::max(c->select_smem, need);
+  c->fused_select = false;
   CUDA_TRY(c, select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024)));
   return SMART_OK;
 }
@@ -364,6 +419,7 @@ smart_status smart_destroy(smart_ctx* c) {
   if (c->P.xs) cudaFree(c->P.xs);
   if (c->P.xr) cudaFree(c->P.xr);
   if (c->ws) cudaFree(c->ws);
+  if (c->cost_dev) cudaFree(c->cost_dev);
   delete c;
   return SMART_OK;
 }
@@ -389,9 +445,11 @@ smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits
   if (layer != c->next_layer || c->phase != 0 || layer > c->cfg.max_depth)
     return fail(c, SMART_ESTATE, "expand layer %d out of order (expected %d, phase %d)", layer, c->next_layer, c->phase);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  long long ld_bytes = (long long)ld * c->P.esz;
-  bool aligned = ((reinterpret_cast<uintptr_t>(d_logits) & 15) == 0) && (ld_bytes % 16 == 0);
-  launch_expand(c->P, layer, d_logits, ld_bytes, aligned, c->grid_expand, s);
+  const long long ld_bytes = (long long)ld * c->P.esz;
+  // TMA bulk copies need 16-byte aligned rows and 16-byte multiple row lengths
+  const bool tma = ((reinterpret_cast<uintptr_t>(d_logits) & 15) == 0) && (ld_bytes % 16 == 0) &&
+                   (((long long)c->P.V * c->P.esz) % 16 == 0);
+  launch_expand(c->P, layer, d_logits, ld_bytes, tma, c->fused_select, c->grid_expand, s);
   CUDA_TRY(c, cudaGetLastError());
   c->phase = 1;
   c->last_stream = s;
@@ -404,15 +462,15 @@ smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int3
     return fail(c, SMART_ESTATE, "select layer %d out of order (expected %d after expand)", layer, c->next_layer);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (c->P.nranks > 1) {
-    launch_select(c->P, layer, 0, c->select_smem, s);
+    launch_select(c->P, layer, 1 /* kSelLocal */, c->select_smem, s);
     CUDA_TRY(c, cudaGetLastError());
     ncclResult_t r = g_nccl.AllGather(c->P.xs, c->P.xr, (size_t)c->P.xstride, ncclUint8,
                                       static_cast<ncclComm_t>(c->nccl_comm), s);
     if (r != ncclSuccess) return fail(c, SMART_ENCCL, "ncclAllGather: %s", g_nccl.GetErrorString(r));
-    launch_select(c->P, layer, 1, c->select_smem, s);
-  } else {
-    launch_select(c->P, layer, 2, c->select_smem, s);
-  }
+    launch_select(c->P, layer, 2 /* kSelGlobal */, c->select_smem, s);
+  } else if (!c->fused_select) {
+    launch_select(c->P, layer, 0 /* kSelFull */, c->select_smem, s);
+  }  // else: already done by the layer kernel's last CTA
   CUDA_TRY(c, cudaGetLastError());
   if (d_frontier || d_frontier_count) launch_export_frontier(c->P, layer & 1, d_frontier, d_frontier_count, s);
   CUDA_TRY(c, cudaGetLastError());
@@ -441,9 +499,10 @@ smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld,
   if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld < vocab");
   if (!c->masked) return fail(c, SMART_ESTATE, "verify_accept must follow build_mask");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  long long ld_bytes = (long long)ld * c->P.esz;
-  bool aligned = ((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ld_bytes % 16 == 0);
-  launch_verify(c->P, d_target, ld_bytes, aligned, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s);
+  const long long ld_bytes = (long long)ld * c->P.esz;
+  const bool tma = ((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ld_bytes % 16 == 0) &&
+                   (((long long)c->P.V * c->P.esz) % 16 == 0);
+  launch_verify(c->P, d_target, ld_bytes, tma, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s);
   CUDA_TRY(c, cudaGetLastError());
   c->last_stream = s;
   return SMART_OK;
@@ -463,6 +522,18 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
   if (!st) st = smart_build_mask(c, d_mask, d_pos, d_parent, d_tok, d_tree_len, stream);
   if (!st && d_target) st = smart_verify_accept(c, d_target, ld_t, d_accept_len, d_accept_path, d_bonus, stream);
   return st;
+}
+
+extern "C" int smart_debug_probes(smart_ctx* c, unsigned long long* host16, int reset) {
+  if (!c || !c->P.dbg) return -1;
+  cudaStreamSynchronize(c->last_stream);
+  if (host16) cudaMemcpy(host16, c->P.dbg, 64 * 8, cudaMemcpyDeviceToHost);
+  if (reset) {
+    unsigned long long init[64];
+    for (int i = 0; i < 64; ++i) init[i] = (i == 0 || i == 8) ? ~0ull : 0ull;
+    cudaMemcpy(c->P.dbg, init, sizeof init, cudaMemcpyHostToDevice);
+  }
+  return 0;
 }
 
 smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {

@@ -6,7 +6,7 @@
 //   ties); follow the child with token t if it exists, else stop with bonus t.  All tree rows'
 //   argmaxes are streamed in one HBM pass (same persistent chunk scheduler as K1); the request
 //   whose last row completes runs the walk (one warp).
-#include "smart_internal.cuh"
+#include "stream.cuh"
 
 namespace smart {
 
@@ -16,14 +16,6 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
   return d;
-}
-
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
 }
 
 }  // namespace
@@ -63,9 +55,11 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
 
 namespace {
 
-// ---- K3: one CTA (1024 threads) for the whole local batch ----
+// ---- K3: one CTA (1024 threads = 32 warps) for the whole local batch; each warp stages one
+// request's (parent, depth, token) arrays in shared memory, then walks ancestors on chip ----
 __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, int32_t* pos, int32_t* parent,
                                                     int32_t* tok, int32_t* tree_len) {
+  extern __shared__ int s_tree[];  // [32 warps][3 * T]
   __shared__ int s_run[33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, MW = P.MW;
@@ -77,15 +71,16 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
     for (int r = b0; r < b1; ++r) local += P.n_nodes[r];
     int incl = local;
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(kFull, incl, o);
+      const int t = __shfl_up_sync(kFull, incl, o);
       if (lane >= o) incl += t;
     }
     if (lane == 31) s_run[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      int v = s_run[lane], iv = v;
+      const int v = s_run[lane];
+      int iv = v;
       for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(kFull, iv, o);
+        const int t = __shfl_up_sync(kFull, iv, o);
         if (lane >= o) iv += t;
       }
       s_run[lane] = iv - v;
@@ -99,83 +94,124 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
     }
     if (tid == 0) P.vrow_off[P.b_loc] = s_run[32];
   }
-  const int total = P.b_loc * T;
-  for (int idx = tid; idx < total; idx += 1024) {
-    const int r = idx / T, i = idx % T;
+  int* sp = s_tree + (size_t)warp * 3 * T;
+  int* sd = sp + T;
+  int* st = sd + T;
+  for (int r = warp; r < P.b_loc; r += 32) {
     const int n = P.n_nodes[r];
-    const size_t o = (size_t)r * T + i;
-    if (i < n) {
-      if (mask) {
-        for (int w = 0; w < MW; ++w) {
-          uint32_t word = 0;
-          for (int j = i; j >= 0; j = P.parent[(size_t)r * T + j])
-            if ((j >> 5) == w) word |= 1u << (j & 31);
-          mask[o * MW + w] = word;
-        }
-      }
-      if (pos) pos[o] = P.root_pos[r] + P.depth[o];
-      if (parent) parent[o] = P.parent[o];
-      if (tok) tok[o] = P.tok[o];
-    } else {
-      if (mask)
-        for (int w = 0; w < MW; ++w) mask[o * MW + w] = 0u;
-      if (pos) pos[o] = 0;
-      if (parent) parent[o] = -1;
-      if (tok) tok[o] = -1;
+    const int rp = P.root_pos[r];
+    for (int i = lane; i < n; i += 32) {
+      sp[i] = P.parent[(size_t)r * T + i];
+      sd[i] = P.depth[(size_t)r * T + i];
+      st[i] = P.tok[(size_t)r * T + i];
     }
-    if (i == 0 && tree_len) tree_len[r] = n;
+    __syncwarp();
+    for (int i = lane; i < T; i += 32) {
+      const size_t o = (size_t)r * T + i;
+      if (i < n) {
+        if (mask) {
+          for (int w = 0; w < MW; ++w) {
+            uint32_t word = 0;
+            for (int j = i; j >= 0; j = sp[j])  // ancestor-or-self chain (depth <= 16)
+              if ((j >> 5) == w) word |= 1u << (j & 31);
+            mask[o * MW + w] = word;
+          }
+        }
+        if (pos) pos[o] = rp + sd[i];
+        if (parent) parent[o] = sp[i];
+        if (tok) tok[o] = st[i];
+      } else {
+        if (mask)
+          for (int w = 0; w < MW; ++w) mask[o * MW + w] = 0u;
+        if (pos) pos[o] = 0;
+        if (parent) parent[o] = -1;
+        if (tok) tok[o] = -1;
+      }
+    }
+    if (lane == 0 && tree_len) tree_len[r] = n;
+    __syncwarp();
   }
 }
 
 struct VerifyShared {
-  float wv[kStreamWarps];
-  int wi[kStreamWarps];
+  float wv[kConsumerWarps];
+  int wi[kConsumerWarps];
   int last, rlast;
-  float bv;
-  int bi;
+  int walk[1];  // [3 * T] staged (parent, token, argmax) of the walked request (dynamic tail)
 };
 
-template <bool BF16, bool ALIGNED>
-__global__ void __launch_bounds__(kStreamThreads, 2)
+__device__ __forceinline__ int find_request(const Params& P, int row) {
+  int a = 0, b = P.b_loc - 1;
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (P.vrow_off[m] <= row) a = m;
+    else b = m - 1;
+  }
+  return a;
+}
+
+// K4: persistent TMA-staged stream over all tree rows (request r, node i < tree_len[r]) of the
+// target logits; exact argmax per row (value desc, index asc); the request whose last row
+// completes runs the greedy walk.
+template <bool BF16, bool TMA>
+__global__ void __launch_bounds__(kLayerThreads, 2)
 verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int32_t* accept_len,
               int32_t* accept_path, int32_t* bonus) {
   constexpr int EPV = BF16 ? 8 : 4;
   constexpr int ESZ = BF16 ? 2 : 4;
   constexpr int EPT = kVecPerThread * EPV;
-  __shared__ VerifyShared sh;
+  extern __shared__ __align__(128) char dsm[];
+  char* ring = dsm;
+  StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
+  VerifyShared& sh = *reinterpret_cast<VerifyShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NR = P.vrow_off[P.b_loc];
   const int cpr = P.cpr, CE = P.chunk_elems, V = P.V, T = P.T;
-  const long long TOT = (long long)NR * cpr;
-  const long long lo = TOT * blockIdx.x / gridDim.x;
-  const long long hi = TOT * (blockIdx.x + 1) / gridDim.x;
+  const long long row_bytes = (long long)V * ESZ;
+  const RowRange rr = cta_range_min((long long)NR * cpr, P.min_units);
+  if (rr.lo >= rr.hi) return;
+  auto row_base = [&](int row) {
+    const int r = find_request(P, row);
+    return target + ((long long)r * T + (row - P.vrow_off[r])) * ld_bytes;
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&pipe.full[s], 1);
+      mbar_init(&pipe.empty[s], kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (TMA && lane == 0) produce(pipe, ring, rr, cpr, row_bytes, row_base);
+    return;
+  }
   int nanf = 0;
-  long long q = lo;
-  while (q < hi) {
+  long long i = 0;
+  long long q = rr.lo;
+  while (q < rr.hi) {
     const int row = (int)(q / cpr);
     const int c0 = (int)(q % cpr);
-    const int nch = (int)min((long long)(cpr - c0), hi - q);
-    // row -> (request, node) by binary search over vrow_off
-    int a = 0, b = P.b_loc - 1;
-    while (a < b) {
-      int m = (a + b + 1) >> 1;
-      if (P.vrow_off[m] <= row) a = m;
-      else b = m - 1;
-    }
-    const int r = a, i = row - P.vrow_off[a];
-    const char* rp = target + ((long long)r * T + i) * ld_bytes;
+    const int nch = (int)min((long long)(cpr - c0), rr.hi - q);
+    const int r = find_request(P, row);
+    const int node = row - P.vrow_off[r];
     float bv = -INFINITY;
     int bi = kIdxSentinel;
-    for (int c = c0; c < c0 + nch; ++c) {
+    for (int c = c0; c < c0 + nch; ++c, ++i) {
       const int cbase = c * CE;
       float x[EPT];
+      if (TMA) {
+        const int s = (int)(i % kStages);
+        mbar_wait(&pipe.full[s], (uint32_t)((i / kStages) & 1));
+        const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
+        uint4 raw[kVecPerThread];
 #pragma unroll
-      for (int j = 0; j < kVecPerThread; ++j) {
-        int e0 = cbase + (j * kStreamThreads + tid) * EPV;
-        uint4 v;
-        if (ALIGNED && e0 + EPV <= V) {
-          v = ldg_stream(rp + (size_t)e0 * ESZ);
-          uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pipe.empty[s]);
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
           for (int q2 = 0; q2 < 4; ++q2) {
             if (BF16) {
@@ -185,7 +221,17 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
               x[j * 4 + q2] = __uint_as_float(w[q2]);
             }
           }
-        } else {
+        }
+        if (c == cpr - 1) {
+#pragma unroll
+          for (int n = 0; n < EPT; ++n)
+            if (cbase + ((n / EPV) * kConsumers + tid) * EPV + (n % EPV) >= V) x[n] = -INFINITY;
+        }
+      } else {
+        const char* rp = row_base(row);
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+          const int e0 = cbase + (j * kConsumers + tid) * EPV;
 #pragma unroll
           for (int e = 0; e < EPV; ++e) {
             float xv = -INFINITY;
@@ -204,13 +250,13 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
       int mi = kIdxSentinel;
 #pragma unroll
       for (int n = 0; n < EPT; ++n) {
-        int gi = cbase + ((n / EPV) * kStreamThreads + tid) * EPV + (n % EPV);
+        const int gi = cbase + ((n / EPV) * kConsumers + tid) * EPV + (n % EPV);
         if (x[n] == m && mi == kIdxSentinel && gi < V) mi = gi;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        float ov = __shfl_xor_sync(kFull, m, o);
-        int oi = __shfl_xor_sync(kFull, mi, o);
+        const float ov = __shfl_xor_sync(kFull, m, o);
+        const int oi = __shfl_xor_sync(kFull, mi, o);
         if (better(ov, oi, m, mi)) {
           m = ov;
           mi = oi;
@@ -225,97 +271,105 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
       sh.wv[warp] = bv;
       sh.wi[warp] = bi;
     }
-    __syncthreads();
+    consumer_sync();
     if (tid == 0) {
       float v = sh.wv[0];
       int ix = sh.wi[0];
-      for (int w = 1; w < kStreamWarps; ++w)
+      for (int w = 1; w < kConsumerWarps; ++w)
         if (better(sh.wv[w], sh.wi[w], v, ix)) {
           v = sh.wv[w];
           ix = sh.wi[w];
         }
-      size_t so = (size_t)row * cpr + c0;
+      const size_t so = (size_t)row * cpr + c0;
       P.vsegv[so] = v;
       P.vsegi[so] = ix;
       P.vseglen[so] = nch;
       __threadfence();
-      int old = atomicAdd(&P.row_done[row], nch);
+      const int old = atomicAdd(&P.row_done[row], nch);
       sh.last = (old + nch == cpr);
     }
-    __syncthreads();
-    if (sh.last) {
-      // merge this row's segments (warp 0)
-      if (warp == 0) {
-        __threadfence();
-        float v = -INFINITY;
-        int ix = kIdxSentinel;
-        for (int c = lane; c < cpr; c += 32) {
-          size_t so = (size_t)row * cpr + c;
-          if (__ldcg(&P.vseglen[so]) > 0) {
-            float sv = __ldcg(&P.vsegv[so]);
-            int si = __ldcg(&P.vsegi[so]);
-            if (better(sv, si, v, ix)) {
-              v = sv;
-              ix = si;
-            }
-            P.vseglen[so] = 0;
+    consumer_sync();
+    if (sh.last && warp == 0) {
+      __threadfence();
+      float v = -INFINITY;
+      int ix = kIdxSentinel;
+      for (int c = lane; c < cpr; c += 32) {
+        const size_t so = (size_t)row * cpr + c;
+        if (__ldcg(&P.vseglen[so]) > 0) {
+          const float sv = __ldcg(&P.vsegv[so]);
+          const int si = __ldcg(&P.vsegi[so]);
+          if (better(sv, si, v, ix)) {
+            v = sv;
+            ix = si;
           }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          float ov = __shfl_xor_sync(kFull, v, o);
-          int oi = __shfl_xor_sync(kFull, ix, o);
-          if (better(ov, oi, v, ix)) {
-            v = ov;
-            ix = oi;
-          }
-        }
-        if (lane == 0) {
-          P.vrow_arg[(size_t)r * T + i] = ix;
-          P.row_done[row] = 0;
-          __threadfence();
-          int old = atomicAdd(&P.req_done[r], 1);
-          sh.rlast = (old + 1 == P.n_nodes[r]);
-        }
-        __syncwarp();
-        if (sh.rlast) {
-          // greedy walk of request r
-          __threadfence();
-          const int n = P.n_nodes[r];
-          const int D = P.d > 0 ? P.d : 1;
-          int cur = 0, acc = 0, bon = -1;
-          for (;;) {
-            int t = __ldcg(&P.vrow_arg[(size_t)r * T + cur]);
-            int found = -1;
-            for (int j0 = cur + 1; j0 < n; j0 += 32) {
-              int j = j0 + lane;
-              bool f = j < n && P.parent[(size_t)r * T + j] == cur && P.tok[(size_t)r * T + j] == t;
-              unsigned bal = __ballot_sync(kFull, f);
-              if (bal) {
-                found = j0 + __ffs(bal) - 1;
-                break;
-              }
-            }
-            if (found < 0) {
-              bon = t;
-              break;
-            }
-            if (lane == 0 && accept_path && acc < D) accept_path[(size_t)r * D + acc] = found;
-            ++acc;
-            cur = found;
-          }
-          if (lane == 0) {
-            if (accept_len) accept_len[r] = acc;
-            if (bonus) bonus[r] = bon;
-            atomicAdd(P.sum_accept, (unsigned long long)acc);
-            P.req_done[r] = 0;
-          }
-          if (accept_path)
-            for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;
+          P.vseglen[so] = 0;
         }
       }
-      __syncthreads();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(kFull, v, o);
+        const int oi = __shfl_xor_sync(kFull, ix, o);
+        if (better(ov, oi, v, ix)) {
+          v = ov;
+          ix = oi;
+        }
+      }
+      int rl = 0;
+      if (lane == 0) {
+        P.vrow_arg[(size_t)r * T + node] = ix;
+        P.row_done[row] = 0;
+        __threadfence();
+        const int old = atomicAdd(&P.req_done[r], 1);
+        rl = (old + 1 == P.n_nodes[r]);
+      }
+      rl = __shfl_sync(kFull, rl, 0);
+      if (rl) {
+        // greedy walk of request r: follow the child whose token is the target argmax.
+        // The request's tree (parent, token, row argmax) is staged in shared memory first.
+        __threadfence();
+        const int n = P.n_nodes[r];
+        const int D = P.d > 0 ? P.d : 1;
+        int* s_par = sh.walk;
+        int* s_tok = sh.walk + T;
+        int* s_arg = sh.walk + 2 * T;
+        for (int j = lane; j < n; j += 32) {
+          s_par[j] = P.parent[(size_t)r * T + j];
+          s_tok[j] = P.tok[(size_t)r * T + j];
+          s_arg[j] = __ldcg(&P.vrow_arg[(size_t)r * T + j]);
+        }
+        __syncwarp();
+        int cur = 0, acc = 0, bon = -1;
+        for (;;) {
+          const int t = s_arg[cur];
+          int found = -1;
+          for (int j0 = cur + 1; j0 < n; j0 += 32) {
+            const int j = j0 + lane;
+            const bool f = j < n && s_par[j] == cur && s_tok[j] == t;
+            const unsigned bal = __ballot_sync(kFull, f);
+            if (bal) {
+              found = j0 + __ffs(bal) - 1;
+              break;
+            }
+          }
+          if (found < 0) {
+            bon = t;
+            break;
+          }
+          if (lane == 0 && accept_path && acc < D) accept_path[(size_t)r * D + acc] = found;
+          ++acc;
+          cur = found;
+        }
+        if (lane == 0) {
+          if (accept_len) accept_len[r] = acc;
+          if (bonus) bonus[r] = bon;
+          atomicAdd(P.sum_accept, (unsigned long long)acc);
+          P.req_done[r] = 0;
+        }
+        if (accept_path)
+          for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;
+      }
     }
+    consumer_sync();
     q += nch;
   }
   if (nanf) atomicOr(P.err, kErrTargetNaN);
@@ -325,24 +379,39 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
 
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok, int32_t* tree_len,
                  cudaStream_t s) {
-  mask_kernel<<<1, 1024, 0, s>>>(P, mask, pos, parent, tok, tree_len);
+  const size_t smem = (size_t)32 * 3 * P.T * sizeof(int);
+  mask_kernel<<<1, 1024, smem, s>>>(P, mask, pos, parent, tok, tree_len);
+}
+
+cudaError_t mask_set_smem() {
+  return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 3 * 1024 * 4);
+}
+
+size_t verify_smem_bytes(int T) {
+  return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(VerifyShared) + (size_t)3 * T * 4;
 }
 
 int verify_occupancy() {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true>, kStreamThreads, 0);
+  const int sm = (int)verify_smem_bytes(1024);
+  cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(verify_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(verify_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(verify_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true>, kLayerThreads, verify_smem_bytes(1024));
   return n > 0 ? n : 1;
 }
 
-void launch_verify(const Params& P, const void* target, long long ld_bytes, bool aligned, int32_t* accept_len,
+void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma, int32_t* accept_len,
                    int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s) {
   const char* t = static_cast<const char*>(target);
+  const size_t sm = verify_smem_bytes(P.T);
   if (P.dtype == SMART_BF16) {
-    if (aligned) verify_kernel<true, true><<<grid, kStreamThreads, 0, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
-    else verify_kernel<true, false><<<grid, kStreamThreads, 0, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) verify_kernel<true, true><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    else verify_kernel<true, false><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
   } else {
-    if (aligned) verify_kernel<false, true><<<grid, kStreamThreads, 0, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
-    else verify_kernel<false, false><<<grid, kStreamThreads, 0, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) verify_kernel<false, true><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    else verify_kernel<false, false><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
   }
 }
 

@@ -1,0 +1,604 @@
+// select_core.cuh — A3-A6 of one layer as a block-level device routine (any block size that is a
+// multiple of 32).  Called (a) by the last CTA of the fused layer kernel (256 consumer threads)
+// and (b) by the standalone select kernel (multi-rank phases, very large batches).
+//
+// PAPER.md: marginal benefit Eq.(13); marginal cost Eq.(15); decision rule
+// Eq.(12)/(16) P:294-300 / P:347-355; Algorithm 1 lines 5-12 P:859-871; budget Eq.(8) P:243.
+// Readings: Q3 mid-layer budget cut, Q6 |P| frozen at layer start, Q7 FROZEN/PREFIX, Q8 strict >,
+// Q9 ties (b desc, request asc, c asc), Q13 batch-coupled cost, Q19 omega.
+//
+// Determinism: every floating-point reduction has a structure fixed by the data size only
+// (32-wide xor/up trees per tile, sequential over tiles), never by the block size or by how the
+// batch is sharded — G ranks reproduce the G = 1 decisions bit for bit.
+#pragma once
+
+#include "smart_internal.cuh"
+
+namespace smart {
+
+// barrier among the NT threads running the selection: named barrier 1 (the fused layer kernel's
+// producer warp never joins it; in the standalone kernel NT == blockDim.x)
+template <int NT>
+__device__ __forceinline__ void blk_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+enum SelectMode { kSelFull = 0, kSelLocal = 1, kSelGlobal = 2 };
+
+__device__ __forceinline__ unsigned long long sel_key(float b, int r_glob, int c) {
+  return ((unsigned long long)(~float_orderable(b)) << 32) | ((unsigned long long)(unsigned)r_glob << 16) |
+         (unsigned long long)(unsigned)c;
+}
+__device__ __forceinline__ float sel_key_b(unsigned long long key) {
+  uint32_t o = ~(uint32_t)(key >> 32);
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ int sel_key_r(unsigned long long key) { return (int)((key >> 16) & 0xffffu); }
+__device__ __forceinline__ int sel_key_c(unsigned long long key) { return (int)(key & 0xffffu); }
+
+// b * S = c_T (omega b + E) / cost(N), cost from the host-built fp64 table (0/0 := 0, Q4)
+__device__ __forceinline__ double speed_tab(const Params& P, double E, long long N, int b) {
+  double C = P.cost_tab[N];
+  return C > 0.0 ? P.c_T * ((double)P.omega * b + E) / C : 0.0;
+}
+
+struct SelScratch {
+  double tile_d[260];
+  int tile_i[1040];
+  double bcast_d[4];
+  long long bcast_l[2];
+  int bcast_i[8];
+  int wred_i[32];
+  double wred_d[32];
+};
+
+// ---- deterministic, block-size independent helpers -----------------------------------------
+
+// sum of a[0..n) (smem): 32-wide xor trees per tile, tiles summed in order by one thread
+template <int NT>
+__device__ double det_sum(const double* a, int n, SelScratch& ss) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntile = (n + 31) / 32;
+  for (int t = warp; t < ntile; t += NT / 32) {
+    int i = t * 32 + lane;
+    double v = i < n ? a[i] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) ss.tile_d[t] = v;
+  }
+  blk_sync<NT>();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int t = 0; t < ntile; ++t) s += ss.tile_d[t];
+    ss.bcast_d[0] = s;
+  }
+  blk_sync<NT>();
+  double r = ss.bcast_d[0];
+  blk_sync<NT>();
+  return r;
+}
+
+template <int NT>
+__device__ long long block_sum_ll(long long v, SelScratch& ss) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  blk_sync<NT>();
+  if (lane == 0) ss.wred_d[warp] = (double)v;  // exact for counts < 2^53
+  blk_sync<NT>();
+  if (tid == 0) {
+    double s = 0;
+    for (int w = 0; w < NT / 32; ++w) s += ss.wred_d[w];
+    ss.bcast_l[0] = (long long)s;
+  }
+  blk_sync<NT>();
+  long long r = ss.bcast_l[0];
+  blk_sync<NT>();
+  return r;
+}
+
+// exclusive scan of ints in smem a[0..n) in place; returns total (ints: association-free)
+template <int NT>
+__device__ int excl_scan_int(int* a, int n, SelScratch& ss) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ntile = (n + 31) / 32;
+  for (int t = warp; t < ntile; t += NT / 32) {
+    const int i = t * 32 + lane;
+    const int v = i < n ? a[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (i < n) a[i] = incl - v;
+    if (lane == 31) ss.tile_i[t] = incl;
+  }
+  blk_sync<NT>();
+  if (warp == 0) {
+    // tile totals: each lane owns a contiguous group of tiles, then one warp scan
+    const int per = (ntile + 31) / 32;
+    const int t0 = lane * per, t1 = min(ntile, t0 + per);
+    int loc = 0;
+    for (int t = t0; t < t1; ++t) loc += ss.tile_i[t];
+    int incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    int run = incl - loc;
+    for (int t = t0; t < t1; ++t) {
+      const int v = ss.tile_i[t];
+      ss.tile_i[t] = run;
+      run += v;
+    }
+    if (lane == 31) ss.bcast_i[0] = incl;
+  }
+  blk_sync<NT>();
+  for (int i = tid; i < n; i += NT) a[i] += ss.tile_i[i >> 5];
+  const int total = ss.bcast_i[0];
+  blk_sync<NT>();
+  return total;
+}
+
+// ascending bitonic sort of keys[0..P2) (P2 power of two)
+template <int NT>
+__device__ void bitonic_sort(unsigned long long* keys, int P2) {
+  const int tid = threadIdx.x;
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (P2 >> 1); i += NT) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool asc = (lo & size) == 0;
+        unsigned long long a = keys[lo], b = keys[hi];
+        if ((a > b) == asc) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      blk_sync<NT>();
+    }
+  }
+}
+
+// ---- layout of the dynamic shared memory used by select_layer --------------------------------
+struct SelLayout {
+  int* cnt;       // [b_loc] frontier rows of the layer per request
+  int* off;       // [b_loc] frontier offset
+  int* nd;        // [b_loc] drafted nodes before the layer
+  int* base;      // [b_loc] eligible base (A3), later next-frontier offsets
+  int* adm;       // [b_loc] admitted per request
+  int* nxt;       // [b_loc] next-frontier count per request
+  float* D;       // [b_loc] benefit divisor |P_r| (PATH_MEAN) or 1
+  int* crow;      // [nc_cap] request of each candidate
+  float* cb;      // [nc_cap] benefit of each candidate
+  int* pre;       // [nc_cap + 1] exclusive scan of admitted flags (flags first)
+  float* cum;     // [nc_cap] path score of each candidate
+  Cand* cd;       // [nc_cap] staged candidate records
+  int* fin;       // [b_loc] finished flag
+  double* ctab;   // [nc_cap + 2] cost(N0 + j)
+  double* dtab;   // [nc_cap + 2] marginal cost at N0 + j
+  double* E;      // [max(b_loc, b_glob)] E_r (global order in kSelGlobal)
+  unsigned long long* keys;  // [P2]
+  unsigned long long* keys2;  // [P2] rank-sort output
+};
+
+// cost-table window: global eligible count <= nranks * nc_cap
+__host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks = 1) {
+  size_t bytes = (size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4;
+  bytes = (bytes + 15) & ~size_t(15);
+  bytes += (size_t)nc_cap * sizeof(Cand);
+  bytes += ((size_t)nc_cap * nranks + 2) * 16;
+  bytes += (size_t)b_all * 8;
+  bytes = (bytes + 15) & ~size_t(15);
+  bytes += (size_t)sort_cap * 16;
+  return bytes;
+}
+
+__device__ inline SelLayout sel_layout(char* smem, int b_loc, int b_all, int nc_cap, int nranks, int sort_cap) {
+  SelLayout L;
+  int* ip = reinterpret_cast<int*>(smem);
+  L.cnt = ip;
+  L.off = ip + b_loc;
+  L.nd = ip + 2 * b_loc;
+  L.base = ip + 3 * b_loc;
+  L.adm = ip + 4 * b_loc;
+  L.nxt = ip + 5 * b_loc;
+  L.D = reinterpret_cast<float*>(ip + 6 * b_loc);
+  L.crow = ip + 7 * b_loc;
+  L.cb = reinterpret_cast<float*>(L.crow + nc_cap);
+  L.pre = reinterpret_cast<int*>(L.cb + nc_cap);
+  L.cum = reinterpret_cast<float*>(L.pre + nc_cap + 1);
+  L.fin = reinterpret_cast<int*>(L.cum + nc_cap);
+  size_t bytes = ((size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4 + 15) & ~size_t(15);
+  L.cd = reinterpret_cast<Cand*>(smem + bytes);
+  bytes += (size_t)nc_cap * sizeof(Cand);
+  L.ctab = reinterpret_cast<double*>(smem + bytes);
+  L.dtab = L.ctab + (size_t)nc_cap * nranks + 2;
+  bytes += ((size_t)nc_cap * nranks + 2) * 16;
+  L.E = reinterpret_cast<double*>(smem + bytes);
+  bytes += (size_t)b_all * 8;
+  bytes = (bytes + 15) & ~size_t(15);
+  L.keys = reinterpret_cast<unsigned long long*>(smem + bytes);
+  L.keys2 = L.keys + sort_cap;
+  return L;
+}
+
+// warp-level exclusive scan of per-request ints held lane-blocked: lane l owns requests
+// [l*per, min(n, (l+1)*per)) stored in smem a[]; returns the total (ints: association-free)
+__device__ __forceinline__ int warp_excl_scan_smem(int* a, int n, int lane) {
+  const int per = (n + 31) / 32;
+  const int r0 = lane * per, r1 = min(n, r0 + per);
+  int loc = 0;
+  for (int r = r0; r < r1; ++r) loc += a[r];
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += u;
+  }
+  int run = incl - loc;
+  for (int r = r0; r < r1; ++r) {
+    const int v = a[r];
+    a[r] = run;
+    run += v;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  __syncwarp();
+  return total;
+}
+
+// deterministic sum of a[0..n) (smem) by one warp: 32-wide xor trees per tile, tiles in order
+__device__ __forceinline__ double warp_det_sum(const double* a, int n, int lane) {
+  double s = 0.0;
+  for (int t = 0; t < n; t += 32) {
+    double v = (t + lane < n) ? a[t + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    s += v;
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// select_layer: A3-A6 for `layer`.  mode kSelFull: single rank (or LOCAL cost scope);
+// kSelLocal: A3 + local sort, pack the exchange record; kSelGlobal: merge gathered records,
+// A5 on the global list, commit own requests.
+// Warp-centric: warp 0 runs every per-request step with shuffles (no block barriers); all NT
+// threads join only the two O(n^2) rank loops (within-request ranks, global rank sort).
+// ---------------------------------------------------------------------------------------------
+template <int NT>
+__device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
+  __shared__ SelScratch ss;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int par = (layer - 1) & 1, npar = layer & 1;
+  const int k = P.k, bl = P.b_loc;
+  const int b_all = (mode == kSelGlobal) ? P.b_glob : bl;
+  const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+  DevTrace& tr = P.trace[layer - 1];
+  const int R = *P.fr_total[par];
+  const int nct = R * k;  // candidates of this layer (local)
+  SelLayout L = sel_layout(smem, bl, b_all, P.cap_rows * k, P.nranks, P.sort_cap);
+  stamp(P, tid == 0, 9);
+
+  // ---- stage per-request state and the candidates (one wave of independent loads) ----
+  for (int r = tid; r < bl; r += NT) {
+    L.cnt[r] = P.fr_cnt[par][r];
+    L.off[r] = P.fr_off[par][r];
+    L.nd[r] = P.n_nodes[r] - 1;
+    L.D[r] = (P.accept_model == SMART_PATH_MEAN) ? (float)P.leaf_cnt[r] : 1.f;  // Eq.(13), Q6
+    L.fin[r] = P.finished[r];
+    if (mode != kSelGlobal) L.E[r] = P.E_r[r];
+  }
+  {
+    // cost-table window from N0 = drafted nodes before the layer (kept by the previous layer)
+    const long long n0g = *P.N_glob;
+    const int ncap = P.cap_rows * k * P.nranks + 2;
+    for (int j = tid; j < ncap; j += NT) {
+      const long long N = min(n0g + j, (long long)P.n_cost - 1);
+      L.ctab[j] = P.cost_tab[N];
+      L.dtab[j] = P.dc_tab[N];
+    }
+  }
+  if (mode == kSelGlobal) {
+    for (int i = tid; i < P.nranks * P.m_cap; i += NT) {
+      const int g = i / P.m_cap, e = i % P.m_cap;
+      L.keys[i] = reinterpret_cast<const unsigned long long*>(P.xr + (size_t)g * P.xstride)[e];
+    }
+    for (int i = tid; i < P.b_glob; i += NT) {
+      const int g = i / bl, r = i % bl;
+      L.E[i] = reinterpret_cast<const double*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8)[r];
+    }
+  }
+  if (tid == 0) L.pre[nct] = 0;
+  for (int q = tid; q < nct; q += NT) {
+    L.crow[q] = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
+    const Cand c = P.cand[lbase + q];
+    L.cd[q] = c;
+    L.cum[q] = c.cum;
+    L.pre[q] = 0;
+  }
+  blk_sync<NT>();
+  stamp(P, tid == 0, 10);
+
+  // ---- A3 (warp 0): per-request eligibility e_r = min(B - n_r, W, |U_r|), eligible bases ----
+  int ne = 0;
+  long long N0 = 0;
+  if (warp == 0) {
+    long long nl = 0;
+    for (int r = lane; r < bl; r += 32) {
+      int q = P.B - L.nd[r];
+      if (q > P.Wq) q = P.Wq;
+      if (q < 0) q = 0;
+      L.base[r] = min(q, L.cnt[r] * k);
+      nl += L.nd[r];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nl += __shfl_xor_sync(kFull, nl, o);
+    __syncwarp();
+    const int tot = warp_excl_scan_smem(L.base, bl, lane);
+    if (lane == 0) {
+      ss.bcast_i[2] = tot;
+      ss.bcast_l[1] = nl;
+    }
+  }
+  // all threads: benefit b = cum / D_r
+  for (int q = tid; q < nct; q += NT) {
+    const float D = L.D[L.crow[q]];
+    L.cb[q] = (D == 1.f) ? L.cum[q] : __fdiv_rn(L.cum[q], D);
+  }
+  blk_sync<NT>();
+  if (mode != kSelGlobal) {
+    ne = ss.bcast_i[2];
+    N0 = ss.bcast_l[1];
+    // within-request rank by (b desc, c asc); eligible if rank < e_r
+    for (int q = tid; q < nct; q += NT) {
+      const int r = L.crow[q];
+      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+      const float b = L.cb[q];
+      P.cand_b[lbase + q] = b;
+      int rank = 0;
+      for (int j = s0; j < s1; ++j) {
+        const float bj = L.cb[j];
+        rank += (bj > b) || (bj == b && j < q);
+      }
+      const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
+      if (rank < e_r) L.keys[L.base[r] + rank] = sel_key(b, P.b_off + r, q - s0);
+    }
+    blk_sync<NT>();
+  }
+  stamp(P, tid == 0, 11);
+
+  // ---- A4: sort (local list, or the gathered lists of all ranks) ----
+  const int nsort = (mode == kSelGlobal) ? P.nranks * P.m_cap : ne;
+  if (nsort <= 1024) {
+    // rank sort (keys unique; padding ~0 keys sort to the end)
+    for (int i = tid; i < nsort; i += NT) {
+      const unsigned long long key = L.keys[i];
+      int rank = 0;
+#pragma unroll 8
+      for (int f = 0; f < nsort; ++f) rank += (L.keys[f] < key);
+      L.keys2[rank] = key;
+    }
+    blk_sync<NT>();
+    unsigned long long* t = L.keys;
+    L.keys = L.keys2;
+    L.keys2 = t;
+  } else {
+    int P2 = 1;
+    while (P2 < nsort) P2 <<= 1;
+    for (int i = nsort + tid; i < P2; i += NT) L.keys[i] = ~0ull;
+    blk_sync<NT>();
+    bitonic_sort<NT>(L.keys, P2);
+  }
+  stamp(P, tid == 0, 12);
+
+  if (mode == kSelLocal) {
+    unsigned long long* xk = reinterpret_cast<unsigned long long*>(P.xs);
+    double* xE = reinterpret_cast<double*>(P.xs + (size_t)P.m_cap * 8);
+    int* xh = reinterpret_cast<int*>(P.xs + (size_t)P.m_cap * 8 + (size_t)bl * 8);
+    for (int i = tid; i < P.m_cap; i += NT) xk[i] = i < ne ? L.keys[i] : ~0ull;
+    for (int r = tid; r < bl; r += NT) {
+      xh[r] = L.nd[r];
+      xE[r] = L.E[r];
+    }
+    if (tid == 0) {
+      xh[bl] = ne;
+      xh[bl + 1] = R;
+    }
+    return;
+  }
+
+  int R_all = R;
+  if (mode == kSelGlobal) {
+    long long nloc = 0, eloc = 0, rloc = 0;
+    for (int i = tid; i < P.b_glob; i += NT) {
+      const int g = i / bl, r = i % bl;
+      nloc += reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8)[r];
+    }
+    for (int g = tid; g < P.nranks; g += NT) {
+      const int* h = reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8);
+      eloc += h[bl];
+      rloc += h[bl + 1];
+    }
+    N0 = block_sum_ll<NT>(nloc, ss);
+    ne = (int)block_sum_ll<NT>(eloc, ss);
+    R_all = (int)block_sum_ll<NT>(rloc, ss);
+  }
+  const int bc = (P.cost_scope == SMART_COST_LOCAL) ? bl : P.b_glob;
+  auto sp = [&](double E, int j) {  // b*S at N0 + j from the prefetched window
+    const double C = L.ctab[j];
+    return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
+  };
+
+  // ---- A5 + A6 on warp 0 (no block barriers) ----
+  if (warp == 0) {
+    const double E0 = warp_det_sum(L.E, b_all, lane);  // global request order (Q13)
+    const double Sb0 = sp(E0, 0);
+    const double dc0 = L.dtab[0];
+    const double ac = P.alpha * P.c_T;
+    // exclusive prefix of b over the sorted list: 32-tiles (fixed trees), tiles in order
+    int first_fail = ne;
+    double bestS = Sb0;
+    int bestj = 0;
+    double run = 0.0;
+    for (int t = 0; t < ne; t += 32) {
+      const int j = t + lane;
+      const double bj = j < ne ? (double)sel_key_b(L.keys[j]) : 0.0;
+      double incl = bj;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (j < ne) {
+        const double before = run + (incl - bj);  // sum of b over positions < j
+        // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
+        // cost == 0 means S := 0, i.e. admit any positive benefit)
+        bool ok;
+        if (P.selection == SMART_FROZEN) {
+          ok = (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > P.c_T * ((double)P.omega * bc + E0) * dc0) : (bj > 0.0);
+        } else {
+          const double C = L.ctab[j];
+          ok = (C > 0.0) ? (ac * bj * C > P.c_T * ((double)P.omega * bc + E0 + before) * L.dtab[j]) : (bj > 0.0);
+        }
+        if (!ok && j < first_fail) first_fail = j;
+        const double Sa = sp(E0 + before + bj, j + 1);
+        if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+          bestS = Sa;
+          bestj = j + 1;
+        }
+      }
+      run += __shfl_sync(kFull, incl, 31);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      first_fail = min(first_fail, __shfl_xor_sync(kFull, first_fail, o));
+      const double os = __shfl_xor_sync(kFull, bestS, o);
+      const int oj = __shfl_xor_sync(kFull, bestj, o);
+      if (os > bestS || (os == bestS && oj < bestj)) {
+        bestS = os;
+        bestj = oj;
+      }
+    }
+    const int js = first_fail;
+    // sum of the admitted benefits (same tile structure as the prefix above)
+    double adm_b = 0.0;
+    for (int t = 0; t < js; t += 32) {
+      double v = (t + lane < js) ? (double)sel_key_b(L.keys[t + lane]) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      adm_b += v;
+    }
+    if (lane == 0) {
+      tr.executed = R_all > 0 ? 1 : 0;
+      tr.n_rows = R;
+      tr.n_cand = nct;
+      tr.n_elig = ne;
+      tr.n_admit = js;
+      tr.argmax_j = bestj;
+      tr.N0 = (int)N0;
+      tr.E0 = E0;
+      tr.S0 = Sb0 / bc;
+      tr.dc0 = dc0;
+      tr.saturated = (N0 + ne >= P.sat_from) ? 1 : 0;
+      if (tr.saturated) atomicOr(P.err, kErrSaturated);
+    }
+    stamp(P, lane == 0, 13);
+    // ---- A6: commit (own requests) ----
+    for (int j = lane; j < js; j += 32) {
+      const unsigned long long key = L.keys[j];
+      const int r = sel_key_r(key) - P.b_off;
+      if (r >= 0 && r < bl) L.pre[L.off[r] * k + sel_key_c(key)] = 1;
+    }
+    __syncwarp();
+    for (int q = lane; q < nct; q += 32) P.cand_adm[lbase + q] = L.pre[q];
+    // per request (lane-strided): admitted count, finish, next-frontier count
+    for (int r = lane; r < bl; r += 32) {
+      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+      int a = 0;
+      for (int q = s0; q < s1; ++q) a += L.pre[q];
+      L.adm[r] = a;
+      const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
+      L.nxt[r] = fin ? 0 : a;
+      L.base[r] = fin ? 0 : a;
+      P.fr_cnt[npar][r] = fin ? 0 : a;
+      if (fin && L.cnt[r] > 0) P.finished[r] = 1;
+    }
+    __syncwarp();
+    const int total = warp_excl_scan_smem(L.base, bl, lane);
+    for (int r = lane; r < bl; r += 32) P.fr_off[npar][r] = L.base[r];
+    if (lane == 0) *P.fr_total[npar] = total;
+    // nodes in canonical order (c asc) + E bookkeeping, one lane per request (deterministic)
+    for (int r = lane; r < bl; r += 32) {
+      const int a = L.adm[r];
+      if (a == 0) continue;
+      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+      const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
+      const int n0 = L.nd[r] + 1;
+      int rank = 0;
+      double esum = 0.0, psum_new = 0.0, psum_par = 0.0;
+      int nparents = 0;
+      for (int q0 = s0; q0 < s1; q0 += k) {
+        bool any = false;
+        for (int q = q0; q < q0 + k; ++q) {
+          if (!L.pre[q]) continue;
+          const Cand cd = L.cd[q];
+          const int node = n0 + rank;
+          const size_t o = (size_t)r * P.T + node;
+          P.tok[o] = cd.tok;
+          P.parent[o] = cd.parent;
+          P.depth[o] = layer;
+          P.p[o] = cd.p;
+          P.cum[o] = cd.cum;
+          esum += (double)cd.cum;
+          if (P.accept_model == SMART_PATH_MEAN) {
+            const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
+            P.path_sum[o] = pps + (double)cd.cum;
+            psum_new += pps + (double)cd.cum;
+            if (!any) {
+              psum_par += pps;
+              ++nparents;
+            }
+          }
+          any = true;
+          if (L.nxt[r] > 0) P.fr[npar][L.base[r] + rank] = make_int2(r, node);
+          ++rank;
+        }
+      }
+      P.n_nodes[r] = n0 + a;
+      if (P.accept_model == SMART_PATH_MEAN) {
+        const int lc = P.leaf_cnt[r] - nparents + a;
+        const double ls = P.leaf_sum[r] - psum_par + psum_new;
+        P.leaf_cnt[r] = lc;
+        P.leaf_sum[r] = ls;
+        L.E[gi] = ls / (double)lc;  // Eq.(2) path mean of the committed tree
+      } else {
+        L.E[gi] += esum;  // node sum (Q11)
+      }
+      P.E_r[r] = L.E[gi];
+    }
+    __syncwarp();
+    // ---- totals after the layer (trace S_after) ----
+    if (mode == kSelFull) {
+      const double Ea = warp_det_sum(L.E, bl, lane);
+      if (lane == 0) {
+        tr.S_after = sp(Ea, js) / bc;
+        *P.N_glob = (int)(N0 + js);
+        *P.E_glob = Ea;
+      }
+    } else if (lane == 0) {
+      // NODE_SUM: E after = E0 + sum of admitted benefits (exact); PATH_MEAN: approximate
+      const double Ea = E0 + adm_b;
+      tr.S_after = sp(Ea, js) / bc;
+      *P.N_glob = (int)(N0 + js);
+      *P.E_glob = Ea;
+    }
+    stamp(P, lane == 0, 22);
+  }
+}
+
+}  // namespace smart

@@ -18,8 +18,10 @@ constexpr int kStreamThreads = 256;      // CTA size of the streaming kernels (8
 constexpr int kStreamWarps = kStreamThreads / kWarp;
 constexpr int kVecPerThread = kChunkBytes / 16 / kStreamThreads;  // 4 x 16 B per thread
 constexpr int kWarpBuf = 64;             // per-warp candidate staging (top-k filter)
+constexpr int kSegBuf = 128;             // per-warp segment candidate buffer
 constexpr int kSelectThreads = 1024;     // single-CTA selection kernel
 constexpr int kMaxK = 32;
+constexpr int kMaxCpr = 64;   // chunks per row (V*esz <= 1 MiB)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kIdxSentinel = 0x7fffffff;
 
@@ -76,15 +78,26 @@ struct Params {
 
   // ---- A1 streaming scratch ----
   float2* ms;         // [cap_rows*cpr*8] per (chunk, warp) softmax partial (max, sum)
-  float* segv;        // [cap_rows*cpr*8*k] per (segment start chunk, warp) top-k values
-  int* segi;          //   ... and indices
+  unsigned long long* segkey;  // [cap_rows*cpr*k] per-segment (at its first chunk) CTA top-k keys
   int* seglen;        // [cap_rows*cpr] segment length in chunks (at its first chunk)
   int* row_done;      // [max(cap_rows, b_loc*T)] arrival counters (self-resetting)
+  int* layer_done;    // [SMART_MAX_DEPTH] rows merged per layer (self-resetting)
   float2* rowstat;    // [cap_rows] (M, Z) of the last expanded layer
   Cand* cand;         // [d][cap_rows*k]
   float* cand_b;      // [d][cap_rows*k] benefit
   int* cand_adm;      // [d][cap_rows*k] admitted flag
   int2* cand_rs;      // [d][cap_rows] (local request, frontier slot) of each candidate row
+
+  // ---- cost model tables (fp64, host-built with the same formula; N in [0, n_cost)) ----
+  const double* cost_tab;   // cost(N) = C_draft(N) + C_verify(N)         Eqs.(4),(5)
+  const double* dc_tab;     // marginal cost at N (DERIVATIVE Eq.(15) / DIFFERENCE)
+  int n_cost;
+  int sort_cap;             // key capacity of the selection sort (power of two)
+  int min_units;            // chunks per CTA at least in the streaming kernels
+  long long sat_from;       // smallest N whose exponent was clamped (Q17)
+
+  // ---- optional timing probes (SMART_TIMING=1): globaltimer ns, see probe() ----
+  unsigned long long* dbg;
 
   // ---- select / stats ----
   DevTrace* trace;    // [SMART_MAX_DEPTH]
@@ -118,6 +131,21 @@ __device__ __forceinline__ bool better(float av, int ai, float bv, int bi) {
   return av > bv || (av == bv && ai < bi);
 }
 
+// release/acquire fences at GPU scope (cheaper than the sequentially consistent __threadfence)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// arrival counter: one thread, after a CTA barrier, publishes the CTA's writes (release, cumulative
+// over the barrier) and acquires the other arrivals' writes (CUTLASS-semaphore pattern)
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// 64-bit top-k key: larger key = better (value desc, then index asc) — one compare per step
+__device__ __forceinline__ unsigned long long tk_key(float v, int i);
+__device__ __forceinline__ float tk_val(unsigned long long key);
+__device__ __forceinline__ int tk_idx(unsigned long long key);
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -128,6 +156,15 @@ __device__ __forceinline__ uint32_t float_orderable(float f) {
   uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+__device__ __forceinline__ unsigned long long tk_key(float v, int i) {
+  return ((unsigned long long)float_orderable(v) << 32) | (unsigned long long)(0xffffffffu - (unsigned)i);
+}
+__device__ __forceinline__ float tk_val(unsigned long long key) {
+  const uint32_t o = (uint32_t)(key >> 32);
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+__device__ __forceinline__ int tk_idx(unsigned long long key) { return (int)(0xffffffffu - (uint32_t)key); }
+constexpr unsigned long long kKeySentinel = 0x007fffff80000000ull;  // tk_key(-inf, INT_MAX)
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -148,6 +185,24 @@ __device__ __forceinline__ int warp_sum_i(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// probe slots: 0 min CTA start, 1 max CTA start, 2 max stream end, 3 last merge start,
+// 4 last merge end, 5 select start, 6 select end, 7 max CTA end, 8 first merge start
+__device__ __forceinline__ void probe_min(const Params& P, int slot) {
+  if (P.dbg) atomicMin(&P.dbg[slot], gtime());
+}
+__device__ __forceinline__ void probe_max(const Params& P, int slot) {
+  if (P.dbg) atomicMax(&P.dbg[slot], gtime());
+}
+// cycle stamps (clock64) of one thread into dbg[32 + slot]
+__device__ __forceinline__ void stamp(const Params& P, bool on, int slot) {
+  if (P.dbg && on) P.dbg[32 + slot] = clock64();
 }
 
 // ---- cost model (fp64; Eqs.(4),(5),(15); clamp Q17) ----
@@ -172,17 +227,20 @@ __device__ __forceinline__ double speed_b(const Params& P, double E, long long N
 
 // ---- kernels (host launchers in api.cu) ----
 __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32_t* root_pos);
-void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool aligned,
-                   int grid, cudaStream_t s);
+void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool tma,
+                   bool fuse_select, int grid, cudaStream_t s);
+size_t layer_smem_bytes(int cpr, int k);
 int expand_occupancy();
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
-size_t select_smem_bytes(int sort_cap);
+size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks);
 cudaError_t select_set_smem(size_t bytes);
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok,
                  int32_t* tree_len, cudaStream_t s);
-void launch_verify(const Params& P, const void* target, long long ld_bytes, bool aligned,
+void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma,
                    int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s);
+size_t verify_smem_bytes(int T);
 int verify_occupancy();
+cudaError_t mask_set_smem();
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
                             cudaStream_t s);
 
