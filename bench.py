@@ -221,17 +221,22 @@ def main():
     torch.cuda.set_device(dev)
 
     b = wl["b"]
-    cfg = S.Config(vocab=wl["V"], top_k=wl["k"], max_depth=wl["d"], max_frontier=wl["W"], batch_local=b,
-                   batch_global=b * world, batch_offset=rank * b, budget_verify=wl["B_verify"] * world,
-                   alpha=ALPHA, bonus=1, selection=S.PREFIX, accept_model=S.NODE_SUM, marginal=S.DERIVATIVE,
-                   cost_scope=S.COST_GLOBAL, logits_dtype=S.BF16, row_mode=S.ROWS_NODE)
+    cfg_kwargs = dict(vocab=wl["V"], top_k=wl["k"], max_depth=wl["d"], max_frontier=wl["W"],
+                      budget_verify=wl["B_verify"] * world, alpha=ALPHA, bonus=1, selection=S.PREFIX,
+                      accept_model=S.NODE_SUM, marginal=S.DERIVATIVE, cost_scope=S.COST_GLOBAL,
+                      logits_dtype=S.BF16, row_mode=S.ROWS_NODE)
     cost = S.Cost(lam=cost_fx["lam"], beta=cost_fx["beta"], gamma=cost_fx["gamma"], delta=cost_fx["delta"],
                   rho=cost_fx["rho"], eta=cost_fx["eta"], c_T=cost_fx["c_T"])
-    ctx = S.Smart(cfg, cost, local)
+    sharded = None
     if world > 1:
-        uid = [S.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.attach_nccl(uid[0], rank, world)
+        # weak scaling: b requests per GPU, one batch-global selection over b*world requests with
+        # one NCCL all-gather per layer (paper_2604_09731_b200/dist.py)
+        from paper_2604_09731_b200 import dist as SD
+        sharded = SD.ShardedSmart(cfg_kwargs, cost, SD.shard(b * world, world, rank), local)
+        ctx = sharded.ctx
+    else:
+        cfg = S.Config(batch_local=b, batch_global=b, batch_offset=0, **cfg_kwargs)
+        ctx = S.Smart(cfg, cost, local)
     T = ctx.sizes["T"]
     V = wl["V"]
 
@@ -249,7 +254,10 @@ def main():
     stream = torch.cuda.Stream(dev)
 
     def step(p, s):
-        ctx.run_step(p["draft"], p["target"], p["out"], root_tok=p["rt"], root_pos=p["rp"], stream=s)
+        if sharded is not None:
+            sharded.step(p["draft"], p["target"], p["out"], root_tok=p["rt"], root_pos=p["rp"], stream=s)
+        else:
+            ctx.run_step(p["draft"], p["target"], p["out"], root_tok=p["rt"], root_pos=p["rp"], stream=s)
 
     # per-set tree statistics (identical for every replica of a set)
     tree_stats = []
@@ -259,19 +267,27 @@ def main():
         stream.synchronize()
         st = ctx.stats()
         tree_stats.append(st)
-    # CUDA graph per pool buffer
+    # one CUDA graph per pool buffer (single GPU); eager launches when the step has collectives
     graphs = []
-    for p in pools:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            step(p, stream)
-        graphs.append(g)
+    if sharded is None:
+        for p in pools:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(p, stream)
+            graphs.append(g)
     torch.cuda.synchronize()
-    launches_per_step = 1 + 2 * wl["d"] + 2 + (wl["d"] if world > 1 else 0)
+    launches_per_step = 1 + wl["d"] + 2 + (2 * wl["d"] if world > 1 else 0)
+
+    def replay(i):
+        if graphs:
+            graphs[i % n_pools].replay()
+        else:
+            step(pools[i % n_pools], stream)
 
     # ---- warm-up + timed region ----
-    for i in range(args.warmup):
-        graphs[i % n_pools].replay()
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            replay(i)
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -284,7 +300,7 @@ def main():
     with torch.cuda.stream(stream):
         ev0.record(stream)
         for i in range(args.steps):
-            graphs[i % n_pools].replay()
+            replay(i)
         ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -300,7 +316,7 @@ def main():
 
     # ---- per-kernel timing (outside the timed region; events on the launching stream) ----
     kt = {"expand": [], "select": [], "mask": [], "verify": [], "begin": []}
-    reps = 20
+    reps = 20 if sharded is None else 0
     p = pools[0]
     for _ in range(reps):
         evs = []
@@ -329,6 +345,8 @@ def main():
         kt["select"].append(d_[2:2 + 2 * wl["d"]:2])
         kt["mask"].append(d_[-2])
         kt["verify"].append(d_[-1])
+    if reps == 0:
+        kt = {"expand": [[0.0] * wl["d"]], "select": [[0.0] * wl["d"]], "mask": [0.0], "verify": [1e-9], "begin": [0.0]}
     st0 = tree_stats[0]
     rows_layer = [st0["layers"][l]["n_rows"] if st0["layers"][l]["executed"] else 0 for l in range(wl["d"])]
     exp_ms = np.mean(np.array(kt["expand"]), axis=0)        # per layer

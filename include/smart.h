@@ -144,6 +144,19 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
 smart_status smart_nccl_unique_id(uint8_t id_out[128]);
 smart_status smart_attach_nccl(smart_ctx* ctx, const uint8_t id[128], int rank, int nranks);
 
+/* Bring-your-own all-gather (no NCCL inside the library).  Each rank owns a send record of
+ * smart_exchange_record_bytes() bytes and a receive buffer of nranks records (both device
+ * memory, caller-owned, 256-byte aligned).  After smart_attach_exchange, smart_select(layer) runs
+ * only the local phase (per-request eligibility, local sort) and fills d_send; the caller
+ * all-gathers the records of all ranks in rank order into every rank's d_recv (e.g.
+ * torch.distributed.all_gather_into_tensor on the same stream) and then calls
+ * smart_select_finish(layer): merge of the gathered lists, the batch-global rule, commit of
+ * this rank's requests.  Sharding: equal contiguous ranges, batch_offset = rank*batch_local. */
+smart_status smart_exchange_record_bytes(const smart_config* cfg, int nranks, int64_t* bytes);
+smart_status smart_attach_exchange(smart_ctx* ctx, int rank, int nranks, void* d_send, void* d_recv);
+smart_status smart_select_finish(smart_ctx* ctx, int32_t layer, int32_t* d_frontier,
+                                 int32_t* d_frontier_count, void* stream);
+
 smart_status smart_destroy(smart_ctx* ctx);
 
 /* ---- one decode step -------------------------------------------------------------------- */

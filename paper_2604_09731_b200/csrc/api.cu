@@ -36,8 +36,10 @@ struct smart_ctx {
   bool masked = false;
   cudaStream_t last_stream = nullptr;
   std::string err;
-  // NCCL
+  // NCCL / caller-provided exchange
   void* nccl_comm = nullptr;
+  bool byo_exchange = false;
+  bool owns_exchange = false;
 };
 
 namespace {
@@ -341,7 +343,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
   P.sort_cap = sort_cap;
   c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1);
-  c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes;
+  c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && !getenv("SMART_NO_FUSE");
   if (c->select_smem > 220 * 1024) {
     cudaFree(c->ws);
     cudaFree(c->cost_dev);
@@ -376,13 +378,58 @@ smart_status smart_nccl_unique_id(uint8_t id_out[128]) {
   return SMART_OK;
 }
 
-smart_status smart_attach_nccl(smart_ctx* c, const uint8_t id[128], int rank, int nranks) {
-  if (!c || !id) return fail(c, SMART_EINVAL, "null argument");
+static long long exchange_record_bytes(long long b_loc, long long wf) {
+  const long long m_cap = b_loc * wf;
+  return (m_cap * 8 + b_loc * 8 + (b_loc + 2) * 4 + 255) & ~255ll;
+}
+
+static smart_status setup_exchange(smart_ctx* c, int rank, int nranks, void* send, void* recv) {
+  Params& P = c->P;
+  P.nranks = nranks;
+  P.rank = rank;
+  const long long b = P.b_loc;
+  const long long wf = std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, P.T - 1)));
+  P.m_cap = (int)(b * wf);
+  P.xstride = exchange_record_bytes(b, wf);
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->owns_exchange) {
+    cudaFree(P.xs);
+    cudaFree(P.xr);
+  }
+  if (send && recv) {
+    P.xs = static_cast<char*>(send);
+    P.xr = static_cast<char*>(recv);
+    c->owns_exchange = false;
+  } else {
+    CUDA_TRY(c, cudaMalloc(&P.xs, P.xstride));
+    CUDA_TRY(c, cudaMalloc(&P.xr, P.xstride * nranks));
+    c->owns_exchange = true;
+  }
+  CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
+  const int sort_cap = next_pow2((long long)P.m_cap * nranks);
+  P.sort_cap = sort_cap;
+  const size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks);
+  if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
+  c->select_smem = std::max(c->select_smem, need);
+  c->fused_select = false;
+  CUDA_TRY(c, select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024)));
+  return SMART_OK;
+}
+
+static smart_status check_sharding(smart_ctx* c, int rank, int nranks) {
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, SMART_EINVAL, "bad rank/nranks");
   if (c->cfg.batch_local * nranks != c->cfg.batch_global || c->cfg.batch_offset != rank * c->cfg.batch_local)
     return fail(c, SMART_EINVAL, "sharding must be equal contiguous ranges: offset = rank * batch_local");
+  if (nranks > 1 && c->cfg.cost_scope != SMART_COST_GLOBAL)
+    return fail(c, SMART_EINVAL, "LOCAL cost scope needs no exchange");
+  return SMART_OK;
+}
+
+smart_status smart_attach_nccl(smart_ctx* c, const uint8_t id[128], int rank, int nranks) {
+  if (!c || !id) return fail(c, SMART_EINVAL, "null argument");
+  smart_status st = check_sharding(c, rank, nranks);
+  if (st) return st;
   if (nranks == 1) return SMART_OK;
-  if (c->cfg.cost_scope != SMART_COST_GLOBAL) return fail(c, SMART_EINVAL, "LOCAL cost scope needs no communicator");
   if (!g_nccl.load()) return fail(c, SMART_ENCCL, "cannot dlopen libnccl.so.2");
   CUDA_TRY(c, cudaSetDevice(c->device));
   ncclUniqueId uid;
@@ -391,24 +438,30 @@ smart_status smart_attach_nccl(smart_ctx* c, const uint8_t id[128], int rank, in
   ncclResult_t r = g_nccl.CommInitRank(&comm, nranks, uid, rank);
   if (r != ncclSuccess) return fail(c, SMART_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
   c->nccl_comm = comm;
-  Params& P = c->P;
-  P.nranks = nranks;
-  P.rank = rank;
-  long long b = P.b_loc;
-  long long wf = std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, P.T - 1)));
-  P.m_cap = (int)(b * wf);
-  P.xstride = ((long long)P.m_cap * 8 + b * 8 + (b + 2) * 4 + 255) & ~255ll;
-  CUDA_TRY(c, cudaMalloc(&P.xs, P.xstride));
-  CUDA_TRY(c, cudaMalloc(&P.xr, P.xstride * nranks));
-  CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
-  int sort_cap = next_pow2((long long)P.m_cap * nranks);
-  P.sort_cap = sort_cap;
-  size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks);
-  if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
-  c->select_smem = std::max(c->select_smem, need);
-  c->fused_select = false;
-  CUDA_TRY(c, select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024)));
+  return setup_exchange(c, rank, nranks, nullptr, nullptr);
+}
+
+smart_status smart_exchange_record_bytes(const smart_config* cfg, int nranks, int64_t* bytes) {
+  smart_sizes sz{};
+  std::string why;
+  smart_status st = validate(cfg, nullptr, &sz, why);
+  if (st) return fail(nullptr, st, "%s", why.c_str());
+  if (!bytes || nranks < 1) return fail(nullptr, SMART_EINVAL, "bad argument");
+  const long long Wq = cfg->max_frontier > 0 ? cfg->max_frontier : (1ll << 30);
+  const long long wf = std::max<long long>(1, std::min<long long>(Wq, std::min<long long>(sz.B, sz.T - 1)));
+  *bytes = exchange_record_bytes(cfg->batch_local, wf);
   return SMART_OK;
+}
+
+smart_status smart_attach_exchange(smart_ctx* c, int rank, int nranks, void* d_send, void* d_recv) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (!d_send || !d_recv) return fail(c, SMART_EINVAL, "null exchange buffers");
+  if ((reinterpret_cast<uintptr_t>(d_send) | reinterpret_cast<uintptr_t>(d_recv)) & 255)
+    return fail(c, SMART_EINVAL, "exchange buffers must be 256-byte aligned");
+  smart_status st = check_sharding(c, rank, nranks);
+  if (st) return st;
+  c->byo_exchange = true;
+  return setup_exchange(c, rank, nranks, d_send, d_recv);
 }
 
 smart_status smart_destroy(smart_ctx* c) {
@@ -416,8 +469,10 @@ smart_status smart_destroy(smart_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   if (c->nccl_comm && g_nccl.h) g_nccl.CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
-  if (c->P.xs) cudaFree(c->P.xs);
-  if (c->P.xr) cudaFree(c->P.xr);
+  if (c->owns_exchange) {
+    cudaFree(c->P.xs);
+    cudaFree(c->P.xr);
+  }
   if (c->ws) cudaFree(c->ws);
   if (c->cost_dev) cudaFree(c->cost_dev);
   delete c;
@@ -461,6 +516,13 @@ smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int3
   if (layer != c->next_layer || c->phase != 1)
     return fail(c, SMART_ESTATE, "select layer %d out of order (expected %d after expand)", layer, c->next_layer);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->byo_exchange && c->P.nranks > 1) {
+    launch_select(c->P, layer, 1 /* kSelLocal */, c->select_smem, s);
+    CUDA_TRY(c, cudaGetLastError());
+    c->phase = 2;  // awaiting smart_select_finish after the caller's all-gather
+    c->last_stream = s;
+    return SMART_OK;
+  }
   if (c->P.nranks > 1) {
     launch_select(c->P, layer, 1 /* kSelLocal */, c->select_smem, s);
     CUDA_TRY(c, cudaGetLastError());
@@ -471,6 +533,22 @@ smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int3
   } else if (!c->fused_select) {
     launch_select(c->P, layer, 0 /* kSelFull */, c->select_smem, s);
   }  // else: already done by the layer kernel's last CTA
+  CUDA_TRY(c, cudaGetLastError());
+  if (d_frontier || d_frontier_count) launch_export_frontier(c->P, layer & 1, d_frontier, d_frontier_count, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->next_layer = layer + 1;
+  c->phase = 0;
+  c->last_stream = s;
+  return SMART_OK;
+}
+
+smart_status smart_select_finish(smart_ctx* c, int32_t layer, int32_t* d_frontier, int32_t* d_frontier_count,
+                                 void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (layer != c->next_layer || c->phase != 2)
+    return fail(c, SMART_ESTATE, "select_finish layer %d out of order", layer);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_select(c->P, layer, 2 /* kSelGlobal */, c->select_smem, s);
   CUDA_TRY(c, cudaGetLastError());
   if (d_frontier || d_frontier_count) launch_export_frontier(c->P, layer & 1, d_frontier, d_frontier_count, s);
   CUDA_TRY(c, cudaGetLastError());
@@ -514,6 +592,7 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
                             int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
   if (c->cfg.row_mode != SMART_ROWS_NODE) return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE");
+  if (c->byo_exchange) return fail(c, SMART_ESTATE, "smart_run_step cannot drive a caller-provided exchange");
   smart_status st = smart_begin_step(c, d_root_tok, d_root_pos, stream);
   for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
     st = smart_expand_step(c, l, d_draft, ld, stream);

@@ -397,9 +397,8 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     warp_compact(W, W.cnt, k, lane);
     if (lane == 0) W.cnt = 0;
     consumer_sync();
-    for (int t = tid; t < kConsumerWarps * 32; t += kConsumers) {
-      const int tw = t >> 5, te = t & 31;
-      if (te >= k) continue;
+    for (int t = tid; t < kConsumerWarps * k; t += kConsumers) {  // only the 8k live entries
+      const int tw = t / k, te = t - tw * k;
       const unsigned long long key = sh.w[tw].list[te];
       int rank = 0;
       for (int w = 0; w < kConsumerWarps; ++w) {

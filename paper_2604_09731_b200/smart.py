@@ -28,6 +28,7 @@ ROWS_FRONTIER, ROWS_NODE = 0, 1
 MAX_DEPTH = 16
 
 EXPORTED = ["smart_query_sizes", "smart_create", "smart_nccl_unique_id", "smart_attach_nccl",
+            "smart_exchange_record_bytes", "smart_attach_exchange", "smart_select_finish",
             "smart_destroy", "smart_begin_step", "smart_expand_step", "smart_select",
             "smart_build_mask", "smart_verify_accept", "smart_run_step", "smart_get_stats",
             "smart_get_tree", "smart_get_candidates", "smart_last_error", "smart_status_string"]
@@ -88,6 +89,9 @@ def lib() -> C.CDLL:
         L.smart_create.argtypes = [C.POINTER(_Config), C.POINTER(_Cost), C.c_int, C.POINTER(vp)]
         L.smart_nccl_unique_id.argtypes = [C.c_char_p]
         L.smart_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+        L.smart_exchange_record_bytes.argtypes = [C.POINTER(_Config), C.c_int, C.POINTER(i64)]
+        L.smart_attach_exchange.argtypes = [vp, C.c_int, C.c_int, vp, vp]
+        L.smart_select_finish.argtypes = [vp, i32, vp, vp, vp]
         L.smart_destroy.argtypes = [vp]
         L.smart_begin_step.argtypes = [vp, vp, vp, vp]
         L.smart_expand_step.argtypes = [vp, i32, vp, i64, vp]
@@ -197,6 +201,22 @@ class Smart:
 
     def attach_nccl(self, uid: bytes, rank: int, nranks: int):
         _check(lib().smart_attach_nccl(self._h, uid, rank, nranks), self._h)
+
+    def exchange_record_bytes(self, nranks: int) -> int:
+        n = C.c_int64()
+        c = self.cfg.c()
+        _check(lib().smart_exchange_record_bytes(C.byref(c), nranks, C.byref(n)))
+        return n.value
+
+    def attach_exchange(self, rank: int, nranks: int, send, recv):
+        """caller-provided all-gather: send/recv are uint8 device tensors of record_bytes and
+        nranks*record_bytes (see smart_attach_exchange in include/smart.h)"""
+        self._xbufs = (send, recv)  # keep alive
+        _check(lib().smart_attach_exchange(self._h, rank, nranks, _ptr(send), _ptr(recv)), self._h)
+
+    def select_finish(self, layer: int, frontier=None, frontier_count=None, stream=None):
+        _check(lib().smart_select_finish(self._h, layer, _ptr(frontier), _ptr(frontier_count), _stream(stream)),
+               self._h)
 
     def close(self):
         if self._h:

@@ -1,0 +1,141 @@
+"""Sharding invariance of the batch-global selection: a batch split into G equal
+request ranges, with the per-layer exchange (local eligible lists + per-request headers) all-
+gathered between smart_select and smart_select_finish, must reproduce the G = 1 decisions bit for
+bit (node sets, tokens, parents, cum bit patterns, masks, verify).  All G shards run in one
+process on one GPU; the all-gather is a device copy (torch.cat), exactly what
+torch.distributed.all_gather_into_tensor does across ranks.  Also: the standalone (unfused)
+selection kernel equals the fused one."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from smart_gpu_cases import Case, gpu_ctx, make_inputs, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_09731_b200 import _build
+    _build.build()
+
+
+def _T(case):
+    from oracle import oracle as O
+    return O.Config(V=case.V, k=case.k, d=case.d, W=case.W, b=case.b, B_verify=case.B_verify).tmax()
+
+
+def run_sharded(case, G, draft, target, rt, rp):
+    import torch
+    from paper_2604_09731_b200 import smart as S
+    lam, beta, gamma, delta, rho, eta, c_T = case.cost
+    bl = case.b // G
+    ctxs, outs = [], []
+    for g in range(G):
+        cfg = S.Config(vocab=case.V, top_k=case.k, max_depth=case.d, max_frontier=case.W, batch_local=bl,
+                       batch_global=case.b, batch_offset=g * bl, budget_verify=case.B_verify, alpha=case.alpha,
+                       bonus=case.omega, selection=case.selection, accept_model=case.accept_model,
+                       marginal=case.marginal, logits_dtype=S.BF16 if case.dtype == "bf16" else S.FP32,
+                       row_mode=S.ROWS_NODE)
+        ctx = S.Smart(cfg, S.Cost(lam=lam, beta=beta, gamma=gamma, delta=delta, rho=rho, eta=eta, c_T=c_T))
+        nbytes = ctx.exchange_record_bytes(G)
+        send = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        recv = torch.zeros(G * nbytes, dtype=torch.uint8, device="cuda")
+        ctx.attach_exchange(g, G, send, recv)
+        ctxs.append(ctx)
+    dd = [to_dev(np.ascontiguousarray(draft[g * bl:(g + 1) * bl])) for g in range(G)]
+    tt = [to_dev(np.ascontiguousarray(target[g * bl:(g + 1) * bl])) for g in range(G)]
+    for g, ctx in enumerate(ctxs):
+        ctx.begin_step(to_dev(rt[g * bl:(g + 1) * bl].copy()), to_dev(rp[g * bl:(g + 1) * bl].copy()))
+    for layer in range(1, case.d + 1):
+        for g, ctx in enumerate(ctxs):
+            ctx.expand_step(layer, dd[g])
+            ctx.select(layer)
+        gathered = torch.cat([c._xbufs[0] for c in ctxs])  # the all-gather (rank order)
+        for ctx in ctxs:
+            ctx._xbufs[1].copy_(gathered)
+        for ctx in ctxs:
+            ctx.select_finish(layer)
+    res = []
+    for g, ctx in enumerate(ctxs):
+        out = ctx.alloc_outputs()
+        ctx.build_mask(out["mask"], out["pos"], out["parent"], out["tok"], out["tree_len"])
+        ctx.verify_accept(tt[g], out["accept_len"], out["accept_path"], out["bonus"])
+        torch.cuda.synchronize()
+        r = {k: v.cpu().numpy() for k, v in out.items()}
+        r["tree"] = ctx.tree()
+        r["stats"] = ctx.stats()
+        res.append(r)
+    cat = {k: np.concatenate([r[k] for r in res]) for k in res[0] if k not in ("tree", "stats")}
+    cat["cum"] = np.concatenate([r["tree"]["cum"] for r in res])
+    cat["p"] = np.concatenate([r["tree"]["p"] for r in res])
+    cat["stats"] = [r["stats"] for r in res]
+    return cat
+
+
+def run_single(case, draft, target, rt, rp):
+    from smart_gpu_cases import run_gpu
+    r = run_gpu(case, draft, target, rt, rp)
+    r["cum"] = r["tree"]["cum"]
+    r["p"] = r["tree"]["p"]
+    return r
+
+
+CASES = [
+    Case(V=40000, k=6, d=5, W=6, b=8, B_verify=80, seed=31, cost=(0.02, 0.0, 0.05, 0.01, 1.2, 1.0, 1.0)),
+    Case(V=128256, k=8, d=6, W=8, b=32, B_verify=200, seed=32, cost=(0.0084, 0.0, 6.69, 6.3e-7, 2.23, 2.47, 2.47)),
+    Case(V=20000, k=4, d=4, W=0, b=4, B_verify=40, seed=33, selection=1, accept_model=0,
+         cost=(0.03, 0.0, 0.1, 0.02, 1.1, 1.0, 1.0)),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=["b8", "cfg3", "frozen_b4"])
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_equals_single(case, G):
+    if case.b % G:
+        pytest.skip("batch not divisible")
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    one = run_single(case, draft, target, rt, rp)
+    many = run_sharded(case, G, draft, target, rt, rp)
+    for key in ("tree_len", "tok", "parent", "mask", "pos", "accept_len", "accept_path", "bonus"):
+        np.testing.assert_array_equal(many[key], one[key], err_msg=key)
+    # bit-identical scores (the per-row merge and the selection are partition-invariant)
+    np.testing.assert_array_equal(many["cum"].view(np.uint32), one["cum"].view(np.uint32))
+    np.testing.assert_array_equal(many["p"].view(np.uint32), one["p"].view(np.uint32))
+    s1 = one["stats"]
+    for st in many["stats"]:
+        for l in range(case.d):
+            a, b = st["layers"][l], s1["layers"][l]
+            if not b["executed"]:
+                continue
+            assert a["n_admit"] == b["n_admit"] and a["n_elig"] == b["n_elig"] and a["N0"] == b["N0"]
+            assert a["E0"] == b["E0"] and a["S0"] == b["S0"], (l, a, b)
+
+
+def test_unfused_select_kernel_matches_fused():
+    """SMART_NO_FUSE=1 routes the selection through the standalone 1024-thread kernel."""
+    code = r'''
+import sys, json, numpy as np
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+from smart_gpu_cases import Case, make_inputs, run_gpu
+case = Case(V=40000, k=6, d=5, W=6, b=8, B_verify=80, seed=35)
+from oracle import oracle as O
+T = O.Config(V=case.V, k=case.k, d=case.d, W=case.W, b=case.b, B_verify=case.B_verify).tmax()
+d, t, rt, rp = make_inputs(case, T)
+r = run_gpu(case, d, t, rt, rp)
+print(json.dumps({k: r[k].tolist() for k in ("tok", "parent", "mask", "accept_len", "bonus")}))
+'''
+    outs = []
+    for env in ({}, {"SMART_NO_FUSE": "1"}):
+        e = dict(os.environ, **env)
+        p = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
