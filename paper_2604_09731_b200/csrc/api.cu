@@ -18,6 +18,14 @@
 
 using namespace smart;
 
+bool smart::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SMART_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 struct smart_ctx {
   smart_config cfg;
   smart_cost cost;
@@ -131,6 +139,8 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
   int ce = kChunkBytes / esz;
   int cpr = (c->vocab + ce - 1) / ce;
   if (cpr > kMaxCpr) return bad("vocab too large for the chunk scheduler (> 64 chunks of 16 KiB per row)");
+  if (std::max<long long>(cap_rows, (long long)c->batch_local * T) * cpr >= (1ll << 31))
+    return bad("streamed (row, chunk) units exceed 2^31");
   if (s) {
     s->B = B;
     s->T = (int)T;
@@ -251,6 +261,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.root_pos, b * 4);
   for (int q = 0; q < 2; ++q) {
     add(&P.fr[q], cap * 8);
+    add(&P.fr_cum[q], cap * 4);
     add(&P.fr_cnt[q], b * 4);
     add(&P.fr_off[q], b * 4);
     add(&P.fr_total[q], 4);
@@ -275,6 +286,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.vseglen, vrows * cpr * 4);
   add(&P.vrow_arg, vrows * 4);
   add(&P.vrow_off, (b + 1) * 4);
+  add(&P.vrow_rn, vrows * 8);
   add(&P.req_done, b * 4);
   size_t total = 0;
   for (auto& it : items) total += (it.bytes + 255) & ~size_t(255);
@@ -331,7 +343,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   P.min_units = getenv("SMART_MIN_UNITS") ? atoi(getenv("SMART_MIN_UNITS")) : 2;
   if (P.min_units < 1) P.min_units = 1;
   if (getenv("SMART_TIMING")) {
-    e = cudaMalloc(&P.dbg, 64 * sizeof(unsigned long long));
+    e = cudaMalloc(&P.dbg, 1024 * sizeof(unsigned long long));
     if (e != cudaSuccess) P.dbg = nullptr;
   }
   // launch geometry: persistent streaming grids sized to the SM count
@@ -483,7 +495,7 @@ smart_status smart_begin_step(smart_ctx* c, const int32_t* d_root_tok, const int
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int thr = 256, grid = (c->P.b_loc + thr - 1) / thr;
-  begin_step_kernel<<<grid, thr, 0, s>>>(c->P, d_root_tok, d_root_pos);
+  launch_k(begin_step_kernel, dim3(grid), dim3(thr), 0, s, c->P, d_root_tok, d_root_pos);
   CUDA_TRY(c, cudaGetLastError());
   c->next_layer = 1;
   c->phase = 0;
@@ -606,10 +618,10 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
 extern "C" int smart_debug_probes(smart_ctx* c, unsigned long long* host16, int reset) {
   if (!c || !c->P.dbg) return -1;
   cudaStreamSynchronize(c->last_stream);
-  if (host16) cudaMemcpy(host16, c->P.dbg, 64 * 8, cudaMemcpyDeviceToHost);
+  if (host16) cudaMemcpy(host16, c->P.dbg, 1024 * 8, cudaMemcpyDeviceToHost);
   if (reset) {
-    unsigned long long init[64];
-    for (int i = 0; i < 64; ++i) init[i] = (i == 0 || i == 8) ? ~0ull : 0ull;
+    static unsigned long long init[1024];
+    for (int i = 0; i < 1024; ++i) init[i] = (i == 0 || i == 8 || (i >= 64 && !(i & 1))) ? ~0ull : 0ull;
     cudaMemcpy(c->P.dbg, init, sizeof init, cudaMemcpyHostToDevice);
   }
   return 0;

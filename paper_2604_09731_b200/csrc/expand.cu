@@ -85,11 +85,12 @@ __device__ __forceinline__ void load_direct(const char* row, int chunk_base, int
   }
 }
 
-// logits row of frontier row `row` (layer parity `par`)
+// logits row of frontier row `row` (layer parity `par`); rows [row0, row0 + kStageRows) use the
+// frontier entries staged in shared memory
 __device__ __forceinline__ const char* row_ptr(const Params& P, int par, const char* base, long long ld_bytes,
-                                              int row) {
+                                              int row, const int2* rfe, int row0) {
   if (P.row_mode == SMART_ROWS_NODE) {
-    const int2 fe = P.fr[par][row];
+    const int2 fe = (row - row0 < kStageRows) ? rfe[row - row0] : P.fr[par][row];
     return base + ((long long)fe.x * P.T + fe.y) * ld_bytes;
   }
   return base + (long long)row * ld_bytes;
@@ -99,43 +100,33 @@ __device__ __forceinline__ const char* row_ptr(const Params& P, int par, const c
 struct WarpTopk {
   unsigned long long buf[kSegBuf];  // candidates of the current segment (appended; compacted)
   unsigned long long list[kMaxK];   // compacted top-k, sorted best first
-  int cnt;
 };
 
 struct ExpandShared {
-  unsigned long long tau;  // CTA threshold hint (best k-th key bound of any warp)
-  int last, last_layer;
+  int2 rfe[kStageRows];  // frontier entries of the CTA's first rows
+  unsigned pub[2][kConsumerWarps * 4];  // per chunk (double-buffered): top-j lane maxima of each warp
+  unsigned long long cl[kConsumerWarps * kMaxK];  // segment end: each warp's top-k (distinct sentinels)
+  int last_layer;
   WarpTopk w[kConsumerWarps];
-  float red[kConsumerWarps];
-  int2 fe;
-  float pc;
-  int nseg;
 };
 
 // row-merge staging, carved from the dynamic shared memory after ExpandShared (sized by cpr, k)
 struct MergeStage {
-  float2* ms;                // [cpr * 8] softmax partials
-  unsigned long long* keys;  // [cpr * k] segment lists
-  int* seglen;               // [cpr]
-  int* segstart;             // [cpr] chunk index of each existing segment
+  unsigned long long* keys;  // [cpr * k] segment lists (valid at segment-start chunks)
+  unsigned long long* surv;  // [cpr * k] survivors of the threshold
 };
 
-__host__ __device__ inline size_t merge_stage_bytes(int cpr, int k) {
-  return (size_t)cpr * kConsumerWarps * 8 + (size_t)cpr * k * 8 + (size_t)cpr * 8 + 16;
-}
+__host__ __device__ inline size_t merge_stage_bytes(int cpr, int k) { return (size_t)cpr * k * 16; }
 
 __device__ inline MergeStage merge_stage(char* base, int cpr, int k) {
   MergeStage m;
-  m.ms = reinterpret_cast<float2*>(base);
-  m.keys = reinterpret_cast<unsigned long long*>(m.ms + cpr * kConsumerWarps);
-  m.seglen = reinterpret_cast<int*>(m.keys + cpr * k);
-  m.segstart = m.seglen + cpr;
+  m.keys = reinterpret_cast<unsigned long long*>(base);
+  m.surv = m.keys + (size_t)cpr * k;
   return m;
 }
 
-// Warp-level compaction: list <- top-k of buf[0..n) by rank counting (keys distinct, except
-// sentinels which never rank inside the top-k of a buffer holding >= k real keys); the buffer
-// then restarts from the list.
+// Warp-level compaction: list <- top-k of buf[0..n) by rank counting (keys distinct); ranks >= n
+// are sentinels.  The buffer then restarts from the list (caller sets its count to min(n, k)).
 __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane) {
   if (lane < k) w.list[lane] = kKeySentinel;
   __syncwarp();
@@ -148,70 +139,113 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
   }
   __syncwarp();
   if (lane < k) w.buf[lane] = w.list[lane];
-  if (lane == 0) w.cnt = min(n, k);
   __syncwarp();
 }
 
-// ---- row merge by the CTA that completed the row (256 consumer threads) ----
-// Everything the merge needs is fetched in one wave into shared memory, then merged by rank.
-__device__ void merge_row(const Params& P, int layer, int par, int row, ExpandShared& sh, MergeStage st) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// ---- row merge by one warp of the CTA that completed the row (no CTA barriers) ----
+// One load wave (partials, segment lengths, segment lists, frontier entry and its cum), then:
+// M = max, Z = sum s*exp(m - M) with an association fixed by cpr; T = the best k-th entry over
+// the segment lists (a lower bound of the row's k-th best key, every list holding its segment's
+// top-k); the entries >= T are ranked among themselves and the top k written with p and cum.
+__device__ void merge_row_warp(const Params& P, int layer, int par, int row, MergeStage st) {
+  const int lane = threadIdx.x & 31;
+  const bool sp = (row == 0 && lane == 0);
+  stamp(P, sp, 24);
   const int k = P.k, cpr = P.cpr;
-  const int npart = cpr * kConsumerWarps;
+  const int npart = cpr * kConsumerWarps;  // <= 512
+  const int nkey = cpr * k;                // <= 2048
+  // ---- load wave ----
   const float2* ms = P.ms + (size_t)row * npart;
-  for (int q = tid; q < npart; q += kConsumers) st.ms[q] = __ldcg(&ms[q]);
-  for (int c = tid; c < cpr; c += kConsumers) {
-    st.seglen[c] = __ldcg(&P.seglen[(size_t)row * cpr + c]);
-    P.seglen[(size_t)row * cpr + c] = 0;  // self-cleaning for the next use
-  }
-  for (int q = tid; q < cpr * k; q += kConsumers) st.keys[q] = __ldcg(&P.segkey[(size_t)row * cpr * k + q]);
-  if (tid == 0) {
-    const int2 fe = P.fr[par][row];
-    sh.fe = fe;
-    sh.pc = P.cum[(size_t)fe.x * P.T + fe.y];
-    sh.nseg = 0;
-  }
-  consumer_sync();
-  for (int c = tid; c < cpr; c += kConsumers)
-    if (st.seglen[c] > 0) st.segstart[atomicAdd(&sh.nseg, 1)] = c;
-  // (1) softmax normaliser: M = max, Z = sum s*exp(m - M), association fixed by cpr only
-  float m = -INFINITY;
-  for (int q = tid; q < npart; q += kConsumers) m = fmaxf(m, st.ms[q].x);
-  m = warp_max(m);
-  if (lane == 0) sh.red[warp] = m;
-  consumer_sync();
-  float M = sh.red[0];
+  float2 part[kMaxCpr * kConsumerWarps / 32];
 #pragma unroll
-  for (int w = 1; w < kConsumerWarps; ++w) M = fmaxf(M, sh.red[w]);
+  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t)
+    part[t] = (lane + 32 * t < npart) ? __ldcg(&ms[lane + 32 * t]) : make_float2(-INFINITY, 0.f);
+  int* sl = P.seglen + (size_t)row * cpr;
+  const int sl0 = lane < cpr ? __ldcg(&sl[lane]) : 0;
+  const int sl1 = lane + 32 < cpr ? __ldcg(&sl[lane + 32]) : 0;
+  const unsigned long long* sk = P.segkey + (size_t)row * nkey;
+  for (int e0 = 0; e0 < nkey; e0 += 256) {  // batches of independent loads, then the stores
+    unsigned long long v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 32 + lane;
+      v[u] = e < nkey ? __ldcg(&sk[e]) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 32 + lane;
+      if (e < nkey) st.keys[e] = v[u];
+    }
+  }
+  int2 fe = make_int2(0, 0);
+  float pc = 0.f;
+  if (lane == 0) {
+    fe = P.fr[par][row];
+    pc = P.fr_cum[par][row];
+  }
+  if (lane < cpr) sl[lane] = 0;  // self-cleaning for the next use
+  if (lane + 32 < cpr) sl[lane + 32] = 0;
+  stamp(P, sp, 25);
+  // ---- (1) softmax normaliser ----
+  float m = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t) m = fmaxf(m, part[t].x);
+  const float M = warp_max_fast(m);
   const float ML = M * kLog2e;
   float z = 0.f;
-  for (int q = tid; q < npart; q += kConsumers) {
-    const float2 v = st.ms[q];
+#pragma unroll
+  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t) {
+    const float2 v = part[t];
     if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
   }
-  z = warp_sum(z);
-  consumer_sync();  // everyone has read sh.red (M); segstart complete
-  if (lane == 0) sh.red[warp] = z;
-  consumer_sync();
-  float Z = 0.f;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) Z += sh.red[w];
-  // (2) exact top-k of the union of the existing segment lists, by rank
-  const int nseg = sh.nseg;
-  const int n = nseg * k;
-  const int2 fe = sh.fe;
-  const float pc = sh.pc;
-  for (int e = tid; e < n; e += kConsumers) {
-    const int es = e / k;  // once per entry (not in the inner loop)
-    const unsigned long long key = st.keys[st.segstart[es] * k + (e - es * k)];
-    int rank = 0;
-    for (int s2 = 0; s2 < nseg; ++s2) {
-      const unsigned long long* Lk = st.keys + st.segstart[s2] * k;
-#pragma unroll 8
-      for (int f = 0; f < k; ++f) rank += (Lk[f] > key);
+  const float Z = warp_sum(z);
+  stamp(P, sp, 26);
+  // ---- (2) threshold T = max over segments of their k-th entry ----
+  const unsigned long long v0 = __ballot_sync(kFull, sl0 > 0), v1 = __ballot_sync(kFull, sl1 > 0);
+  __syncwarp();  // st.keys visible
+  unsigned long long tail = 0ull;
+  if (sl0 > 0) tail = st.keys[lane * k + k - 1];
+  if (sl1 > 0 && st.keys[(lane + 32) * k + k - 1] > tail) tail = st.keys[(lane + 32) * k + k - 1];
+  const unsigned th = __reduce_max_sync(kFull, (unsigned)(tail >> 32));
+  const unsigned tl = __reduce_max_sync(kFull, (unsigned)(tail >> 32) == th ? (unsigned)tail : 0u);
+  const unsigned long long T = ((unsigned long long)th << 32) | tl;
+  stamp(P, sp, 27);
+  // ---- (3) survivors (entries >= T of existing segments), compacted by ballot ----
+  const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;  // e / k == umulhi(e, kmag) (k >= 2, e < 2^16)
+  int ns = 0;
+  for (int e0 = 0; e0 < nkey; e0 += 32) {
+    const int e = e0 + lane;
+    bool sv = false;
+    unsigned long long key = 0ull;
+    if (e < nkey) {
+      const int c = (k == 1) ? e : (int)__umulhi((unsigned)e, kmag);
+      const bool valid = c < 32 ? ((v0 >> c) & 1ull) : ((v1 >> (c - 32)) & 1ull);
+      if (valid) {
+        key = st.keys[e];
+        sv = key >= T;
+      }
     }
+    const unsigned bal = __ballot_sync(kFull, sv);
+    if (sv) st.surv[ns + __popc(bal & ((1u << lane) - 1u))] = key;
+    ns += __popc(bal);
+  }
+  __syncwarp();
+  stamp(P, sp, 28);
+  // ---- (4) exact top-k among the survivors by rank; A1 p and A2 cum ----
+  fe.x = __shfl_sync(kFull, fe.x, 0);
+  fe.y = __shfl_sync(kFull, fe.y, 0);
+  pc = __shfl_sync(kFull, pc, 0);
+  for (int s0 = lane; s0 < ns; s0 += 32) {
+    const unsigned long long key = st.surv[s0];
+    int r0 = 0, r1 = 0;
+    int t = 0;
+    for (; t + 1 < ns; t += 2) {
+      r0 += (st.surv[t] > key);
+      r1 += (st.surv[t + 1] > key);
+    }
+    if (t < ns) r0 += (st.surv[t] > key);
+    const int rank = r0 + r1;
     if (rank < k) {
-      // (3) A1 probability and A2 path score of the rank-th candidate
       const float v = tk_val(key);
       const float pj = ex2(fmaf(v, kLog2e, -ML)) / Z;  // p = exp(x - M) / Z   (tau = 1, Q10)
       Cand cd;
@@ -222,12 +256,15 @@ __device__ void merge_row(const Params& P, int layer, int par, int row, ExpandSh
       P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
     }
   }
-  if (tid == 0) {
+  stamp(P, sp, 29);
+  if (lane == 0) {
     P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, row - P.fr_off[par][fe.x]);
     P.rowstat[row] = make_float2(M, Z);
     if (!(Z >= 1.0f) || isinf(Z) || isnan(M)) atomicOr(P.err, kErrDraftNaN);  // Q23
     P.row_done[row] = 0;
   }
+  __syncwarp();
+  stamp(P, sp, 30);
 }
 
 template <bool BF16, bool TMA>
@@ -244,10 +281,24 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (layer - 1) & 1;
   if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&pipe.full[s], 1);
+      mbar_init(&pipe.empty[s], kConsumerWarps);
+    }
+    mbar_fence_init();
+    sh.last_layer = 0;
+  }
+  tl_start(P, 32 + layer);
+  pdl_wait();
+  pdl_trigger();
+  tl_start(P, layer);
+  if (tid == 0) {
     probe_min(P, 0);
     probe_max(P, 1);
   }
   const int R = *P.fr_total[par];
+  const bool t0 = (blockIdx.x == 0 && tid == 0);
+  gstamp(P, t0, 16);
   if (R == 0) {
     // A_{l-1} is empty for every request: the step has terminated at this layer
     if (fuse_select && blockIdx.x == 0 && tid == 0) *P.fr_total[layer & 1] = 0;
@@ -255,51 +306,47 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   }
   const int k = P.k, cpr = P.cpr, CE = P.chunk_elems, V = P.V;
   const long long row_bytes = (long long)V * (BF16 ? 2 : 4);
-  const RowRange rr = cta_range_min((long long)R * cpr, P.min_units);
+  const RowRange rr = cta_range_min(R * cpr, P.min_units);
   if (rr.lo >= rr.hi) return;
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&pipe.full[s], 1);
-      mbar_init(&pipe.empty[s], kConsumerWarps);
-    }
-    mbar_fence_init();
-    sh.tau = 0ull;
-    sh.last_layer = 0;
-  }
-  if (tid < kConsumerWarps) sh.w[tid].cnt = 0;
+  // the CTA's frontier entries, staged once (no dependent global load per chunk)
+  const int row0 = rr.lo / cpr;
+  const int nstage = min((rr.hi - 1) / cpr - row0 + 1, kStageRows);
+  if (tid < nstage) sh.rfe[tid] = P.fr[par][row0 + tid];
   __syncthreads();
+  gstamp(P, t0, 17);
 
   if (warp == kConsumerWarps) {  // ---- producer warp ----
+    gstamp(P, blockIdx.x == 0 && lane == 0, 27);
     if (TMA && lane == 0)
-      produce(pipe, ring, rr, cpr, row_bytes, [&](int row) { return row_ptr(P, par, logits, ld_bytes, row); });
+      produce(pipe, ring, rr, cpr, row_bytes, [&](int row) { return row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0); });
     return;
   }
 
   // ---- consumer warps ----
   WarpTopk& W = sh.w[warp];
-  long long i = 0;
-  long long q = rr.lo;
+  int wcnt = 0;  // entries in W.buf (warp-uniform)
+  int i = 0;
+  int q = rr.lo;
+  int row = row0, c0 = rr.lo - row0 * cpr;
   while (q < rr.hi) {
-    const int row = (int)(q / cpr);
-    const int c0 = (int)(q % cpr);
-    const int nch = (int)min((long long)(cpr - c0), rr.hi - q);
+    const int nch = min(cpr - c0, rr.hi - q);
     unsigned long long bound = 0ull;  // lower bound of the segment's k-th best key
     for (int c = c0; c < c0 + nch; ++c, ++i) {
       uint4 raw[kVecPerThread];
+      const int s = (int)(i % kStages);
       if (TMA) {
-        const int s = (int)(i % kStages);
         mbar_wait(&pipe.full[s], (uint32_t)((i / kStages) & 1));
+        gstamp(P, t0 && i < 2, 18 + 3 * (int)i);
+        stamp(P, t0 && i == 0, 0);
         const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
 #pragma unroll
         for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage as soon as it is in registers
       } else {
-        load_direct<BF16>(row_ptr(P, par, logits, ld_bytes, row), c * CE, V, tid, raw);
+        load_direct<BF16>(row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0), c * CE, V, tid, raw);
       }
       float x[EPT];
       unpack<BF16>(raw, x);
+      stamp(P, t0 && i == 0, 1);
       const int cbase = c * CE;
       if (c == cpr - 1) {  // ragged last chunk: elements past the row end -> -inf
 #pragma unroll
@@ -319,7 +366,9 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         vm[j] = fmaxf(a0, a1);
       }
       const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
-      const float Mw = warp_max(m);
+      stamp(P, t0 && i == 0, 2);
+      const float Mw = warp_max_fast(m);
+      stamp(P, t0 && i == 0, 3);
       float s4[4] = {0.f, 0.f, 0.f, 0.f};
       if (Mw != -INFINITY) {
         const float ML = Mw * kLog2e;
@@ -328,110 +377,172 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       }
       const float sacc = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
       if (lane == 0) P.ms[((size_t)row * cpr + c) * kConsumerWarps + warp] = make_float2(Mw, sacc);
+      stamp(P, t0 && i == 0, 4);
+      gstamp(P, t0 && i < 2, 19 + 3 * (int)i);
 
       // ---- top-k candidates of this warp-chunk ----
-      if (c == c0) {
-        // segment seeding: v_k = k-th largest lane-maximum VALUE; k distinct elements have
-        // value >= v_k, so key(v_k, INT_MAX) is a valid lower bound of the k-th best key
-        const unsigned om = (m == m) ? float_orderable(m) : 0u;
-        unsigned thr = 0xffffffffu, vk = 0u;
-        int got = 0;
-        for (int it = 0; it < k && got < k; ++it) {
-          const unsigned cur = __reduce_max_sync(kFull, om < thr ? om : 0u);
-          got += __popc(__ballot_sync(kFull, om == cur));
-          thr = cur;
-          vk = cur;
+      // CTA-wide bound for this chunk: every warp publishes its top-j lane maxima (j = ceil(k/8),
+      // one lane per round, so ties keep their multiplicity); these 8j values are distinct
+      // elements of the row, so their k-th largest v_k bounds the row's k-th best value from
+      // below and key(v_k, INT_MAX) bounds the segment's k-th best key.
+      {
+        const int jr = (k + kConsumerWarps - 1) / kConsumerWarps;
+        unsigned* pub = sh.pub[i & 1];
+        unsigned rem = (m == m) ? float_orderable(m) : 0u;
+        for (int r = 0; r < jr; ++r) {
+          const unsigned cur = __reduce_max_sync(kFull, rem);
+          const unsigned bal = __ballot_sync(kFull, rem == cur);
+          if (lane == __ffs(bal) - 1) rem = 0u;
+          if (lane == 0) pub[warp * jr + r] = cur;
         }
-        if (got >= k) {
+        consumer_sync();
+        const int np = kConsumerWarps * jr;
+        const unsigned u = lane < np ? pub[lane] : 0u;
+        int gt = 0;
+        for (int o = 0; o < np; o += 4) {
+          const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
+          gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+        }
+        const unsigned vk = __reduce_min_sync(kFull, (lane < np && gt < k) ? u : 0xffffffffu);
+        if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)
           const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
           if (b0 > bound) bound = b0;
         }
       }
-      {
-        const unsigned long long hk = *(volatile unsigned long long*)&sh.tau;
-        if (hk > bound) bound = hk;
-      }
-      if (W.cnt > kSegBuf - 32) {  // keep room for this chunk's appends
-        warp_compact(W, W.cnt, k, lane);
-        if (W.list[k - 1] > bound) bound = W.list[k - 1];
-      }
-      const float bv = tk_val(bound);
-      bool cl = (m >= bv) && (m == m);
-      unsigned pushed = 0u;
-      while (__any_sync(kFull, cl)) {
-        bool more = false;
-        if (cl) {
+      stamp(P, t0 && i == 0, 5);
+      // elements whose value reaches the bound are appended to the warp buffer at positions from
+      // a warp prefix sum (no shared atomics); when the buffer would overflow it is compacted to
+      // its top-k, the bound tightened and the remaining elements re-filtered
+      float bv = bound ? tk_val(bound) : -INFINITY;
+      unsigned pend = 0u;
+      if (m >= bv) {
 #pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j)
-            if (vm[j] >= bv) {
+        for (int n = 0; n < EPT; ++n) pend |= (x[n] >= bv ? 1u : 0u) << n;
+      }
+      for (;;) {
+        const int cnt = __popc(pend);
+        int incl, total;
+        if (!__any_sync(kFull, cnt > 1)) {  // common case: at most one candidate per lane
+          const unsigned bal = __ballot_sync(kFull, cnt > 0);
+          incl = __popc(bal & (0xffffffffu >> (31 - lane)));
+          total = __popc(bal);
+        } else {
+          incl = cnt;
 #pragma unroll
-              for (int e = 0; e < EPV; ++e) {
-                const int n = j * EPV + e;
-                if (x[n] >= bv && !((pushed >> n) & 1u)) {
-                  const unsigned long long key = tk_key(x[n], elem_index<BF16>(cbase, tid, n));
-                  if (key >= bound) {
-                    const int slot = atomicAdd(&W.cnt, 1);
-                    if (slot < kSegBuf) {
-                      W.buf[slot] = key;
-                      pushed |= 1u << n;
-                    } else {
-                      more = true;
-                    }
-                  }
-                }
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+          }
+          total = __shfl_sync(kFull, incl, 31);
+        }
+        if (total == 0) break;
+        if (pend) {
+          int pos = wcnt + incl - cnt;
+          unsigned bits = pend;
+          while (bits) {
+            const int n = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            if (pos < kSegBuf) {
+              const int idx = elem_index<BF16>(cbase, tid, n);
+              float v;
+              if (idx >= V) {
+                v = -INFINITY;
+              } else if (TMA) {  // the stage is still held: reload the element from shared memory
+                const char* sp = ring + (size_t)s * kChunkBytes +
+                                 ((size_t)((n / EPV) * kConsumers + tid) * EPV + (n % EPV)) * (BF16 ? 2 : 4);
+                v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(sp)) << 16)
+                         : *reinterpret_cast<const float*>(sp);
+              } else {
+                const char* rp = row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0) + (size_t)idx * (BF16 ? 2 : 4);
+                v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(rp)) << 16)
+                         : *reinterpret_cast<const float*>(rp);
               }
+              W.buf[pos] = tk_key(v, idx);
+              pend &= ~(1u << n);
             }
+            ++pos;
+          }
+        }
+        if (wcnt + total <= kSegBuf) {
+          wcnt += total;
+          break;
         }
         __syncwarp();
-        cl = more;
-        if (__any_sync(kFull, more)) {  // buffer full: compact, tighten, retry the rest
-          if (lane == 0) W.cnt = kSegBuf;
-          __syncwarp();
-          warp_compact(W, kSegBuf, k, lane);
-          if (W.list[k - 1] > bound) bound = W.list[k - 1];
-        }
+        warp_compact(W, kSegBuf, k, lane);
+        wcnt = k;
+        if (W.list[k - 1] > bound) bound = W.list[k - 1];
+        bv = tk_val(bound);
+#pragma unroll
+        for (int n = 0; n < EPT; ++n)
+          if (!(x[n] >= bv)) pend &= ~(1u << n);
       }
-      if (lane == 0 && bound) atomicMax(&sh.tau, bound);
+      __syncwarp();
+      if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
+      gstamp(P, t0 && i < 2, 20 + 3 * (int)i);
+      stamp(P, t0 && i == 0, 6);
     }
-    // ---- segment end: warp buffers -> warp top-k -> CTA segment list (rank merge), arrival ----
-    warp_compact(W, W.cnt, k, lane);
-    if (lane == 0) W.cnt = 0;
+    // ---- segment end: warp buffers (top-k only if longer) -> CTA segment list (rank merge) ----
+    if (wcnt > k) {
+      warp_compact(W, wcnt, k, lane);
+      wcnt = k;
+    }
+    // padding keys are distinct and below every real key (value -inf, index > INT_MAX)
+    if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
+    wcnt = 0;
+    gstamp(P, t0 && q == rr.lo, 24);
     consumer_sync();
-    for (int t = tid; t < kConsumerWarps * k; t += kConsumers) {  // only the 8k live entries
-      const int tw = t / k, te = t - tw * k;
-      const unsigned long long key = sh.w[tw].list[te];
-      int rank = 0;
-      for (int w = 0; w < kConsumerWarps; ++w) {
-#pragma unroll 8
-        for (int f = 0; f < k; ++f) rank += (sh.w[w].list[f] > key);
+    gstamp(P, t0 && q == rr.lo, 28);
+    {
+      const int n = kConsumerWarps * k;  // even
+      if (tid < n) {
+        const unsigned long long key = sh.cl[tid];
+        const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
+        int r0 = 0, r1 = 0;
+#pragma unroll 4
+        for (int f = 0; f < n / 2; ++f) {
+          const ulonglong2 v = c2[f];
+          r0 += (v.x > key);
+          r1 += (v.y > key);
+        }
+        const int rank = r0 + r1;
+        if (rank < k) P.segkey[((size_t)row * cpr + c0) * k + rank] = key;
       }
-      if (rank < k) P.segkey[((size_t)row * cpr + c0) * k + rank] = key;
     }
     if (tid == 0) P.seglen[(size_t)row * cpr + c0] = nch;
+    gstamp(P, t0 && q == rr.lo, 25);
     consumer_sync();
-    if (tid == 0) {
-      const int old = atom_add_acq_rel_gpu(&P.row_done[row], nch);  // publish + acquire
-      sh.last = (old + nch == cpr);
-      sh.tau = 0ull;
-    }
-    consumer_sync();
-    if (sh.last) {
-      if (tid == 0) {
-        probe_max(P, 3);
-        probe_min(P, 8);
+    // warp 0 alone: arrival (release of the CTA's lists, acquire of the others'), and the row
+    // merge when this CTA completed the row; the other warps go on with the next segment
+    if (warp == 0) {
+      int last = 0;
+      if (lane == 0) {
+        const int old = atom_add_acq_rel_gpu(&P.row_done[row], nch);  // publish + acquire
+        last = (old + nch == cpr);
       }
-      merge_row(P, layer, par, row, sh, mst);
-      if (tid == 0) probe_max(P, 4);
-      consumer_sync();
-      if (tid == 0) {
-        const int old = atom_add_acq_rel_gpu(&P.layer_done[layer - 1], 1);
-        sh.last_layer = (old + 1 == R);
+      last = __shfl_sync(kFull, last, 0);
+      gstamp(P, t0 && q == rr.lo, 26);
+      if (last) {  // this CTA completed the row
+        if (lane == 0) {
+          probe_max(P, 3);
+          probe_min(P, 8);
+        }
+        gstamp(P, lane == 0 && row == 0, 29);
+        merge_row_warp(P, layer, par, row, mst);
+        gstamp(P, lane == 0 && row == 0, 30);
+        if (lane == 0) {
+          probe_max(P, 4);
+          const int old = atom_add_acq_rel_gpu(&P.layer_done[layer - 1], 1);
+          if (old + 1 == R) sh.last_layer = 1;
+        }
+        __syncwarp();
       }
-      consumer_sync();
     }
     q += nch;
+    ++row;
+    c0 = 0;
   }
   if (tid == 0) probe_max(P, 2);
+  consumer_sync();
   if (sh.last_layer) {
     if (tid == 0) {
       P.layer_done[layer - 1] = 0;
@@ -441,6 +552,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     if (tid == 0) probe_max(P, 6);
   }
   if (tid == 0) probe_max(P, 7);
+  tl_end(P, layer);
 }
 
 }  // namespace
@@ -466,11 +578,11 @@ void launch_expand(const Params& P, int layer, const void* logits, long long ld_
   const size_t smem = layer_smem_bytes(P.cpr, P.k);
   const int f = fuse_select ? 1 : 0;
   if (P.dtype == SMART_BF16) {
-    if (tma) layer_kernel<true, true><<<grid, kLayerThreads, smem, s>>>(P, layer, base, ld_bytes, f);
-    else layer_kernel<true, false><<<grid, kLayerThreads, smem, s>>>(P, layer, base, ld_bytes, f);
+    if (tma) launch_k(layer_kernel<true, true>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
+    else launch_k(layer_kernel<true, false>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
   } else {
-    if (tma) layer_kernel<false, true><<<grid, kLayerThreads, smem, s>>>(P, layer, base, ld_bytes, f);
-    else layer_kernel<false, false><<<grid, kLayerThreads, smem, s>>>(P, layer, base, ld_bytes, f);
+    if (tma) launch_k(layer_kernel<false, true>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
+    else launch_k(layer_kernel<false, false>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
   }
 }
 

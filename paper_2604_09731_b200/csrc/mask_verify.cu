@@ -12,6 +12,11 @@ namespace smart {
 
 namespace {
 
+__device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {  // packed bf16x2 max, NaN-propagating
+  uint32_t d;
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -21,6 +26,9 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
 }  // namespace
 
 __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32_t* root_pos) {
+  pdl_wait();
+  pdl_trigger();
+  tl_start(P, 0);
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < P.b_loc) {
     size_t o = (size_t)r * P.T;
@@ -37,6 +45,7 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
     P.finished[r] = 0;
     P.root_pos[r] = root_pos ? root_pos[r] : 0;
     P.fr[0][r] = make_int2(r, 0);  // A_0 = {root}
+    P.fr_cum[0][r] = 1.f;
     P.fr_cnt[0][r] = 1;
     P.fr_off[0][r] = r;
   }
@@ -51,6 +60,7 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
     *P.N_glob = 0;
     *P.E_glob = 0.0;
   }
+  tl_end(P, 0);
 }
 
 namespace {
@@ -63,6 +73,10 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
   __shared__ int s_run[33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, MW = P.MW;
+  tl_start(P, 52);
+  pdl_wait();
+  pdl_trigger();
+  tl_start(P, 20);
   // verify-row offsets: exclusive scan of n_nodes (rows of K4)
   {
     const int per = (P.b_loc + 1023) / 1024;
@@ -93,6 +107,7 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
       run += P.n_nodes[r];
     }
     if (tid == 0) P.vrow_off[P.b_loc] = s_run[32];
+    __syncthreads();
   }
   int* sp = s_tree + (size_t)warp * 3 * T;
   int* sd = sp + T;
@@ -100,10 +115,12 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
   for (int r = warp; r < P.b_loc; r += 32) {
     const int n = P.n_nodes[r];
     const int rp = P.root_pos[r];
+    const int vo = P.vrow_off[r];
     for (int i = lane; i < n; i += 32) {
       sp[i] = P.parent[(size_t)r * T + i];
       sd[i] = P.depth[(size_t)r * T + i];
       st[i] = P.tok[(size_t)r * T + i];
+      P.vrow_rn[vo + i] = make_int2(r, i);  // verify row -> (request, node)
     }
     __syncwarp();
     for (int i = lane; i < T; i += 32) {
@@ -131,24 +148,16 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
     if (lane == 0 && tree_len) tree_len[r] = n;
     __syncwarp();
   }
+  tl_end(P, 20);
 }
 
 struct VerifyShared {
-  float wv[kConsumerWarps];
-  int wi[kConsumerWarps];
-  int last, rlast;
+  int2 rn[kStageRows];  // (request, node) of the CTA's first rows
+  float wv[2][kConsumerWarps];
+  int wi[2][kConsumerWarps];
   int walk[1];  // [3 * T] staged (parent, token, argmax) of the walked request (dynamic tail)
 };
 
-__device__ __forceinline__ int find_request(const Params& P, int row) {
-  int a = 0, b = P.b_loc - 1;
-  while (a < b) {
-    const int m = (a + b + 1) >> 1;
-    if (P.vrow_off[m] <= row) a = m;
-    else b = m - 1;
-  }
-  return a;
-}
 
 // K4: persistent TMA-staged stream over all tree rows (request r, node i < tree_len[r]) of the
 // target logits; exact argmax per row (value desc, index asc); the request whose last row
@@ -159,21 +168,11 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
               int32_t* accept_path, int32_t* bonus) {
   constexpr int EPV = BF16 ? 8 : 4;
   constexpr int ESZ = BF16 ? 2 : 4;
-  constexpr int EPT = kVecPerThread * EPV;
   extern __shared__ __align__(128) char dsm[];
   char* ring = dsm;
   StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
   VerifyShared& sh = *reinterpret_cast<VerifyShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NR = P.vrow_off[P.b_loc];
-  const int cpr = P.cpr, CE = P.chunk_elems, V = P.V, T = P.T;
-  const long long row_bytes = (long long)V * ESZ;
-  const RowRange rr = cta_range_min((long long)NR * cpr, P.min_units);
-  if (rr.lo >= rr.hi) return;
-  auto row_base = [&](int row) {
-    const int r = find_request(P, row);
-    return target + ((long long)r * T + (row - P.vrow_off[r])) * ld_bytes;
-  };
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&pipe.full[s], 1);
@@ -181,123 +180,164 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
     }
     mbar_fence_init();
   }
+  tl_start(P, 53);
+  pdl_wait();
+  pdl_trigger();
+  tl_start(P, 21);
+  const int NR = P.vrow_off[P.b_loc];
+  const int cpr = P.cpr, CE = P.chunk_elems, V = P.V, T = P.T;
+  const long long row_bytes = (long long)V * ESZ;
+  const RowRange rr = cta_range_min(NR * cpr, P.min_units);
+  if (rr.lo >= rr.hi) return;
+  // the CTA's row descriptors, staged once (no dependent global loads per chunk)
+  const int row0 = rr.lo / cpr;
+  const int nstage = min((rr.hi - 1) / cpr - row0 + 1, kStageRows);
+  if (tid < nstage) sh.rn[tid] = P.vrow_rn[row0 + tid];
+  auto rown = [&](int row) { return row - row0 < kStageRows ? sh.rn[row - row0] : P.vrow_rn[row]; };
+  auto row_base = [&](int row) {
+    const int2 e = rown(row);
+    return target + ((long long)e.x * T + e.y) * ld_bytes;
+  };
   __syncthreads();
   if (warp == kConsumerWarps) {
     if (TMA && lane == 0) produce(pipe, ring, rr, cpr, row_bytes, row_base);
     return;
   }
   int nanf = 0;
-  long long i = 0;
-  long long q = rr.lo;
+  int i = 0;
+  int q = rr.lo;
+  int row = row0, c0 = rr.lo - row0 * cpr;
+  int seg = -1;
   while (q < rr.hi) {
-    const int row = (int)(q / cpr);
-    const int c0 = (int)(q % cpr);
-    const int nch = (int)min((long long)(cpr - c0), rr.hi - q);
-    const int r = find_request(P, row);
-    const int node = row - P.vrow_off[r];
+    ++seg;
+    const int nch = min(cpr - c0, rr.hi - q);
+    const int2 rnode = rown(row);
+    const int r = rnode.x, node = rnode.y;
     float bv = -INFINITY;
     int bi = kIdxSentinel;
     for (int c = c0; c < c0 + nch; ++c, ++i) {
+      gstamp(P, blockIdx.x == 0 && tid == 0 && i < 8, 100 + (int)i);
       const int cbase = c * CE;
-      float x[EPT];
+      uint4 raw[kVecPerThread];
       if (TMA) {
         const int s = (int)(i % kStages);
         mbar_wait(&pipe.full[s], (uint32_t)((i / kStages) & 1));
         const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
-        uint4 raw[kVecPerThread];
 #pragma unroll
         for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
         __syncwarp();
         if (lane == 0) mbar_arrive(&pipe.empty[s]);
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-          for (int q2 = 0; q2 < 4; ++q2) {
-            if (BF16) {
-              x[j * 8 + 2 * q2] = __uint_as_float(w[q2] << 16);
-              x[j * 8 + 2 * q2 + 1] = __uint_as_float(w[q2] & 0xffff0000u);
-            } else {
-              x[j * 4 + q2] = __uint_as_float(w[q2]);
-            }
-          }
-        }
-        if (c == cpr - 1) {
-#pragma unroll
-          for (int n = 0; n < EPT; ++n)
-            if (cbase + ((n / EPV) * kConsumers + tid) * EPV + (n % EPV) >= V) x[n] = -INFINITY;
-        }
       } else {
         const char* rp = row_base(row);
 #pragma unroll
         for (int j = 0; j < kVecPerThread; ++j) {
           const int e0 = cbase + (j * kConsumers + tid) * EPV;
+          uint32_t w[4];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) w[q2] = BF16 ? 0xff80ff80u : 0xff800000u;
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e0 + e < V) {
+              if (BF16) {
+                const uint32_t h = *reinterpret_cast<const unsigned short*>(rp + (size_t)(e0 + e) * 2);
+                w[e >> 1] = (e & 1) ? ((w[e >> 1] & 0x0000ffffu) | (h << 16)) : ((w[e >> 1] & 0xffff0000u) | h);
+              } else {
+                w[e] = *reinterpret_cast<const uint32_t*>(rp + (size_t)(e0 + e) * 4);
+              }
+            }
+          raw[j] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      if (c == cpr - 1) {  // ragged last chunk: elements past the row end -> -inf
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+          const int e0 = cbase + (j * kConsumers + tid) * EPV;
+          uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e0 + e >= V) {
+              if (BF16) w[e >> 1] = (e & 1) ? ((w[e >> 1] & 0x0000ffffu) | 0xff800000u) : ((w[e >> 1] & 0xffff0000u) | 0xff80u);
+              else w[e] = 0xff800000u;
+            }
+          raw[j] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      // ---- exact argmax of this (chunk, warp): vector maxima on packed values (bf16x2 max),
+      // one-instruction warp max, then the index is searched only in the vectors holding it ----
+      float vm[kVecPerThread];
+#pragma unroll
+      for (int j = 0; j < kVecPerThread; ++j) {
+        if (BF16) {
+          const uint32_t mw = bmax2_nan(bmax2_nan(raw[j].x, raw[j].y), bmax2_nan(raw[j].z, raw[j].w));
+          vm[j] = fmax_nan(__uint_as_float(mw << 16), __uint_as_float(mw & 0xffff0000u));
+        } else {
+          vm[j] = fmax_nan(fmax_nan(__uint_as_float(raw[j].x), __uint_as_float(raw[j].y)),
+                           fmax_nan(__uint_as_float(raw[j].z), __uint_as_float(raw[j].w)));
+        }
+      }
+      float m = fmax_nan(fmax_nan(vm[0], vm[1]), fmax_nan(vm[2], vm[3]));
+      if (m != m) {  // a NaN logit: flagged (Q23); the row's argmax is then unspecified
+        nanf = 1;
+        m = -INFINITY;
+      }
+      const float Mw = warp_max_fast(m);
+      int li = kIdxSentinel;
+#pragma unroll
+      for (int j = 0; j < kVecPerThread; ++j)
+        if (vm[j] == Mw) {
+          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+          const int e0 = cbase + (j * kConsumers + tid) * EPV;
 #pragma unroll
           for (int e = 0; e < EPV; ++e) {
-            float xv = -INFINITY;
-            if (e0 + e < V) {
-              if (BF16) xv = __uint_as_float(((uint32_t)*reinterpret_cast<const unsigned short*>(rp + (size_t)(e0 + e) * 2)) << 16);
-              else xv = *reinterpret_cast<const float*>(rp + (size_t)(e0 + e) * 4);
-            }
-            x[j * EPV + e] = xv;
+            const float xv = BF16 ? __uint_as_float((e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16))
+                                  : __uint_as_float(w[e]);
+            if (xv == Mw && e0 + e < V) li = min(li, e0 + e);
           }
         }
-      }
-      float m = -INFINITY;
-#pragma unroll
-      for (int n = 0; n < EPT; ++n) m = fmax_nan(m, x[n]);
-      if (m != m) nanf = 1;
-      int mi = kIdxSentinel;
-#pragma unroll
-      for (int n = 0; n < EPT; ++n) {
-        const int gi = cbase + ((n / EPV) * kConsumers + tid) * EPV + (n % EPV);
-        if (x[n] == m && mi == kIdxSentinel && gi < V) mi = gi;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(kFull, m, o);
-        const int oi = __shfl_xor_sync(kFull, mi, o);
-        if (better(ov, oi, m, mi)) {
-          m = ov;
-          mi = oi;
-        }
-      }
-      if (better(m, mi, bv, bi)) {
-        bv = m;
+      const int mi = (int)__reduce_min_sync(kFull, (unsigned)li);
+      if (better(Mw, mi, bv, bi)) {
+        bv = Mw;
         bi = mi;
       }
     }
+    // ---- segment end: CTA best (warp 0, two reductions), one acq_rel arrival per CTA; warp 0
+    // alone then merges a completed row and walks a completed request while the other warps
+    // stream on (the per-warp bests are double-buffered by segment parity) ----
+    const int sb = seg & 1;
     if (lane == 0) {
-      sh.wv[warp] = bv;
-      sh.wi[warp] = bi;
+      sh.wv[sb][warp] = bv;
+      sh.wi[sb][warp] = bi;
     }
     consumer_sync();
-    if (tid == 0) {
-      float v = sh.wv[0];
-      int ix = sh.wi[0];
-      for (int w = 1; w < kConsumerWarps; ++w)
-        if (better(sh.wv[w], sh.wi[w], v, ix)) {
-          v = sh.wv[w];
-          ix = sh.wi[w];
+    gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 0);
+    if (warp == 0) {
+      int last = 0;
+      {
+        const float v = lane < kConsumerWarps ? sh.wv[sb][lane] : -INFINITY;
+        const int ix = lane < kConsumerWarps ? sh.wi[sb][lane] : kIdxSentinel;
+        const float vb = warp_max_fast(v);
+        const int ib = (int)__reduce_min_sync(kFull, (unsigned)(v == vb ? ix : kIdxSentinel));
+        if (lane == 0) {
+          const size_t so = (size_t)row * cpr + c0;
+          P.vsegv[so] = vb;
+          P.vsegi[so] = ib;
+          P.vseglen[so] = nch;
+          const int old = atom_add_acq_rel_gpu(&P.row_done[row], nch);  // publish + acquire
+          last = (old + nch == cpr);
         }
-      const size_t so = (size_t)row * cpr + c0;
-      P.vsegv[so] = v;
-      P.vsegi[so] = ix;
-      P.vseglen[so] = nch;
-      __threadfence();
-      const int old = atomicAdd(&P.row_done[row], nch);
-      sh.last = (old + nch == cpr);
-    }
-    consumer_sync();
-    if (sh.last && warp == 0) {
-      __threadfence();
+        last = __shfl_sync(kFull, last, 0);
+      }
+      gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 1);
+      if (last) {
+      // row merge: one load wave over the row's segments, two warp reductions
       float v = -INFINITY;
       int ix = kIdxSentinel;
       for (int c = lane; c < cpr; c += 32) {
         const size_t so = (size_t)row * cpr + c;
-        if (__ldcg(&P.vseglen[so]) > 0) {
-          const float sv = __ldcg(&P.vsegv[so]);
-          const int si = __ldcg(&P.vsegi[so]);
+        const int sl = __ldcg(&P.vseglen[so]);
+        const float sv = __ldcg(&P.vsegv[so]);
+        const int si = __ldcg(&P.vsegi[so]);
+        if (sl > 0) {
           if (better(sv, si, v, ix)) {
             v = sv;
             ix = si;
@@ -305,28 +345,20 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
           P.vseglen[so] = 0;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(kFull, v, o);
-        const int oi = __shfl_xor_sync(kFull, ix, o);
-        if (better(ov, oi, v, ix)) {
-          v = ov;
-          ix = oi;
-        }
-      }
+      const float vb = warp_max_fast(v);
+      ix = (int)__reduce_min_sync(kFull, (unsigned)(v == vb ? ix : kIdxSentinel));
       int rl = 0;
       if (lane == 0) {
         P.vrow_arg[(size_t)r * T + node] = ix;
         P.row_done[row] = 0;
-        __threadfence();
-        const int old = atomicAdd(&P.req_done[r], 1);
+        const int old = atom_add_acq_rel_gpu(&P.req_done[r], 1);
         rl = (old + 1 == P.n_nodes[r]);
       }
       rl = __shfl_sync(kFull, rl, 0);
+      gstamp(P, blockIdx.x == 0 && lane == 0 && seg < 4, 110 + 4 * seg + 2);
       if (rl) {
         // greedy walk of request r: follow the child whose token is the target argmax.
         // The request's tree (parent, token, row argmax) is staged in shared memory first.
-        __threadfence();
         const int n = P.n_nodes[r];
         const int D = P.d > 0 ? P.d : 1;
         int* s_par = sh.walk;
@@ -368,11 +400,16 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
         if (accept_path)
           for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;
       }
+      }
     }
-    consumer_sync();
+    gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 3);
     q += nch;
+    ++row;
+    c0 = 0;
   }
   if (nanf) atomicOr(P.err, kErrTargetNaN);
+  tl_end(P, 21);
+  if (P.dbg && tid == 0) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA end (debug timeline)
 }
 
 }  // namespace
@@ -380,7 +417,7 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok, int32_t* tree_len,
                  cudaStream_t s) {
   const size_t smem = (size_t)32 * 3 * P.T * sizeof(int);
-  mask_kernel<<<1, 1024, smem, s>>>(P, mask, pos, parent, tok, tree_len);
+  launch_k(mask_kernel, dim3(1), dim3(1024), smem, s, P, mask, pos, parent, tok, tree_len);
 }
 
 cudaError_t mask_set_smem() {
@@ -407,11 +444,11 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
   const char* t = static_cast<const char*>(target);
   const size_t sm = verify_smem_bytes(P.T);
   if (P.dtype == SMART_BF16) {
-    if (tma) verify_kernel<true, true><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
-    else verify_kernel<true, false><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) launch_k(verify_kernel<true, true>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
+    else launch_k(verify_kernel<true, false>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
   } else {
-    if (tma) verify_kernel<false, true><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
-    else verify_kernel<false, false><<<grid, kLayerThreads, sm, s>>>(P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) launch_k(verify_kernel<false, true>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
+    else launch_k(verify_kernel<false, false>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
   }
 }
 

@@ -11,6 +11,8 @@ namespace {
 __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int layer, int mode) {
   extern __shared__ __align__(16) char smem[];
   const int par = (layer - 1) & 1;
+  pdl_wait();
+  pdl_trigger();
   if (mode == kSelFull && *P.fr_total[par] == 0) {
     // no frontier: the step has terminated; publish an empty next frontier
     if (threadIdx.x == 0) *P.fr_total[layer & 1] = 0;
@@ -20,6 +22,8 @@ __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int
 }
 
 __global__ void export_frontier_kernel(Params P, int parity, int32_t* out, int32_t* count) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *P.fr_total[parity];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; out && i < n; i += gridDim.x * blockDim.x) {
     const int2 e = P.fr[parity][i];
@@ -40,12 +44,12 @@ cudaError_t select_set_smem(size_t bytes) {
 }
 
 void launch_select(const Params& P, int layer, int mode, size_t smem, cudaStream_t s) {
-  select_kernel<<<1, kSelectThreads, smem, s>>>(P, layer, mode);
+  launch_k(select_kernel, dim3(1), dim3(kSelectThreads), smem, s, P, layer, mode);
 }
 
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count, cudaStream_t s) {
-  if (d_frontier) export_frontier_kernel<<<8, 256, 0, s>>>(P, parity, d_frontier, d_count);
-  else if (d_count) export_frontier_kernel<<<1, 32, 0, s>>>(P, parity, nullptr, d_count);
+  if (d_frontier) launch_k(export_frontier_kernel, dim3(8), dim3(256), 0, s, P, parity, d_frontier, d_count);
+  else if (d_count) launch_k(export_frontier_kernel, dim3(1), dim3(32), 0, s, P, parity, (int32_t*)nullptr, d_count);
 }
 
 }  // namespace smart

@@ -178,6 +178,8 @@ struct SelLayout {
   int* pre;       // [nc_cap + 1] exclusive scan of admitted flags (flags first)
   float* cum;     // [nc_cap] path score of each candidate
   Cand* cd;       // [nc_cap] staged candidate records
+  int* nix;       // [nc_cap] node index of each admitted candidate (index among the request's admits)
+  double* pps;    // [nc_cap] path_sum of the parent (PATH_MEAN)
   int* fin;       // [b_loc] finished flag
   double* ctab;   // [nc_cap + 2] cost(N0 + j)
   double* dtab;   // [nc_cap + 2] marginal cost at N0 + j
@@ -191,6 +193,9 @@ __host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_
   size_t bytes = (size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4;
   bytes = (bytes + 15) & ~size_t(15);
   bytes += (size_t)nc_cap * sizeof(Cand);
+  bytes += (size_t)nc_cap * 4;
+  bytes = (bytes + 15) & ~size_t(15);
+  bytes += (size_t)nc_cap * 8;
   bytes += ((size_t)nc_cap * nranks + 2) * 16;
   bytes += (size_t)b_all * 8;
   bytes = (bytes + 15) & ~size_t(15);
@@ -216,6 +221,11 @@ __device__ inline SelLayout sel_layout(char* smem, int b_loc, int b_all, int nc_
   size_t bytes = ((size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4 + 15) & ~size_t(15);
   L.cd = reinterpret_cast<Cand*>(smem + bytes);
   bytes += (size_t)nc_cap * sizeof(Cand);
+  L.nix = reinterpret_cast<int*>(smem + bytes);
+  bytes += (size_t)nc_cap * 4;
+  bytes = (bytes + 15) & ~size_t(15);
+  L.pps = reinterpret_cast<double*>(smem + bytes);
+  bytes += (size_t)nc_cap * 8;
   L.ctab = reinterpret_cast<double*>(smem + bytes);
   L.dtab = L.ctab + (size_t)nc_cap * nranks + 2;
   bytes += ((size_t)nc_cap * nranks + 2) * 16;
@@ -267,8 +277,9 @@ __device__ __forceinline__ double warp_det_sum(const double* a, int n, int lane)
 // select_layer: A3-A6 for `layer`.  mode kSelFull: single rank (or LOCAL cost scope);
 // kSelLocal: A3 + local sort, pack the exchange record; kSelGlobal: merge gathered records,
 // A5 on the global list, commit own requests.
-// Warp-centric: warp 0 runs every per-request step with shuffles (no block barriers); all NT
-// threads join only the two O(n^2) rank loops (within-request ranks, global rank sort).
+// Latency-oriented: per-candidate work is spread over all NT threads; warp 0 runs the per-request
+// bookkeeping and the A5 scan (lane-contiguous chunks, so the fp64 prefix is a function of the
+// list length only); 7 block barriers in total.
 // ---------------------------------------------------------------------------------------------
 template <int NT>
 __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
@@ -278,26 +289,27 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
   const int k = P.k, bl = P.b_loc;
   const int b_all = (mode == kSelGlobal) ? P.b_glob : bl;
   const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+  const bool pmean = (P.accept_model == SMART_PATH_MEAN);
   DevTrace& tr = P.trace[layer - 1];
   const int R = *P.fr_total[par];
   const int nct = R * k;  // candidates of this layer (local)
   SelLayout L = sel_layout(smem, bl, b_all, P.cap_rows * k, P.nranks, P.sort_cap);
   stamp(P, tid == 0, 9);
 
-  // ---- stage per-request state and the candidates (one wave of independent loads) ----
+  // ---- stage per-request state, the cost window and the candidates (one wave) ----
   for (int r = tid; r < bl; r += NT) {
     L.cnt[r] = P.fr_cnt[par][r];
     L.off[r] = P.fr_off[par][r];
     L.nd[r] = P.n_nodes[r] - 1;
-    L.D[r] = (P.accept_model == SMART_PATH_MEAN) ? (float)P.leaf_cnt[r] : 1.f;  // Eq.(13), Q6
+    L.D[r] = pmean ? (float)P.leaf_cnt[r] : 1.f;  // Eq.(13), Q6
     L.fin[r] = P.finished[r];
     if (mode != kSelGlobal) L.E[r] = P.E_r[r];
   }
   {
-    // cost-table window from N0 = drafted nodes before the layer (kept by the previous layer)
+    // cost window from N0 = drafted nodes before the layer; entries [0, max eligible + 1]
     const long long n0g = *P.N_glob;
-    const int ncap = P.cap_rows * k * P.nranks + 2;
-    for (int j = tid; j < ncap; j += NT) {
+    const int ncw = (mode == kSelGlobal ? P.nranks * P.m_cap : nct) + 2;
+    for (int j = tid; j < ncw; j += NT) {
       const long long N = min(n0g + j, (long long)P.n_cost - 1);
       L.ctab[j] = P.cost_tab[N];
       L.dtab[j] = P.dc_tab[N];
@@ -305,11 +317,11 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
   }
   if (mode == kSelGlobal) {
     for (int i = tid; i < P.nranks * P.m_cap; i += NT) {
-      const int g = i / P.m_cap, e = i % P.m_cap;
+      const int g = i / P.m_cap, e = i - g * P.m_cap;
       L.keys[i] = reinterpret_cast<const unsigned long long*>(P.xr + (size_t)g * P.xstride)[e];
     }
     for (int i = tid; i < P.b_glob; i += NT) {
-      const int g = i / bl, r = i % bl;
+      const int g = i / bl, r = i - g * bl;
       L.E[i] = reinterpret_cast<const double*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8)[r];
     }
   }
@@ -321,12 +333,10 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
     L.cum[q] = c.cum;
     L.pre[q] = 0;
   }
-  blk_sync<NT>();
+  blk_sync<NT>();  // B1
   stamp(P, tid == 0, 10);
 
-  // ---- A3 (warp 0): per-request eligibility e_r = min(B - n_r, W, |U_r|), eligible bases ----
-  int ne = 0;
-  long long N0 = 0;
+  // ---- A3 (warp 0): e_r = min(B - n_r, W, |U_r|), eligible bases ∥ benefits (all) ----
   if (warp == 0) {
     long long nl = 0;
     for (int r = lane; r < bl; r += 32) {
@@ -345,15 +355,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       ss.bcast_l[1] = nl;
     }
   }
-  // all threads: benefit b = cum / D_r
   for (int q = tid; q < nct; q += NT) {
     const float D = L.D[L.crow[q]];
     L.cb[q] = (D == 1.f) ? L.cum[q] : __fdiv_rn(L.cum[q], D);
   }
-  blk_sync<NT>();
+  blk_sync<NT>();  // B2
+  int ne = ss.bcast_i[2];
+  long long N0 = ss.bcast_l[1];
   if (mode != kSelGlobal) {
-    ne = ss.bcast_i[2];
-    N0 = ss.bcast_l[1];
     // within-request rank by (b desc, c asc); eligible if rank < e_r
     for (int q = tid; q < nct; q += NT) {
       const int r = L.crow[q];
@@ -368,22 +377,28 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
       if (rank < e_r) L.keys[L.base[r] + rank] = sel_key(b, P.b_off + r, q - s0);
     }
-    blk_sync<NT>();
+    blk_sync<NT>();  // B3
   }
   stamp(P, tid == 0, 11);
 
   // ---- A4: sort (local list, or the gathered lists of all ranks) ----
   const int nsort = (mode == kSelGlobal) ? P.nranks * P.m_cap : ne;
   if (nsort <= 1024) {
-    // rank sort (keys unique; padding ~0 keys sort to the end)
+    // rank sort (keys unique; padding ~0 keys sort to the end); two keys per shared load
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(L.keys);
     for (int i = tid; i < nsort; i += NT) {
       const unsigned long long key = L.keys[i];
       int rank = 0;
-#pragma unroll 8
-      for (int f = 0; f < nsort; ++f) rank += (L.keys[f] < key);
+      int f = 0;
+#pragma unroll 4
+      for (; f + 1 < nsort; f += 2) {
+        const ulonglong2 v = k2[f >> 1];
+        rank += (v.x < key) + (v.y < key);
+      }
+      if (f < nsort) rank += (L.keys[f] < key);
       L.keys2[rank] = key;
     }
-    blk_sync<NT>();
+    blk_sync<NT>();  // B4
     unsigned long long* t = L.keys;
     L.keys = L.keys2;
     L.keys2 = t;
@@ -412,71 +427,79 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
     return;
   }
 
-  int R_all = R;
-  if (mode == kSelGlobal) {
-    long long nloc = 0, eloc = 0, rloc = 0;
-    for (int i = tid; i < P.b_glob; i += NT) {
-      const int g = i / bl, r = i % bl;
-      nloc += reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8)[r];
-    }
-    for (int g = tid; g < P.nranks; g += NT) {
-      const int* h = reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8);
-      eloc += h[bl];
-      rloc += h[bl + 1];
-    }
-    N0 = block_sum_ll<NT>(nloc, ss);
-    ne = (int)block_sum_ll<NT>(eloc, ss);
-    R_all = (int)block_sum_ll<NT>(rloc, ss);
-  }
   const int bc = (P.cost_scope == SMART_COST_LOCAL) ? bl : P.b_glob;
   auto sp = [&](double E, int j) {  // b*S at N0 + j from the prefetched window
     const double C = L.ctab[j];
     return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
   };
 
-  // ---- A5 + A6 on warp 0 (no block barriers) ----
+  // ---- A5 (warp 0): Eq.(16) scan over the sorted list, cut, argmax_j S_j ----
   if (warp == 0) {
+    int R_all = R;
+    if (mode == kSelGlobal) {
+      long long nloc = 0, eloc = 0, rloc = 0;
+      for (int i = lane; i < P.b_glob; i += 32) {
+        const int g = i / bl, r = i - g * bl;
+        nloc += reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8)[r];
+      }
+      for (int g = lane; g < P.nranks; g += 32) {
+        const int* h = reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8);
+        eloc += h[bl];
+        rloc += h[bl + 1];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        nloc += __shfl_xor_sync(kFull, nloc, o);
+        eloc += __shfl_xor_sync(kFull, eloc, o);
+        rloc += __shfl_xor_sync(kFull, rloc, o);
+      }
+      N0 = nloc;
+      ne = (int)eloc;
+      R_all = (int)rloc;
+    }
     const double E0 = warp_det_sum(L.E, b_all, lane);  // global request order (Q13)
     const double Sb0 = sp(E0, 0);
     const double dc0 = L.dtab[0];
     const double ac = P.alpha * P.c_T;
-    // exclusive prefix of b over the sorted list: 32-tiles (fixed trees), tiles in order
+    const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
+    // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
+    const int per = (ne + 31) >> 5;
+    const int j0 = min(ne, lane * per), j1 = min(ne, j0 + per);
+    double lt = 0.0;
+    for (int j = j0; j < j1; ++j) lt += (double)sel_key_b(L.keys[j]);
+    double lex = lt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(kFull, lex, o);
+      if (lane >= o) lex += u;
+    }
+    lex -= lt;
     int first_fail = ne;
     double bestS = Sb0;
     int bestj = 0;
-    double run = 0.0;
-    for (int t = 0; t < ne; t += 32) {
-      const int j = t + lane;
-      const double bj = j < ne ? (double)sel_key_b(L.keys[j]) : 0.0;
-      double incl = bj;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += u;
+    double before = lex;
+    for (int j = j0; j < j1; ++j) {
+      const double bj = (double)sel_key_b(L.keys[j]);
+      // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
+      // cost == 0 means S := 0, i.e. admit any positive benefit)
+      bool ok;
+      if (P.selection == SMART_FROZEN) {
+        ok = (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > rhs0 * dc0) : (bj > 0.0);
+      } else {
+        const double C = L.ctab[j];
+        ok = (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
       }
-      if (j < ne) {
-        const double before = run + (incl - bj);  // sum of b over positions < j
-        // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
-        // cost == 0 means S := 0, i.e. admit any positive benefit)
-        bool ok;
-        if (P.selection == SMART_FROZEN) {
-          ok = (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > P.c_T * ((double)P.omega * bc + E0) * dc0) : (bj > 0.0);
-        } else {
-          const double C = L.ctab[j];
-          ok = (C > 0.0) ? (ac * bj * C > P.c_T * ((double)P.omega * bc + E0 + before) * L.dtab[j]) : (bj > 0.0);
-        }
-        if (!ok && j < first_fail) first_fail = j;
-        const double Sa = sp(E0 + before + bj, j + 1);
-        if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
-          bestS = Sa;
-          bestj = j + 1;
-        }
+      if (!ok && j < first_fail) first_fail = j;
+      const double Sa = sp(E0 + before + bj, j + 1);
+      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+        bestS = Sa;
+        bestj = j + 1;
       }
-      run += __shfl_sync(kFull, incl, 31);
+      before += bj;
     }
+    first_fail = __reduce_min_sync(kFull, first_fail);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      first_fail = min(first_fail, __shfl_xor_sync(kFull, first_fail, o));
       const double os = __shfl_xor_sync(kFull, bestS, o);
       const int oj = __shfl_xor_sync(kFull, bestj, o);
       if (os > bestS || (os == bestS && oj < bestj)) {
@@ -485,15 +508,16 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       }
     }
     const int js = first_fail;
-    // sum of the admitted benefits (same tile structure as the prefix above)
-    double adm_b = 0.0;
-    for (int t = 0; t < js; t += 32) {
-      double v = (t + lane < js) ? (double)sel_key_b(L.keys[t + lane]) : 0.0;
+    // sum of the admitted benefits (lane chunks, xor tree: a function of (ne, js) only)
+    double ab = 0.0;
+    for (int j = j0; j < min(j1, js); ++j) ab += (double)sel_key_b(L.keys[j]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-      adm_b += v;
-    }
+    for (int o = 16; o > 0; o >>= 1) ab += __shfl_xor_sync(kFull, ab, o);
     if (lane == 0) {
+      ss.bcast_i[3] = js;
+      ss.bcast_d[1] = ab;
+      ss.bcast_d[2] = E0;
+      ss.bcast_l[0] = N0;
       tr.executed = R_all > 0 ? 1 : 0;
       tr.n_rows = R;
       tr.n_cand = nct;
@@ -507,94 +531,129 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       tr.saturated = (N0 + ne >= P.sat_from) ? 1 : 0;
       if (tr.saturated) atomicOr(P.err, kErrSaturated);
     }
-    stamp(P, lane == 0, 13);
-    // ---- A6: commit (own requests) ----
-    for (int j = lane; j < js; j += 32) {
-      const unsigned long long key = L.keys[j];
-      const int r = sel_key_r(key) - P.b_off;
-      if (r >= 0 && r < bl) L.pre[L.off[r] * k + sel_key_c(key)] = 1;
-    }
-    __syncwarp();
-    for (int q = lane; q < nct; q += 32) P.cand_adm[lbase + q] = L.pre[q];
-    // per request (lane-strided): admitted count, finish, next-frontier count
+  }
+  blk_sync<NT>();  // B5
+  const int js = ss.bcast_i[3];
+  stamp(P, tid == 0, 13);
+
+  // ---- A6: commit (own requests) ----
+  for (int j = tid; j < js; j += NT) {
+    const unsigned long long key = L.keys[j];
+    const int r = sel_key_r(key) - P.b_off;
+    if (r >= 0 && r < bl) L.pre[L.off[r] * k + sel_key_c(key)] = 1;
+  }
+  blk_sync<NT>();  // B6
+  if (warp == 0) {
+    // per request (lane-strided): admitted count, finish, next-frontier count, NODE_SUM E
     for (int r = lane; r < bl; r += 32) {
       const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
       int a = 0;
-      for (int q = s0; q < s1; ++q) a += L.pre[q];
+      double esum = 0.0;
+      for (int q = s0; q < s1; ++q)
+        if (L.pre[q]) {
+          ++a;
+          esum += (double)L.cum[q];  // canonical order (c asc)
+        }
       L.adm[r] = a;
       const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
       L.nxt[r] = fin ? 0 : a;
       L.base[r] = fin ? 0 : a;
       P.fr_cnt[npar][r] = fin ? 0 : a;
       if (fin && L.cnt[r] > 0) P.finished[r] = 1;
+      P.n_nodes[r] = L.nd[r] + 1 + a;
+      if (!pmean && a > 0) {
+        const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
+        L.E[gi] += esum;  // node sum (Q11)
+        P.E_r[r] = L.E[gi];
+      }
     }
     __syncwarp();
     const int total = warp_excl_scan_smem(L.base, bl, lane);
     for (int r = lane; r < bl; r += 32) P.fr_off[npar][r] = L.base[r];
     if (lane == 0) *P.fr_total[npar] = total;
-    // nodes in canonical order (c asc) + E bookkeeping, one lane per request (deterministic)
-    for (int r = lane; r < bl; r += 32) {
-      const int a = L.adm[r];
-      if (a == 0) continue;
-      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
-      const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
-      const int n0 = L.nd[r] + 1;
-      int rank = 0;
-      double esum = 0.0, psum_new = 0.0, psum_par = 0.0;
-      int nparents = 0;
-      for (int q0 = s0; q0 < s1; q0 += k) {
-        bool any = false;
-        for (int q = q0; q < q0 + k; ++q) {
-          if (!L.pre[q]) continue;
-          const Cand cd = L.cd[q];
-          const int node = n0 + rank;
-          const size_t o = (size_t)r * P.T + node;
-          P.tok[o] = cd.tok;
-          P.parent[o] = cd.parent;
-          P.depth[o] = layer;
-          P.p[o] = cd.p;
-          P.cum[o] = cd.cum;
-          esum += (double)cd.cum;
-          if (P.accept_model == SMART_PATH_MEAN) {
-            const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
-            P.path_sum[o] = pps + (double)cd.cum;
-            psum_new += pps + (double)cd.cum;
+  } else {
+    // per candidate: admitted flag, node records in canonical order (c asc), parent path sums
+    for (int q = tid - 32; q < nct; q += NT - 32) {
+      const int f = L.pre[q];
+      P.cand_adm[lbase + q] = f;
+      if (!f) continue;
+      const int r = L.crow[q];
+      const int s0 = L.off[r] * k;
+      int idx = 0;
+      for (int j = s0; j < q; ++j) idx += L.pre[j];
+      L.nix[q] = idx;
+      const Cand cd = L.cd[q];
+      const int node = L.nd[r] + 1 + idx;
+      const size_t o = (size_t)r * P.T + node;
+      P.tok[o] = cd.tok;
+      P.parent[o] = cd.parent;
+      P.depth[o] = layer;
+      P.p[o] = cd.p;
+      P.cum[o] = cd.cum;
+      if (pmean) {
+        const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
+        L.pps[q] = pps;
+        P.path_sum[o] = pps + (double)cd.cum;
+      }
+    }
+  }
+  blk_sync<NT>();  // B7
+  stamp(P, tid == 0, 14);
+  // next frontier (own requests that continue), with the cum of each node for the row merge
+  for (int q = tid; q < nct; q += NT) {
+    if (!L.pre[q]) continue;
+    const int r = L.crow[q];
+    if (L.nxt[r] == 0) continue;
+    const int idx = L.nix[q];
+    P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+    P.fr_cum[npar][L.base[r] + idx] = L.cum[q];
+  }
+  if (warp == 0) {
+    if (pmean) {
+      // Eq.(2) path mean of the committed tree: leaves lose their admitted-into parents
+      for (int r = lane; r < bl; r += 32) {
+        if (L.adm[r] == 0) continue;
+        const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+        double psum_new = 0.0, psum_par = 0.0;
+        int nparents = 0;
+        for (int q0 = s0; q0 < s1; q0 += k) {
+          bool any = false;
+          for (int q = q0; q < q0 + k; ++q) {
+            if (!L.pre[q]) continue;
+            const double pps = L.pps[q];
+            psum_new += pps + (double)L.cum[q];
             if (!any) {
               psum_par += pps;
               ++nparents;
             }
+            any = true;
           }
-          any = true;
-          if (L.nxt[r] > 0) P.fr[npar][L.base[r] + rank] = make_int2(r, node);
-          ++rank;
         }
-      }
-      P.n_nodes[r] = n0 + a;
-      if (P.accept_model == SMART_PATH_MEAN) {
-        const int lc = P.leaf_cnt[r] - nparents + a;
+        const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
+        const int lc = P.leaf_cnt[r] - nparents + L.adm[r];
         const double ls = P.leaf_sum[r] - psum_par + psum_new;
         P.leaf_cnt[r] = lc;
         P.leaf_sum[r] = ls;
-        L.E[gi] = ls / (double)lc;  // Eq.(2) path mean of the committed tree
-      } else {
-        L.E[gi] += esum;  // node sum (Q11)
+        L.E[gi] = ls / (double)lc;
+        P.E_r[r] = L.E[gi];
       }
-      P.E_r[r] = L.E[gi];
+      __syncwarp();
     }
-    __syncwarp();
     // ---- totals after the layer (trace S_after) ----
+    const double E0 = ss.bcast_d[2];
+    const long long N0w = ss.bcast_l[0];
     if (mode == kSelFull) {
       const double Ea = warp_det_sum(L.E, bl, lane);
       if (lane == 0) {
         tr.S_after = sp(Ea, js) / bc;
-        *P.N_glob = (int)(N0 + js);
+        *P.N_glob = (int)(N0w + js);
         *P.E_glob = Ea;
       }
     } else if (lane == 0) {
       // NODE_SUM: E after = E0 + sum of admitted benefits (exact); PATH_MEAN: approximate
-      const double Ea = E0 + adm_b;
+      const double Ea = E0 + ss.bcast_d[1];
       tr.S_after = sp(Ea, js) / bc;
-      *P.N_glob = (int)(N0 + js);
+      *P.N_glob = (int)(N0w + js);
       *P.E_glob = Ea;
     }
     stamp(P, lane == 0, 22);

@@ -24,6 +24,7 @@ constexpr int kMaxK = 32;
 constexpr int kMaxCpr = 64;   // chunks per row (V*esz <= 1 MiB)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr int kIdxSentinel = 0x7fffffff;
+constexpr int kStageRows = 64;  // row descriptors a streaming CTA stages in shared memory
 
 // error flag bits (smart_stats.error_flags)
 constexpr int kErrDraftNaN = 1;
@@ -72,6 +73,7 @@ struct Params {
 
   // ---- frontier, ping-pong by layer parity ----
   int2* fr[2];        // (local request, node)
+  float* fr_cum[2];   // cum of each frontier node (prefetched by the row merge)
   int* fr_cnt[2];     // [b_loc]
   int* fr_off[2];     // [b_loc] exclusive prefix
   int* fr_total[2];   // [1]
@@ -112,6 +114,7 @@ struct Params {
   int* vseglen;       // [b_loc*T*cpr]
   int* vrow_arg;      // [b_loc*T]
   int* vrow_off;      // [b_loc+1]
+  int2* vrow_rn;      // [b_loc*T] (request, node) of each verify row (written by the mask kernel)
   int* req_done;      // [b_loc]
 
   // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----
@@ -166,6 +169,12 @@ __device__ __forceinline__ float tk_val(unsigned long long key) {
 __device__ __forceinline__ int tk_idx(unsigned long long key) { return (int)(0xffffffffu - (uint32_t)key); }
 constexpr unsigned long long kKeySentinel = 0x007fffff80000000ull;  // tk_key(-inf, INT_MAX)
 
+// one-instruction warp max (sm_100a redux.sync .f32; NaN inputs ignored like fmaxf)
+__device__ __forceinline__ float warp_max_fast(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
@@ -187,6 +196,31 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
+// Programmatic dependent launch: every kernel of the step is launched with programmatic stream
+// serialization, runs its shared-memory prologue, then waits for the previous kernel of the
+// stream (griddepcontrol.wait: full completion + memory visibility) before its first global read,
+// and immediately lets the next kernel launch (its CTAs take resources as ours retire).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // api.cu: off with SMART_NO_PDL=1
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -199,6 +233,19 @@ __device__ __forceinline__ void probe_min(const Params& P, int slot) {
 }
 __device__ __forceinline__ void probe_max(const Params& P, int slot) {
   if (P.dbg) atomicMax(&P.dbg[slot], gtime());
+}
+// kernel timeline (dbg[64 + 2*kid] = min start, dbg[65 + 2*kid] = max end); kid: 0 begin,
+// 1..d layer kernels, 20 mask, 21 verify, 22 select kernel; kid + 32: CTA launch (before the
+// dependency wait)
+__device__ __forceinline__ void tl_start(const Params& P, int kid) {
+  if (P.dbg && threadIdx.x == 0) atomicMin(&P.dbg[64 + 2 * kid], gtime());
+}
+__device__ __forceinline__ void tl_end(const Params& P, int kid) {
+  if (P.dbg && threadIdx.x == 0) atomicMax(&P.dbg[65 + 2 * kid], gtime());
+}
+// globaltimer stamp of one thread into dbg[slot] (slots 16..31: CTA 0 timeline)
+__device__ __forceinline__ void gstamp(const Params& P, bool on, int slot) {
+  if (P.dbg && on) P.dbg[slot] = gtime();
 }
 // cycle stamps (clock64) of one thread into dbg[32 + slot]
 __device__ __forceinline__ void stamp(const Params& P, bool on, int slot) {

@@ -68,47 +68,47 @@ struct StreamPipe {
 
 // smem layout of a streaming CTA: [ring kStages x 16 KiB][pipe][kernel-specific]
 struct RowRange {
-  long long lo, hi;
+  int lo, hi;  // [lo, hi) of the (row, chunk) units, row-major; totals < 2^31 (checked at create)
 };
 
-// balanced ranges over min(gridDim.x, ceil(total / min_units)) CTAs: small layers use fewer CTAs
-// with several chunks each (all in flight through the TMA ring) instead of many 1-chunk CTAs
-__device__ __forceinline__ RowRange cta_range_min(long long total, int min_units) {
-  long long g = (total + min_units - 1) / min_units;
-  if (g > gridDim.x) g = gridDim.x;
+// balanced contiguous ranges over min(gridDim.x, ceil(total / min_units)) CTAs (32-bit integer
+// math only): small layers use fewer CTAs with several chunks each, all in flight in the ring
+__device__ __forceinline__ RowRange cta_range_min(int total, int min_units) {
+  int g = (total + min_units - 1) / min_units;
+  if (g > (int)gridDim.x) g = (int)gridDim.x;
   RowRange r;
-  if ((long long)blockIdx.x >= g) {
+  const int b = (int)blockIdx.x;
+  if (b >= g) {
     r.lo = r.hi = 0;
     return r;
   }
-  r.lo = total * blockIdx.x / g;
-  r.hi = total * (blockIdx.x + 1) / g;
-  return r;
-}
-
-__device__ __forceinline__ RowRange cta_range(long long total) {
-  RowRange r;
-  r.lo = total * blockIdx.x / gridDim.x;
-  r.hi = total * (blockIdx.x + 1) / gridDim.x;
+  const int base = total / g, rem = total - base * g;
+  r.lo = b * base + min(b, rem);
+  r.hi = r.lo + base + (b < rem ? 1 : 0);
   return r;
 }
 
 // Producer loop (one elected lane): stream chunks [lo, hi) of rows whose base pointer is given
-// by `row_base(row)`; each row is `row_bytes` long (16-byte multiple).
+// by `row_base(row)`; each row is `row_bytes` long (16-byte multiple).  (row, chunk) advance
+// incrementally (no division per chunk).
 template <class RowBase>
 __device__ __forceinline__ void produce(StreamPipe& pipe, char* ring, RowRange rr, int cpr, long long row_bytes,
                                         RowBase row_base) {
-  long long i = 0;
-  for (long long q = rr.lo; q < rr.hi; ++q, ++i) {
-    const int s = (int)(i % kStages);
+  int row = rr.lo / cpr, c = rr.lo - row * cpr;
+  const char* base = row_base(row);
+  int i = 0;
+  for (int q = rr.lo; q < rr.hi; ++q, ++i) {
+    const int s = i % kStages;
     const uint32_t n = (uint32_t)(i / kStages);
     mbar_wait(&pipe.empty[s], (n & 1u) ^ 1u);
-    const int row = (int)(q / cpr), c = (int)(q % cpr);
     const long long off = (long long)c * kChunkBytes;
     const uint32_t bytes = (uint32_t)min((long long)kChunkBytes, row_bytes - off);
-    const char* src = row_base(row) + off;
     mbar_expect_tx(&pipe.full[s], bytes);
-    bulk_g2s(ring + (size_t)s * kChunkBytes, src, bytes, &pipe.full[s]);
+    bulk_g2s(ring + (size_t)s * kChunkBytes, base + off, bytes, &pipe.full[s]);
+    if (++c == cpr) {
+      c = 0;
+      if (q + 1 < rr.hi) base = row_base(++row);
+    }
   }
 }
 

@@ -42,11 +42,15 @@ for rep in range(3):
             print(f"layer {layer}: last CTA start {rel(1)} stream_end {rel(2)} first_merge {rel(8)} "
                   f"last_merge {rel(3)}->{rel(4)} select {rel(5)}->{rel(6)} end {rel(7)} us; select phases "
                   f"stage {rel(9)} rank {rel(10)} sort {rel(11)} rule {rel(12)} fscan {rel(13)} nodes {rel(14)}")
-            print("   CTA0: start", rel(26), "chunks (wait-start, data) ", [(rel(16 + 2 * j), rel(17 + 2 * j)) for j in range(4)],
-                  "seg_end", rel(24), "after_sync", rel(25))
-            cyc = [int(buf[j]) for j in (27, 28, 29, 15)]
-            print("   chunk1 cycles: data->Mw", cyc[1] - cyc[0], "Mw->ms", cyc[2] - cyc[1], "ms->end", cyc[3] - cyc[2])
-            st = [int(buf[32 + j]) for j in range(23)]
+            print("   CTA0: R read", rel(16), "init", rel(17), "producer", rel(27),
+                  "chunk0 (full, softmax, topk)", rel(18), rel(19), rel(20), "chunk1", rel(21), rel(22), rel(23),
+                  "seg compact", rel(24), "cta merge", rel(25), "arrival", rel(26))
+            st = [int(buf[32 + j]) for j in range(32)]
+            print("   CTA0 warp0 chunk0 cycles: lds+unpack", st[1] - st[0], "lanemax", st[2] - st[1], "Mw", st[3] - st[2],
+                  "sumexp+store", st[4] - st[3], "seed", st[5] - st[4], "scan", st[6] - st[5])
+            print("   CTA0 after sync", rel(28), "cta merge pass1 end", rel(31), "pass2 end", rel(25))
+            print("   row0 merge:", rel(29), "->", rel(30), "cycles: loads", st[25] - st[24], "MZ", st[26] - st[25],
+                  "T", st[27] - st[26], "surv", st[28] - st[27], "rank", st[29] - st[28], "tail", st[30] - st[29])
             d = lambda a, b: st[b] - st[a] if st[a] and st[b] else None
             print("   seg_end cycles: compact", d(0, 1), "fence", d(1, 2), "sync", d(2, 3), "rankmerge", d(3, 4),
                   "seglen+fence", d(4, 5), "sync", d(5, 6), "atomic", d(6, 7), "sync", d(7, 8))
