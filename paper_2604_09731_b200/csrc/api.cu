@@ -347,7 +347,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     if (e != cudaSuccess) P.dbg = nullptr;
   }
   // launch geometry: persistent streaming grids sized to the SM count
-  c->grid_expand = c->num_sms * expand_occupancy();
+  c->grid_expand = expand_grid(P.cpr, P.k);
   c->grid_verify = c->num_sms * verify_occupancy();
   // selection: fused into the layer kernel when its scratch fits the stream ring, else the
   // standalone 1024-thread select kernel
@@ -355,7 +355,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
   P.sort_cap = sort_cap;
   c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1);
-  c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && !getenv("SMART_NO_FUSE");
+  c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && c->grid_expand >= 16 && !getenv("SMART_NO_FUSE");
   if (c->select_smem > 220 * 1024) {
     cudaFree(c->ws);
     cudaFree(c->cost_dev);

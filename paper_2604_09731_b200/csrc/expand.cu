@@ -3,10 +3,16 @@
 // layer's selection A3-A6 fused into the tail of the last CTA (single rank).
 //
 // Design:
-//  * HBM stream, TMA-staged: the frontier rows are cut into 16 KiB chunks; a persistent grid
-//    (#SMs x 2 CTAs) takes balanced contiguous ranges of (row, chunk) units.  A producer warp
-//    bulk-copies chunks (cp.async.bulk + mbarrier tx count) into a 6-stage shared-memory ring;
-//    8 consumer warps read 16-byte vectors from it.
+//  * Row teams in thread-block clusters: the persistent grid is made of 8-CTA clusters; from the
+//    layer's row count R each cluster is cut into teams of t in {8,4,2,1} CTAs (the largest t
+//    with R <= #teams, t <= chunks per row), and team n streams rows n, n + #teams, ...  Each
+//    member CTA takes a balanced slice of every row's 16 KiB chunks; its partial results go
+//    straight into the team leader's shared memory (DSMEM stores + one remote mbarrier arrive),
+//    and a dedicated merge warp in the leader finishes the row: no global round trip between
+//    the stream and the row result.
+//  * HBM stream, TMA-staged: per CTA a producer warp bulk-copies chunks (cp.async.bulk +
+//    mbarrier tx count) into a 6-stage shared-memory ring; 8 consumer warps read 16-byte
+//    vectors from it.
 //  * softmax: each consumer warp reduces its 1024 (bf16) / 512 (fp32) elements of a chunk to
 //    (max, sum exp) with a fixed shuffle tree; the row merge combines the cpr x 8 partials in
 //    fixed order, so Z is bit-identical for any grid size or sharding.
@@ -17,9 +23,9 @@
 //    by compactions and a CTA-wide hint.  Only the 16-byte vectors whose max reaches the bound
 //    are scanned; qualifying elements are appended to a per-warp buffer in shared memory, which
 //    is compacted to its top-k (rank counting) when full and at the segment end.
-//  * the CTA that completes a row's last chunk merges that row (Z, exact top-k, p, cum); the CTA
-//    that merges the layer's last row runs the selection for the whole batch (select_core.cuh).
-//    Arrival counters use one acq_rel atomic per CTA after a CTA barrier (no per-thread fences).
+//  * the leader's merge warp computes Z (association fixed by the chunk count), the exact top-k
+//    of the members' lists (threshold + rank), p and cum; the CTA whose merge warp completes the
+//    layer's last row (one acq_rel arrival per row) runs the selection (select_core.cuh).
 #include "select_core.cuh"
 #include "stream.cuh"
 
@@ -85,44 +91,84 @@ __device__ __forceinline__ void load_direct(const char* row, int chunk_base, int
   }
 }
 
-// logits row of frontier row `row` (layer parity `par`); rows [row0, row0 + kStageRows) use the
-// frontier entries staged in shared memory
-__device__ __forceinline__ const char* row_ptr(const Params& P, int par, const char* base, long long ld_bytes,
-                                              int row, const int2* rfe, int row0) {
-  if (P.row_mode == SMART_ROWS_NODE) {
-    const int2 fe = (row - row0 < kStageRows) ? rfe[row - row0] : P.fr[par][row];
-    return base + ((long long)fe.x * P.T + fe.y) * ld_bytes;
-  }
-  return base + (long long)row * ld_bytes;
-}
-
 // per-warp top-k state in shared memory (64-bit keys)
 struct WarpTopk {
-  unsigned long long buf[kSegBuf];  // candidates of the current segment (appended; compacted)
+  unsigned long long buf[kSegBuf];  // candidates of the current row slice (appended; compacted)
   unsigned long long list[kMaxK];   // compacted top-k, sorted best first
 };
 
+constexpr int kCluster = 8;                          // CTAs per cluster (portable maximum)
+constexpr int kMergeWarp = kConsumerWarps + 1;       // warp 9: row merges in team leaders
+constexpr int kLayerThreadsT = kLayerThreads + 32;   // 320 threads: consumers, producer, merger
+
 struct ExpandShared {
-  int2 rfe[kStageRows];  // frontier entries of the CTA's first rows
-  unsigned pub[2][kConsumerWarps * 4];  // per chunk (double-buffered): top-j lane maxima of each warp
-  unsigned long long cl[kConsumerWarps * kMaxK];  // segment end: each warp's top-k (distinct sentinels)
-  int last_layer;
+  int2 rfe[kStageRows];                           // frontier entries of the team's rows
+  float rcum[kStageRows];                         // their path scores (cum of the parent node)
+  unsigned pub[2][kConsumerWarps * 4];            // per chunk: top-j lane maxima of each warp
+  unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k (distinct sentinels)
+  uint64_t ready[2];  // leader: all members' partials of the team's n-th row are in (parity n & 1)
+  uint64_t freeb[2];  // every CTA: the leader has consumed buffer parity p (remote arrive)
   WarpTopk w[kConsumerWarps];
 };
 
-// row-merge staging, carved from the dynamic shared memory after ExpandShared (sized by cpr, k)
-struct MergeStage {
-  unsigned long long* keys;  // [cpr * k] segment lists (valid at segment-start chunks)
-  unsigned long long* surv;  // [cpr * k] survivors of the threshold
+// team buffers (double-buffered by row parity), carved after ExpandShared, written remotely by
+// the members into the leader's copy: softmax partials [cpr][8 warps] and lists [kCluster][k]
+struct TeamBuf {
+  float2* ms[2];
+  unsigned long long* lists[2];
+  unsigned long long* surv;  // merge scratch [kCluster * k]
 };
 
-__host__ __device__ inline size_t merge_stage_bytes(int cpr, int k) { return (size_t)cpr * k * 16; }
+__host__ __device__ inline size_t team_buf_bytes(int cpr, int k) {
+  return 2 * ((size_t)cpr * kConsumerWarps * 8 + (size_t)kCluster * k * 8) + (size_t)kCluster * k * 8;
+}
 
-__device__ inline MergeStage merge_stage(char* base, int cpr, int k) {
-  MergeStage m;
-  m.keys = reinterpret_cast<unsigned long long*>(base);
-  m.surv = m.keys + (size_t)cpr * k;
-  return m;
+__device__ inline TeamBuf team_buf(char* base, int cpr, int k) {
+  TeamBuf t;
+  char* p = base;
+  for (int b = 0; b < 2; ++b) {
+    t.ms[b] = reinterpret_cast<float2*>(p);
+    p += (size_t)cpr * kConsumerWarps * 8;
+    t.lists[b] = reinterpret_cast<unsigned long long*>(p);
+    p += (size_t)kCluster * k * 8;
+  }
+  t.surv = reinterpret_cast<unsigned long long*>(p);
+  return t;
+}
+
+// ---- cluster / DSMEM primitives ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {  // local smem -> cluster address
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void st_cluster_f2(uint32_t a, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a, uint32_t count) {  // remote, release.cluster
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Warp-level compaction: list <- top-k of buf[0..n) by rank counting (keys distinct); ranks >= n
@@ -142,108 +188,54 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
   __syncwarp();
 }
 
-// ---- row merge by one warp of the CTA that completed the row (no CTA barriers) ----
-// One load wave (partials, segment lengths, segment lists, frontier entry and its cum), then:
-// M = max, Z = sum s*exp(m - M) with an association fixed by cpr; T = the best k-th entry over
-// the segment lists (a lower bound of the row's k-th best key, every list holding its segment's
-// top-k); the entries >= T are ranked among themselves and the top k written with p and cum.
-__device__ void merge_row_warp(const Params& P, int layer, int par, int row, MergeStage st) {
+// ---- row merge by the team leader's merge warp, from its own shared memory ----
+// M = max, Z = sum s*exp(m - M) over the row's cpr x 8 partials (association fixed by cpr);
+// T = the best k-th entry over the members' lists (each list is its slice's top-k, so T bounds the
+// row's k-th best key from below); the entries >= T are ranked among themselves and the top k
+// written with p (A1) and cum (A2, Eq.(3)).
+__device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int t,
+                               const float2* ms, const unsigned long long* lists, unsigned long long* surv) {
   const int lane = threadIdx.x & 31;
-  const bool sp = (row == 0 && lane == 0);
-  stamp(P, sp, 24);
   const int k = P.k, cpr = P.cpr;
   const int npart = cpr * kConsumerWarps;  // <= 512
-  const int nkey = cpr * k;                // <= 2048
-  // ---- load wave ----
-  const float2* ms = P.ms + (size_t)row * npart;
-  float2 part[kMaxCpr * kConsumerWarps / 32];
-#pragma unroll
-  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t)
-    part[t] = (lane + 32 * t < npart) ? __ldcg(&ms[lane + 32 * t]) : make_float2(-INFINITY, 0.f);
-  int* sl = P.seglen + (size_t)row * cpr;
-  const int sl0 = lane < cpr ? __ldcg(&sl[lane]) : 0;
-  const int sl1 = lane + 32 < cpr ? __ldcg(&sl[lane + 32]) : 0;
-  const unsigned long long* sk = P.segkey + (size_t)row * nkey;
-  for (int e0 = 0; e0 < nkey; e0 += 256) {  // batches of independent loads, then the stores
-    unsigned long long v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 32 + lane;
-      v[u] = e < nkey ? __ldcg(&sk[e]) : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 32 + lane;
-      if (e < nkey) st.keys[e] = v[u];
-    }
-  }
-  int2 fe = make_int2(0, 0);
-  float pc = 0.f;
-  if (lane == 0) {
-    fe = P.fr[par][row];
-    pc = P.fr_cum[par][row];
-  }
-  if (lane < cpr) sl[lane] = 0;  // self-cleaning for the next use
-  if (lane + 32 < cpr) sl[lane + 32] = 0;
-  stamp(P, sp, 25);
-  // ---- (1) softmax normaliser ----
+  // (1) softmax normaliser
   float m = -INFINITY;
-#pragma unroll
-  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t) m = fmaxf(m, part[t].x);
+  for (int q = lane; q < npart; q += 32) m = fmaxf(m, ms[q].x);
   const float M = warp_max_fast(m);
   const float ML = M * kLog2e;
   float z = 0.f;
-#pragma unroll
-  for (int t = 0; t < kMaxCpr * kConsumerWarps / 32; ++t) {
-    const float2 v = part[t];
+  for (int q = lane; q < npart; q += 32) {
+    const float2 v = ms[q];
     if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
   }
   const float Z = warp_sum(z);
-  stamp(P, sp, 26);
-  // ---- (2) threshold T = max over segments of their k-th entry ----
-  const unsigned long long v0 = __ballot_sync(kFull, sl0 > 0), v1 = __ballot_sync(kFull, sl1 > 0);
-  __syncwarp();  // st.keys visible
-  unsigned long long tail = 0ull;
-  if (sl0 > 0) tail = st.keys[lane * k + k - 1];
-  if (sl1 > 0 && st.keys[(lane + 32) * k + k - 1] > tail) tail = st.keys[(lane + 32) * k + k - 1];
+  // (2) threshold: best tail over the members' lists
+  const unsigned long long tail = lane < t ? lists[lane * k + k - 1] : 0ull;
   const unsigned th = __reduce_max_sync(kFull, (unsigned)(tail >> 32));
   const unsigned tl = __reduce_max_sync(kFull, (unsigned)(tail >> 32) == th ? (unsigned)tail : 0u);
   const unsigned long long T = ((unsigned long long)th << 32) | tl;
-  stamp(P, sp, 27);
-  // ---- (3) survivors (entries >= T of existing segments), compacted by ballot ----
-  const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;  // e / k == umulhi(e, kmag) (k >= 2, e < 2^16)
+  // (3) survivors, compacted by ballot
+  const int nkey = t * k;
   int ns = 0;
   for (int e0 = 0; e0 < nkey; e0 += 32) {
     const int e = e0 + lane;
-    bool sv = false;
-    unsigned long long key = 0ull;
-    if (e < nkey) {
-      const int c = (k == 1) ? e : (int)__umulhi((unsigned)e, kmag);
-      const bool valid = c < 32 ? ((v0 >> c) & 1ull) : ((v1 >> (c - 32)) & 1ull);
-      if (valid) {
-        key = st.keys[e];
-        sv = key >= T;
-      }
-    }
+    const unsigned long long key = e < nkey ? lists[e] : 0ull;
+    const bool sv = e < nkey && key >= T;
     const unsigned bal = __ballot_sync(kFull, sv);
-    if (sv) st.surv[ns + __popc(bal & ((1u << lane) - 1u))] = key;
+    if (sv) surv[ns + __popc(bal & ((1u << lane) - 1u))] = key;
     ns += __popc(bal);
   }
   __syncwarp();
-  stamp(P, sp, 28);
-  // ---- (4) exact top-k among the survivors by rank; A1 p and A2 cum ----
-  fe.x = __shfl_sync(kFull, fe.x, 0);
-  fe.y = __shfl_sync(kFull, fe.y, 0);
-  pc = __shfl_sync(kFull, pc, 0);
+  // (4) exact top-k among the survivors; A1 p and A2 cum
   for (int s0 = lane; s0 < ns; s0 += 32) {
-    const unsigned long long key = st.surv[s0];
+    const unsigned long long key = surv[s0];
     int r0 = 0, r1 = 0;
-    int t = 0;
-    for (; t + 1 < ns; t += 2) {
-      r0 += (st.surv[t] > key);
-      r1 += (st.surv[t + 1] > key);
+    int q = 0;
+    for (; q + 1 < ns; q += 2) {
+      r0 += (surv[q] > key);
+      r1 += (surv[q + 1] > key);
     }
-    if (t < ns) r0 += (st.surv[t] > key);
+    if (q < ns) r0 += (surv[q] > key);
     const int rank = r0 + r1;
     if (rank < k) {
       const float v = tk_val(key);
@@ -256,19 +248,16 @@ __device__ void merge_row_warp(const Params& P, int layer, int par, int row, Mer
       P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
     }
   }
-  stamp(P, sp, 29);
   if (lane == 0) {
     P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, row - P.fr_off[par][fe.x]);
     P.rowstat[row] = make_float2(M, Z);
     if (!(Z >= 1.0f) || isinf(Z) || isnan(M)) atomicOr(P.err, kErrDraftNaN);  // Q23
-    P.row_done[row] = 0;
   }
   __syncwarp();
-  stamp(P, sp, 30);
 }
 
 template <bool BF16, bool TMA>
-__global__ void __launch_bounds__(kLayerThreads, 2)
+__global__ void __launch_bounds__(kLayerThreadsT, 2)
 layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_bytes, int fuse_select) {
   constexpr int EPT = Traits<BF16>::EPT;
   constexpr int EPV = Traits<BF16>::EPV;
@@ -276,300 +265,339 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   char* ring = dsm;
   StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
   ExpandShared& sh = *reinterpret_cast<ExpandShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
-  const MergeStage mst =
-      merge_stage(dsm + kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(ExpandShared), P.cpr, P.k);
+  const TeamBuf tb = team_buf(dsm + kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(ExpandShared), P.cpr, P.k);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (layer - 1) & 1;
+  const uint32_t crank = cluster_ctarank();
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&pipe.full[s], 1);
       mbar_init(&pipe.empty[s], kConsumerWarps);
     }
+    mbar_init(&sh.ready[0], kCluster);  // members arrive with count kCluster / t
+    mbar_init(&sh.ready[1], kCluster);
+    mbar_init(&sh.freeb[0], 1);
+    mbar_init(&sh.freeb[1], 1);
     mbar_fence_init();
-    sh.last_layer = 0;
   }
+  cluster_sync_all();  // barriers initialised cluster-wide before any remote arrive
   tl_start(P, 32 + layer);
   pdl_wait();
   pdl_trigger();
   tl_start(P, layer);
-  if (tid == 0) {
-    probe_min(P, 0);
-    probe_max(P, 1);
-  }
   const int R = *P.fr_total[par];
   const bool t0 = (blockIdx.x == 0 && tid == 0);
   gstamp(P, t0, 16);
   if (R == 0) {
     // A_{l-1} is empty for every request: the step has terminated at this layer
     if (fuse_select && blockIdx.x == 0 && tid == 0) *P.fr_total[layer & 1] = 0;
-    return;
+    return;  // no remote traffic in this launch: early exit is safe
   }
   const int k = P.k, cpr = P.cpr, CE = P.chunk_elems, V = P.V;
   const long long row_bytes = (long long)V * (BF16 ? 2 : 4);
-  const RowRange rr = cta_range_min(R * cpr, P.min_units);
-  if (rr.lo >= rr.hi) return;
-  // the CTA's frontier entries, staged once (no dependent global load per chunk)
-  const int row0 = rr.lo / cpr;
-  const int nstage = min((rr.hi - 1) / cpr - row0 + 1, kStageRows);
-  if (tid < nstage) sh.rfe[tid] = P.fr[par][row0 + tid];
+  // ---- team layout from R: largest t in {8,4,2,1} with R <= #teams and t <= cpr ----
+  // with the fused selection the grid's last cluster is reserved: its rank-0 CTA runs A3-A6
+  const int S = fuse_select ? (int)gridDim.x - kCluster : (int)gridDim.x;
+  const bool sel_cta = fuse_select && (int)blockIdx.x == S;
+  int t = kCluster;
+  while (t > 1 && (R > S / t || t > cpr)) t >>= 1;
+  const int nteams = S / t;
+  const int team = blockIdx.x / t, member = blockIdx.x % t;
+  const uint32_t lrank = crank - (uint32_t)member;  // the team leader's rank in the cluster
+  const int nrows = ((int)blockIdx.x < S && team < R) ? (R - team + nteams - 1) / nteams : 0;
+  const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;  // this CTA's chunks of each row
+  const int nstage = min(nrows, kStageRows);
+  if (tid < nstage) {
+    const int row = team + tid * nteams;
+    sh.rfe[tid] = P.fr[par][row];
+    sh.rcum[tid] = P.fr_cum[par][row];
+  }
   __syncthreads();
   gstamp(P, t0, 17);
+  auto rowfe = [&](int n, int row) { return n < kStageRows ? sh.rfe[n] : P.fr[par][row]; };
+  auto rowp = [&](int n, int row) -> const char* {
+    if (P.row_mode == SMART_ROWS_NODE) {
+      const int2 fe = rowfe(n, row);
+      return logits + ((long long)fe.x * P.T + fe.y) * ld_bytes;
+    }
+    return logits + (long long)row * ld_bytes;
+  };
 
-  if (warp == kConsumerWarps) {  // ---- producer warp ----
-    gstamp(P, blockIdx.x == 0 && lane == 0, 27);
-    if (TMA && lane == 0)
-      produce(pipe, ring, rr, cpr, row_bytes, [&](int row) { return row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0); });
-    return;
-  }
-
-  // ---- consumer warps ----
-  WarpTopk& W = sh.w[warp];
-  int wcnt = 0;  // entries in W.buf (warp-uniform)
-  int i = 0;
-  int q = rr.lo;
-  int row = row0, c0 = rr.lo - row0 * cpr;
-  while (q < rr.hi) {
-    const int nch = min(cpr - c0, rr.hi - q);
-    unsigned long long bound = 0ull;  // lower bound of the segment's k-th best key
-    for (int c = c0; c < c0 + nch; ++c, ++i) {
-      uint4 raw[kVecPerThread];
-      const int s = (int)(i % kStages);
-      if (TMA) {
-        mbar_wait(&pipe.full[s], (uint32_t)((i / kStages) & 1));
-        gstamp(P, t0 && i < 2, 18 + 3 * (int)i);
-        stamp(P, t0 && i == 0, 0);
-        const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
-      } else {
-        load_direct<BF16>(row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0), c * CE, V, tid, raw);
-      }
-      float x[EPT];
-      unpack<BF16>(raw, x);
-      stamp(P, t0 && i == 0, 1);
-      const int cbase = c * CE;
-      if (c == cpr - 1) {  // ragged last chunk: elements past the row end -> -inf
-#pragma unroll
-        for (int n = 0; n < EPT; ++n)
-          if (elem_index<BF16>(cbase, tid, n) >= V) x[n] = -INFINITY;
-      }
-      // ---- softmax partial of this (chunk, warp): max tree, 4 independent sum chains ----
-      float vm[kVecPerThread];
-#pragma unroll
-      for (int j = 0; j < kVecPerThread; ++j) {
-        float a0 = fmaxf(x[j * EPV], x[j * EPV + 1]);
-        float a1 = fmaxf(x[j * EPV + 2], x[j * EPV + 3]);
-        if (EPV == 8) {
-          a0 = fmaxf(a0, fmaxf(x[j * EPV + 4 % EPV], x[j * EPV + 5 % EPV]));
-          a1 = fmaxf(a1, fmaxf(x[j * EPV + 6 % EPV], x[j * EPV + 7 % EPV]));
-        }
-        vm[j] = fmaxf(a0, a1);
-      }
-      const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
-      stamp(P, t0 && i == 0, 2);
-      const float Mw = warp_max_fast(m);
-      stamp(P, t0 && i == 0, 3);
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-      if (Mw != -INFINITY) {
-        const float ML = Mw * kLog2e;
-#pragma unroll
-        for (int n = 0; n < EPT; ++n) s4[n & 3] += ex2(fmaf(x[n], kLog2e, -ML));
-      }
-      const float sacc = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
-      if (lane == 0) P.ms[((size_t)row * cpr + c) * kConsumerWarps + warp] = make_float2(Mw, sacc);
-      stamp(P, t0 && i == 0, 4);
-      gstamp(P, t0 && i < 2, 19 + 3 * (int)i);
-
-      // ---- top-k candidates of this warp-chunk ----
-      // CTA-wide bound for this chunk: every warp publishes its top-j lane maxima (j = ceil(k/8),
-      // one lane per round, so ties keep their multiplicity); these 8j values are distinct
-      // elements of the row, so their k-th largest v_k bounds the row's k-th best value from
-      // below and key(v_k, INT_MAX) bounds the segment's k-th best key.
-      {
-        const int jr = (k + kConsumerWarps - 1) / kConsumerWarps;
-        unsigned* pub = sh.pub[i & 1];
-        unsigned rem = (m == m) ? float_orderable(m) : 0u;
-        for (int r = 0; r < jr; ++r) {
-          const unsigned cur = __reduce_max_sync(kFull, rem);
-          const unsigned bal = __ballot_sync(kFull, rem == cur);
-          if (lane == __ffs(bal) - 1) rem = 0u;
-          if (lane == 0) pub[warp * jr + r] = cur;
-        }
-        consumer_sync();
-        const int np = kConsumerWarps * jr;
-        const unsigned u = lane < np ? pub[lane] : 0u;
-        int gt = 0;
-        for (int o = 0; o < np; o += 4) {
-          const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
-          gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
-        }
-        const unsigned vk = __reduce_min_sync(kFull, (lane < np && gt < k) ? u : 0xffffffffu);
-        if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)
-          const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
-          if (b0 > bound) bound = b0;
+  if (warp == kConsumerWarps) {
+    // ---- producer warp: the member's chunks of each of the team's rows, in order ----
+    if (TMA && lane == 0) {
+      int i = 0;
+      for (int n = 0; n < nrows; ++n) {
+        const int row = team + n * nteams;
+        const char* base = rowp(n, row);
+        for (int c = mlo; c < mhi; ++c, ++i) {
+          const int s = i % kStages;
+          mbar_wait(&pipe.empty[s], ((uint32_t)(i / kStages) & 1u) ^ 1u);
+          const long long off = (long long)c * kChunkBytes;
+          const uint32_t bytes = (uint32_t)min((long long)kChunkBytes, row_bytes - off);
+          mbar_expect_tx(&pipe.full[s], bytes);
+          bulk_g2s(ring + (size_t)s * kChunkBytes, base + off, bytes, &pipe.full[s]);
         }
       }
-      stamp(P, t0 && i == 0, 5);
-      // elements whose value reaches the bound are appended to the warp buffer at positions from
-      // a warp prefix sum (no shared atomics); when the buffer would overflow it is compacted to
-      // its top-k, the bound tightened and the remaining elements re-filtered
-      float bv = bound ? tk_val(bound) : -INFINITY;
-      unsigned pend = 0u;
-      if (m >= bv) {
-#pragma unroll
-        for (int n = 0; n < EPT; ++n) pend |= (x[n] >= bv ? 1u : 0u) << n;
+    }
+  } else if (warp == kMergeWarp) {
+    // ---- merge warp (team leaders): finish each of the team's rows once all members are in ----
+    if (member == 0) {
+      for (int n = 0; n < nrows; ++n) {
+        const int row = team + n * nteams;
+        const int b = n & 1;
+        const int2 fe = rowfe(n, row);
+        const float pc = n < kStageRows ? sh.rcum[n] : P.fr_cum[par][row];
+        mbar_wait_acq_cluster(&sh.ready[b], (uint32_t)(n >> 1) & 1u);
+        gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 24);
+        merge_row_team(P, layer, par, row, fe, pc, t, tb.ms[b], tb.lists[b], tb.surv);
+        gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 25);
+        if (lane < t) mbar_arrive_cluster(mapa_rank(&sh.freeb[b], lrank + lane), 1);  // buffer b is free
+        if (lane == 0) {
+          red_add_release_gpu(&P.layer_done[layer - 1], 1);  // row done (the select CTA polls)
+          gstamp(P, blockIdx.x == 0 && n == 0, 26);
+        }
+        __syncwarp();
       }
-      for (;;) {
-        const int cnt = __popc(pend);
-        int incl, total;
-        if (!__any_sync(kFull, cnt > 1)) {  // common case: at most one candidate per lane
-          const unsigned bal = __ballot_sync(kFull, cnt > 0);
-          incl = __popc(bal & (0xffffffffu >> (31 - lane)));
-          total = __popc(bal);
+    }
+  } else {
+    // ---- consumer warps ----
+    WarpTopk& W = sh.w[warp];
+    int wcnt = 0;  // entries in W.buf (warp-uniform)
+    int i = 0;
+    for (int n = 0; n < nrows; ++n) {
+      const int row = team + n * nteams;
+      const int b = n & 1;
+      if (n >= 2) mbar_wait_acq_cluster(&sh.freeb[b], (uint32_t)((n - 2) >> 1) & 1u);  // leader done with b
+      const uint32_t ms_remote = mapa_rank(tb.ms[b], lrank);
+      unsigned long long bound = 0ull;  // lower bound of the slice's k-th best key
+      for (int c = mlo; c < mhi; ++c, ++i) {
+        uint4 raw[kVecPerThread];
+        const int s = i % kStages;
+        if (TMA) {
+          mbar_wait(&pipe.full[s], ((uint32_t)(i / kStages)) & 1u);
+          gstamp(P, t0 && i < 2, 18 + 3 * i);
+          const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
+#pragma unroll
+          for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
         } else {
-          incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-          }
-          total = __shfl_sync(kFull, incl, 31);
+          load_direct<BF16>(rowp(n, row), c * CE, V, tid, raw);
         }
-        if (total == 0) break;
-        if (pend) {
-          int pos = wcnt + incl - cnt;
-          unsigned bits = pend;
-          while (bits) {
-            const int n = __ffs(bits) - 1;
-            bits &= bits - 1u;
-            if (pos < kSegBuf) {
-              const int idx = elem_index<BF16>(cbase, tid, n);
-              float v;
-              if (idx >= V) {
-                v = -INFINITY;
-              } else if (TMA) {  // the stage is still held: reload the element from shared memory
-                const char* sp = ring + (size_t)s * kChunkBytes +
-                                 ((size_t)((n / EPV) * kConsumers + tid) * EPV + (n % EPV)) * (BF16 ? 2 : 4);
-                v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(sp)) << 16)
-                         : *reinterpret_cast<const float*>(sp);
-              } else {
-                const char* rp = row_ptr(P, par, logits, ld_bytes, row, sh.rfe, row0) + (size_t)idx * (BF16 ? 2 : 4);
-                v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(rp)) << 16)
-                         : *reinterpret_cast<const float*>(rp);
-              }
-              W.buf[pos] = tk_key(v, idx);
-              pend &= ~(1u << n);
+        float x[EPT];
+        unpack<BF16>(raw, x);
+        const int cbase = c * CE;
+        if (c == cpr - 1) {  // ragged last chunk: elements past the row end -> -inf
+#pragma unroll
+          for (int e = 0; e < EPT; ++e)
+            if (elem_index<BF16>(cbase, tid, e) >= V) x[e] = -INFINITY;
+        }
+        // ---- softmax partial of this (chunk, warp): max tree, 4 independent sum chains ----
+        float vm[kVecPerThread];
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+          float a0 = fmaxf(x[j * EPV], x[j * EPV + 1]);
+          float a1 = fmaxf(x[j * EPV + 2], x[j * EPV + 3]);
+          if (EPV == 8) {
+            a0 = fmaxf(a0, fmaxf(x[j * EPV + 4 % EPV], x[j * EPV + 5 % EPV]));
+            a1 = fmaxf(a1, fmaxf(x[j * EPV + 6 % EPV], x[j * EPV + 7 % EPV]));
+          }
+          vm[j] = fmaxf(a0, a1);
+        }
+        const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
+        const float Mw = warp_max_fast(m);
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (Mw != -INFINITY) {
+          const float ML = Mw * kLog2e;
+#pragma unroll
+          for (int e = 0; e < EPT; ++e) s4[e & 3] += ex2(fmaf(x[e], kLog2e, -ML));
+        }
+        const float sacc = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+        gstamp(P, t0 && i < 2, 19 + 3 * i);
+        if (lane == 0) st_cluster_f2(ms_remote + (uint32_t)((c * kConsumerWarps + warp) * 8), make_float2(Mw, sacc));
+
+        // ---- top-k candidates of this warp-chunk ----
+        // CTA-wide bound for this chunk: every warp publishes its top-j lane maxima (j = ceil(k/8),
+        // one lane per round, so ties keep their multiplicity); these 8j values are distinct
+        // elements of the row, so their k-th largest v_k bounds the row's k-th best value from
+        // below and key(v_k, INT_MAX) bounds the slice's k-th best key.
+        {
+          const int jr = (k + kConsumerWarps - 1) / kConsumerWarps;
+          unsigned* pub = sh.pub[i & 1];
+          unsigned rem = (m == m) ? float_orderable(m) : 0u;
+          for (int r = 0; r < jr; ++r) {
+            const unsigned cur = __reduce_max_sync(kFull, rem);
+            const unsigned bal = __ballot_sync(kFull, rem == cur);
+            if (lane == __ffs(bal) - 1) rem = 0u;
+            if (lane == 0) pub[warp * jr + r] = cur;
+          }
+          consumer_sync();
+          const int np = kConsumerWarps * jr;
+          const unsigned u = lane < np ? pub[lane] : 0u;
+          int gt = 0;
+          for (int o = 0; o < np; o += 4) {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
+            gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+          }
+          const unsigned vk = __reduce_min_sync(kFull, (lane < np && gt < k) ? u : 0xffffffffu);
+          if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)
+            const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
+            if (b0 > bound) bound = b0;
+          }
+        }
+        // elements whose value reaches the bound are appended to the warp buffer at positions from
+        // a warp prefix sum (no shared atomics); when the buffer would overflow it is compacted to
+        // its top-k, the bound tightened and the remaining elements re-filtered
+        float bv = bound ? tk_val(bound) : -INFINITY;
+        unsigned pend = 0u;
+        if (m >= bv) {
+#pragma unroll
+          for (int e = 0; e < EPT; ++e) pend |= (x[e] >= bv ? 1u : 0u) << e;
+        }
+        for (;;) {
+          const int cnt = __popc(pend);
+          int incl, total;
+          if (!__any_sync(kFull, cnt > 1)) {  // common case: at most one candidate per lane
+            const unsigned bal = __ballot_sync(kFull, cnt > 0);
+            incl = __popc(bal & (0xffffffffu >> (31 - lane)));
+            total = __popc(bal);
+          } else {
+            incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int tt = __shfl_up_sync(kFull, incl, o);
+              if (lane >= o) incl += tt;
             }
-            ++pos;
+            total = __shfl_sync(kFull, incl, 31);
           }
-        }
-        if (wcnt + total <= kSegBuf) {
-          wcnt += total;
-          break;
-        }
-        __syncwarp();
-        warp_compact(W, kSegBuf, k, lane);
-        wcnt = k;
-        if (W.list[k - 1] > bound) bound = W.list[k - 1];
-        bv = tk_val(bound);
+          if (total == 0) break;
+          if (pend) {
+            int pos = wcnt + incl - cnt;
+            unsigned bits = pend;
+            while (bits) {
+              const int e = __ffs(bits) - 1;
+              bits &= bits - 1u;
+              if (pos < kSegBuf) {
+                const int idx = elem_index<BF16>(cbase, tid, e);
+                float v;
+                if (idx >= V) {
+                  v = -INFINITY;
+                } else if (TMA) {  // the stage is still held: reload the element from shared memory
+                  const char* sp = ring + (size_t)s * kChunkBytes +
+                                   ((size_t)((e / EPV) * kConsumers + tid) * EPV + (e % EPV)) * (BF16 ? 2 : 4);
+                  v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(sp)) << 16)
+                           : *reinterpret_cast<const float*>(sp);
+                } else {
+                  const char* rp = rowp(n, row) + (size_t)idx * (BF16 ? 2 : 4);
+                  v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(rp)) << 16)
+                           : *reinterpret_cast<const float*>(rp);
+                }
+                W.buf[pos] = tk_key(v, idx);
+                pend &= ~(1u << e);
+              }
+              ++pos;
+            }
+          }
+          if (wcnt + total <= kSegBuf) {
+            wcnt += total;
+            break;
+          }
+          __syncwarp();
+          warp_compact(W, kSegBuf, k, lane);
+          wcnt = k;
+          if (W.list[k - 1] > bound) bound = W.list[k - 1];
+          bv = tk_val(bound);
 #pragma unroll
-        for (int n = 0; n < EPT; ++n)
-          if (!(x[n] >= bv)) pend &= ~(1u << n);
-      }
-      __syncwarp();
-      if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
-      gstamp(P, t0 && i < 2, 20 + 3 * (int)i);
-      stamp(P, t0 && i == 0, 6);
-    }
-    // ---- segment end: warp buffers (top-k only if longer) -> CTA segment list (rank merge) ----
-    if (wcnt > k) {
-      warp_compact(W, wcnt, k, lane);
-      wcnt = k;
-    }
-    // padding keys are distinct and below every real key (value -inf, index > INT_MAX)
-    if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
-    wcnt = 0;
-    gstamp(P, t0 && q == rr.lo, 24);
-    consumer_sync();
-    gstamp(P, t0 && q == rr.lo, 28);
-    {
-      const int n = kConsumerWarps * k;  // even
-      if (tid < n) {
-        const unsigned long long key = sh.cl[tid];
-        const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
-        int r0 = 0, r1 = 0;
-#pragma unroll 4
-        for (int f = 0; f < n / 2; ++f) {
-          const ulonglong2 v = c2[f];
-          r0 += (v.x > key);
-          r1 += (v.y > key);
-        }
-        const int rank = r0 + r1;
-        if (rank < k) P.segkey[((size_t)row * cpr + c0) * k + rank] = key;
-      }
-    }
-    if (tid == 0) P.seglen[(size_t)row * cpr + c0] = nch;
-    gstamp(P, t0 && q == rr.lo, 25);
-    consumer_sync();
-    // warp 0 alone: arrival (release of the CTA's lists, acquire of the others'), and the row
-    // merge when this CTA completed the row; the other warps go on with the next segment
-    if (warp == 0) {
-      int last = 0;
-      if (lane == 0) {
-        const int old = atom_add_acq_rel_gpu(&P.row_done[row], nch);  // publish + acquire
-        last = (old + nch == cpr);
-      }
-      last = __shfl_sync(kFull, last, 0);
-      gstamp(P, t0 && q == rr.lo, 26);
-      if (last) {  // this CTA completed the row
-        if (lane == 0) {
-          probe_max(P, 3);
-          probe_min(P, 8);
-        }
-        gstamp(P, lane == 0 && row == 0, 29);
-        merge_row_warp(P, layer, par, row, mst);
-        gstamp(P, lane == 0 && row == 0, 30);
-        if (lane == 0) {
-          probe_max(P, 4);
-          const int old = atom_add_acq_rel_gpu(&P.layer_done[layer - 1], 1);
-          if (old + 1 == R) sh.last_layer = 1;
+          for (int e = 0; e < EPT; ++e)
+            if (!(x[e] >= bv)) pend &= ~(1u << e);
         }
         __syncwarp();
+        if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
+        gstamp(P, t0 && i < 2, 20 + 3 * i);
       }
+      gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 56 + warp);
+      // ---- slice end: warp buffers (top-k only if longer) -> CTA list (rank merge) -> leader ----
+      if (wcnt > k) {
+        warp_compact(W, wcnt, k, lane);
+        wcnt = k;
+      }
+      // padding keys are distinct and below every real key (value -inf, index > INT_MAX)
+      if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
+      wcnt = 0;
+      consumer_sync();
+      gstamp(P, t0 && n == 0, 31);
+      {
+        const int nl = kConsumerWarps * k;  // even
+        if (tid < nl) {
+          const unsigned long long key = sh.cl[tid];
+          const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
+          int r0 = 0, r1 = 0;
+#pragma unroll 4
+          for (int f = 0; f < nl / 2; ++f) {
+            const ulonglong2 v = c2[f];
+            r0 += (v.x > key);
+            r1 += (v.y > key);
+          }
+          const int rank = r0 + r1;
+          if (rank < k) st_cluster_u64(mapa_rank(tb.lists[b] + member * k + rank, lrank), key);
+        }
+      }
+      consumer_sync();  // the CTA's stores precede the arrive (release.cluster is cumulative)
+      if (tid == 0) mbar_arrive_cluster(mapa_rank(&sh.ready[b], lrank), kCluster / t);
+      gstamp(P, t0 && n == 0, 27);
     }
-    q += nch;
-    ++row;
-    c0 = 0;
   }
-  if (tid == 0) probe_max(P, 2);
-  consumer_sync();
-  if (sh.last_layer) {
-    if (tid == 0) {
-      P.layer_done[layer - 1] = 0;
-      probe_max(P, 5);
-    }
-    if (fuse_select) select_layer<kConsumers>(P, layer, kSelFull, ring);
-    if (tid == 0) probe_max(P, 6);
+  if (sel_cta && warp < kConsumerWarps) {
+    // ---- the layer's selection: prefetch + A3 now, then wait for the R row merges ----
+    gstamp(P, tid == 0, 28);
+    const int* done = &P.layer_done[layer - 1];
+    auto wait_rows = [&]() {
+      if (tid == 0) {
+        while (ld_acquire_gpu(done) < R) {
+        }
+        P.layer_done[layer - 1] = 0;  // no further arrivals this launch
+      }
+      consumer_sync();
+      gstamp(P, tid == 0, 30);
+    };
+    select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
+    gstamp(P, tid == 0, 29);
   }
-  if (tid == 0) probe_max(P, 7);
+  // every CTA stays until the cluster is done with its shared memory (remote stores / arrives)
+  cluster_sync_all();
   tl_end(P, layer);
 }
 
 }  // namespace
 
 size_t layer_smem_bytes(int cpr, int k) {
-  return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(ExpandShared) + merge_stage_bytes(cpr, k);
+  return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(ExpandShared) + team_buf_bytes(cpr, k);
 }
 
-int expand_occupancy() {
-  int n = 0;
-  const int sm = (int)layer_smem_bytes(kMaxCpr, kMaxK);
-  cudaFuncSetAttribute(layer_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(layer_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(layer_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(layer_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, layer_kernel<true, true>, kLayerThreads, layer_smem_bytes(16, 10));
-  return n > 0 ? n : 1;
+// grid of the layer kernel: all co-resident 8-CTA clusters (persistent)
+int expand_grid(int cpr, int k) {
+  const size_t sm = layer_smem_bytes(cpr, k);
+  const size_t smax = layer_smem_bytes(kMaxCpr, kMaxK);
+  cudaFuncSetAttribute(layer_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  cudaFuncSetAttribute(layer_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  cudaFuncSetAttribute(layer_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  cudaFuncSetAttribute(layer_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCluster * 64);
+  cfg.blockDim = dim3(kLayerThreadsT);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, layer_kernel<true, true>, &cfg) != cudaSuccess || ncl < 1) {
+    cudaGetLastError();
+    ncl = 1;
+  }
+  return ncl * kCluster;
 }
 
 void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool tma, bool fuse_select,
@@ -577,12 +605,26 @@ void launch_expand(const Params& P, int layer, const void* logits, long long ld_
   const char* base = static_cast<const char*>(logits);
   const size_t smem = layer_smem_bytes(P.cpr, P.k);
   const int f = fuse_select ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kLayerThreadsT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (P.dtype == SMART_BF16) {
-    if (tma) launch_k(layer_kernel<true, true>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
-    else launch_k(layer_kernel<true, false>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
+    if (tma) cudaLaunchKernelEx(&cfg, layer_kernel<true, true>, P, layer, base, ld_bytes, f);
+    else cudaLaunchKernelEx(&cfg, layer_kernel<true, false>, P, layer, base, ld_bytes, f);
   } else {
-    if (tma) launch_k(layer_kernel<false, true>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
-    else launch_k(layer_kernel<false, false>, dim3(grid), dim3(kLayerThreads), smem, s, P, layer, base, ld_bytes, f);
+    if (tma) cudaLaunchKernelEx(&cfg, layer_kernel<false, true>, P, layer, base, ld_bytes, f);
+    else cudaLaunchKernelEx(&cfg, layer_kernel<false, false>, P, layer, base, ld_bytes, f);
   }
 }
 

@@ -52,6 +52,7 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
   if (blockIdx.x == 0 && threadIdx.x < SMART_MAX_DEPTH) {
     DevTrace t{};
     P.trace[threadIdx.x] = t;
+    P.layer_done[threadIdx.x] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *P.fr_total[0] = P.b_loc;

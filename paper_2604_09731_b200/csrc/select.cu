@@ -13,6 +13,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int
   const int par = (layer - 1) & 1;
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) P.layer_done[layer - 1] = 0;  // row arrivals of the layer kernel (unused here)
   if (mode == kSelFull && *P.fr_total[par] == 0) {
     // no frontier: the step has terminated; publish an empty next frontier
     if (threadIdx.x == 0) *P.fr_total[layer & 1] = 0;

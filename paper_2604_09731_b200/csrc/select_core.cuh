@@ -281,8 +281,14 @@ __device__ __forceinline__ double warp_det_sum(const double* a, int n, int lane)
 // bookkeeping and the A5 scan (lane-contiguous chunks, so the fp64 prefix is a function of the
 // list length only); 7 block barriers in total.
 // ---------------------------------------------------------------------------------------------
-template <int NT>
-__device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
+struct NoWait {
+  __device__ void operator()() const {}
+};
+
+// `wait_rows` runs after the prefetch phase (per-request state, cost window, A3) and before the
+// layer's candidates are read: the fused layer kernel's select CTA waits there for the row merges.
+template <int NT, class Wait = NoWait>
+__device__ void select_layer(const Params& P, int layer, int mode, char* smem, Wait wait_rows = Wait()) {
   __shared__ SelScratch ss;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (layer - 1) & 1, npar = layer & 1;
@@ -325,18 +331,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       L.E[i] = reinterpret_cast<const double*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8)[r];
     }
   }
-  if (tid == 0) L.pre[nct] = 0;
-  for (int q = tid; q < nct; q += NT) {
-    L.crow[q] = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
-    const Cand c = P.cand[lbase + q];
-    L.cd[q] = c;
-    L.cum[q] = c.cum;
-    L.pre[q] = 0;
-  }
   blk_sync<NT>();  // B1
-  stamp(P, tid == 0, 10);
-
-  // ---- A3 (warp 0): e_r = min(B - n_r, W, |U_r|), eligible bases ∥ benefits (all) ----
+  // ---- A3 (warp 0): e_r = min(B - n_r, W, |U_r|), eligible bases (independent of this layer's
+  // candidates: runs before the wait) ----
   if (warp == 0) {
     long long nl = 0;
     for (int r = lane; r < bl; r += 32) {
@@ -355,6 +352,29 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       ss.bcast_l[1] = nl;
     }
   }
+  if (warp == 1) {
+    const double E0p = warp_det_sum(L.E, b_all, lane);  // global request order (Q13)
+    if (lane == 0) ss.bcast_d[2] = E0p;
+  }
+  // ---- the layer's candidates (after the row merges) ----
+  wait_rows();
+  if (tid == 0) L.pre[nct] = 0;
+  for (int q = tid; q < nct; q += NT) {
+    L.crow[q] = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
+    const int4 cr = __ldcg(reinterpret_cast<const int4*>(&P.cand[lbase + q]));
+    Cand c;
+    c.tok = cr.x;
+    c.p = __int_as_float(cr.y);
+    c.cum = __int_as_float(cr.z);
+    c.parent = cr.w;
+    L.cd[q] = c;
+    L.cum[q] = c.cum;
+    L.pre[q] = 0;
+    L.nix[q] = 0;
+  }
+  blk_sync<NT>();  // B1b
+  stamp(P, tid == 0, 10);
+  // benefits b = cum / D_r (Eq.(13))
   for (int q = tid; q < nct; q += NT) {
     const float D = L.D[L.crow[q]];
     L.cb[q] = (D == 1.f) ? L.cum[q] : __fdiv_rn(L.cum[q], D);
@@ -457,7 +477,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       ne = (int)eloc;
       R_all = (int)rloc;
     }
-    const double E0 = warp_det_sum(L.E, b_all, lane);  // global request order (Q13)
+    const double E0 = ss.bcast_d[2];  // precomputed before the wait
     const double Sb0 = sp(E0, 0);
     const double dc0 = L.dtab[0];
     const double ac = P.alpha * P.c_T;
@@ -549,11 +569,24 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
       int a = 0;
       double esum = 0.0;
-      for (int q = s0; q < s1; ++q)
-        if (L.pre[q]) {
+      int q = s0;
+      auto one = [&](int qq) {
+        if (L.pre[qq]) {
           ++a;
-          esum += (double)L.cum[q];  // canonical order (c asc)
+          esum += (double)L.cum[qq];  // canonical order (c asc)
         }
+      };
+      for (; q < s1 && (reinterpret_cast<uintptr_t>(L.pre + q) & 15); ++q) one(q);
+      for (; q + 4 <= s1; q += 4) {  // four flags per shared load; most are zero
+        const int4 f = *reinterpret_cast<const int4*>(L.pre + q);
+        if (f.x | f.y | f.z | f.w) {
+          one(q);
+          one(q + 1);
+          one(q + 2);
+          one(q + 3);
+        }
+      }
+      for (; q < s1; ++q) one(q);
       L.adm[r] = a;
       const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
       L.nxt[r] = fin ? 0 : a;
@@ -580,7 +613,13 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem) {
       const int r = L.crow[q];
       const int s0 = L.off[r] * k;
       int idx = 0;
-      for (int j = s0; j < q; ++j) idx += L.pre[j];
+      int j = s0;
+      for (; j < q && (reinterpret_cast<uintptr_t>(L.pre + j) & 15); ++j) idx += L.pre[j];
+      for (; j + 4 <= q; j += 4) {
+        const int4 f = *reinterpret_cast<const int4*>(L.pre + j);
+        idx += f.x + f.y + f.z + f.w;
+      }
+      for (; j < q; ++j) idx += L.pre[j];
       L.nix[q] = idx;
       const Cand cd = L.cd[q];
       const int node = L.nd[r] + 1 + idx;

@@ -144,6 +144,16 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   return old;
 }
 
+// fire-and-forget arrival with release semantics, and the matching acquire poll
+__device__ __forceinline__ void red_add_release_gpu(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // 64-bit top-k key: larger key = better (value desc, then index asc) — one compare per step
 __device__ __forceinline__ unsigned long long tk_key(float v, int i);
 __device__ __forceinline__ float tk_val(unsigned long long key);
@@ -277,7 +287,7 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
 void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool tma,
                    bool fuse_select, int grid, cudaStream_t s);
 size_t layer_smem_bytes(int cpr, int k);
-int expand_occupancy();
+int expand_grid(int cpr, int k);
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
 size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks);
 cudaError_t select_set_smem(size_t bytes);
