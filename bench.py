@@ -37,6 +37,9 @@ WORKLOADS = {
                             desc="Llama-3.1-8B-shaped: vocab 128256, batch 1, depth 6, top-10, EAGLE-style tree"),
     "cfg4_qwen2vl_b12": dict(V=152064, b=12, d=8, k=10, W=10, B_verify=200, fixture="qwen2vl7b_b12",
                              desc="Qwen2-VL-7B-shaped MSD-style: vocab 152064, batch 12, depth 8, top-10"),
+    "cfg5_r1distill_b256": dict(V=152064, b=256, d=6, k=8, W=8, B_verify=2048, fixture="r1distill_b256",
+                                desc="DeepSeek-R1-Distill-shaped: vocab 152064, batch 256, depth 6, top-8, "
+                                     "B_verify 2048 (B = 8), HBM-bound regime"),
 }
 SYNTH = dict(sigma_bg=2.0, a_lo=12.0, a_hi=18.0, sigma_m=2.0)  # DESIGN.md §5 input recipe
 ALPHA = 0.8

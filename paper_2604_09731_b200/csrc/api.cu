@@ -342,6 +342,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   }
   P.min_units = getenv("SMART_MIN_UNITS") ? atoi(getenv("SMART_MIN_UNITS")) : 2;
   if (P.min_units < 1) P.min_units = 1;
+  P.debug_mode = getenv("SMART_DEBUG_MODE") ? atoi(getenv("SMART_DEBUG_MODE")) : 0;
   if (getenv("SMART_TIMING")) {
     e = cudaMalloc(&P.dbg, 1024 * sizeof(unsigned long long));
     if (e != cudaSuccess) P.dbg = nullptr;
@@ -354,7 +355,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   long long elig_cap = b * std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, T - 1)));
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
   P.sort_cap = sort_cap;
-  c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1);
+  c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1, (int)k);
   c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && c->grid_expand >= 16 && !getenv("SMART_NO_FUSE");
   if (c->select_smem > 220 * 1024) {
     cudaFree(c->ws);
@@ -362,6 +363,9 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     delete c;
     return fail(nullptr, SMART_ECAPACITY, "selection needs more than 220 KiB of shared memory");
   }
+  if (getenv("SMART_VERBOSE"))
+    fprintf(stderr, "[smart] grid_expand %d (layer smem %zu B) grid_verify %d select_smem %zu B fused %d\n",
+            c->grid_expand, layer_smem_bytes(P.cpr, P.k), c->grid_verify, c->select_smem, (int)c->fused_select);
   mask_set_smem();
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {
@@ -420,7 +424,7 @@ static smart_status setup_exchange(smart_ctx* c, int rank, int nranks, void* sen
   CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
   const int sort_cap = next_pow2((long long)P.m_cap * nranks);
   P.sort_cap = sort_cap;
-  const size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks);
+  const size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks, P.k);
   if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
   c->select_smem = std::max(c->select_smem, need);
   c->fused_select = false;

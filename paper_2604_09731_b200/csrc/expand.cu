@@ -101,11 +101,12 @@ constexpr int kCluster = 8;                          // CTAs per cluster (portab
 constexpr int kMergeWarp = kConsumerWarps + 1;       // warp 9: row merges in team leaders
 constexpr int kLayerThreadsT = kLayerThreads + 32;   // 320 threads: consumers, producer, merger
 
-struct ExpandShared {
+struct __align__(16) ExpandShared {
+  unsigned long long tau;                         // slice-wide bound hint (best warp k-th key)
   int2 rfe[kStageRows];                           // frontier entries of the team's rows
   float rcum[kStageRows];                         // their path scores (cum of the parent node)
-  unsigned pub[2][kConsumerWarps * 4];            // per chunk: top-j lane maxima of each warp
-  unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k (distinct sentinels)
+  __align__(16) unsigned pub[2][kConsumerWarps * 4];            // slice start: top-j lane maxima per warp
+  __align__(16) unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k
   uint64_t ready[2];  // leader: all members' partials of the team's n-th row are in (parity n & 1)
   uint64_t freeb[2];  // every CTA: the leader has consumed buffer parity p (remote arrive)
   WarpTopk w[kConsumerWarps];
@@ -161,10 +162,10 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
       "{\n"
       ".reg .pred p;\n"
       "WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAITC_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)  // suspend-time hint: sleep instead of re-polling (each poll invalidates L1)
       : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
@@ -279,9 +280,11 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     mbar_init(&sh.freeb[0], 1);
     mbar_init(&sh.freeb[1], 1);
     mbar_fence_init();
+    sh.tau = 0ull;
   }
   cluster_sync_all();  // barriers initialised cluster-wide before any remote arrive
   tl_start(P, 32 + layer);
+  if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA start (debug)
   pdl_wait();
   pdl_trigger();
   tl_start(P, layer);
@@ -383,6 +386,11 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         } else {
           load_direct<BF16>(rowp(n, row), c * CE, V, tid, raw);
         }
+        if (P.debug_mode == 1) {  // timing experiment: stream only
+          __syncwarp();
+          if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);
+          continue;
+        }
         float x[EPT];
         unpack<BF16>(raw, x);
         const int cbase = c * CE;
@@ -405,22 +413,28 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         }
         const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
         const float Mw = warp_max_fast(m);
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        // exp2(x*log2e - M*log2e) on element pairs: FFMA2 + 2 MUFU + FADD2 (two pair accumulators)
+        unsigned long long acc2[2] = {0ull, 0ull};
         if (Mw != -INFINITY) {
           const float ML = Mw * kLog2e;
+          const unsigned long long l2e2 = f2pk(kLog2e, kLog2e), nml2 = f2pk(-ML, -ML);
 #pragma unroll
-          for (int e = 0; e < EPT; ++e) s4[e & 3] += ex2(fmaf(x[e], kLog2e, -ML));
+          for (int e = 0; e < EPT; e += 2) {
+            const unsigned long long y = ffma2(f2pk(x[e], x[e + 1]), l2e2, nml2);
+            acc2[(e >> 1) & 1] = fadd2(acc2[(e >> 1) & 1], f2pk(ex2(f2lo(y)), ex2(f2hi(y))));
+          }
         }
-        const float sacc = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+        const float sacc = warp_sum((f2lo(acc2[0]) + f2hi(acc2[0])) + (f2lo(acc2[1]) + f2hi(acc2[1])));
         gstamp(P, t0 && i < 2, 19 + 3 * i);
         if (lane == 0) st_cluster_f2(ms_remote + (uint32_t)((c * kConsumerWarps + warp) * 8), make_float2(Mw, sacc));
 
         // ---- top-k candidates of this warp-chunk ----
-        // CTA-wide bound for this chunk: every warp publishes its top-j lane maxima (j = ceil(k/8),
-        // one lane per round, so ties keep their multiplicity); these 8j values are distinct
-        // elements of the row, so their k-th largest v_k bounds the row's k-th best value from
-        // below and key(v_k, INT_MAX) bounds the slice's k-th best key.
-        {
+        // CTA-wide bound at the slice's first chunk: every warp publishes its top-j lane maxima
+        // (j = ceil(k/8), one lane per round, so ties keep their multiplicity); these 8j values
+        // are distinct elements of the row, so their k-th largest v_k bounds the row's k-th best
+        // value from below and key(v_k, INT_MAX) bounds the slice's k-th best key.  Later chunks
+        // run barrier-free on the warp's own bound (tightened by compaction).
+        if (c == mlo) {
           const int jr = (k + kConsumerWarps - 1) / kConsumerWarps;
           unsigned* pub = sh.pub[i & 1];
           unsigned rem = (m == m) ? float_orderable(m) : 0u;
@@ -449,11 +463,15 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         // its top-k, the bound tightened and the remaining elements re-filtered
         float bv = bound ? tk_val(bound) : -INFINITY;
         unsigned pend = 0u;
-        if (m >= bv) {
+        if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
 #pragma unroll
-          for (int e = 0; e < EPT; ++e) pend |= (x[e] >= bv ? 1u : 0u) << e;
+          for (int j = 0; j < kVecPerThread; ++j)
+            if (vm[j] >= bv) {
+#pragma unroll
+              for (int e = 0; e < EPV; ++e) pend |= (x[j * EPV + e] >= bv ? 1u : 0u) << (j * EPV + e);
+            }
         }
-        for (;;) {
+        while (__any_sync(kFull, pend != 0u)) {
           const int cnt = __popc(pend);
           int incl, total;
           if (!__any_sync(kFull, cnt > 1)) {  // common case: at most one candidate per lane
@@ -510,8 +528,39 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
           for (int e = 0; e < EPT; ++e)
             if (!(x[e] >= bv)) pend &= ~(1u << e);
         }
+        if (wcnt >= 2 * k && c + 1 < mhi) {  // keep the warp's buffer short
+          __syncwarp();
+          warp_compact(W, wcnt, k, lane);
+          wcnt = k;
+          if (W.list[k - 1] > bound) bound = W.list[k - 1];
+        }
         __syncwarp();
         if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
+        if (((c - mlo) & 3) == 3 && c + 1 < mhi) {
+          // every 4 chunks of a long slice: the CTA's k-th best so far (rank merge of the warps'
+          // lists) becomes everyone's bound, so later chunks rarely hold a candidate
+          if (wcnt > k) {
+            warp_compact(W, wcnt, k, lane);
+            wcnt = k;
+          }
+          if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
+          consumer_sync();
+          const int nl = kConsumerWarps * k;
+          if (tid < nl) {
+            const unsigned long long key = sh.cl[tid];
+            const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
+            int r0 = 0, r1 = 0;
+#pragma unroll 4
+            for (int f = 0; f < nl / 2; ++f) {
+              const ulonglong2 v = c2[f];
+              r0 += (v.x > key);
+              r1 += (v.y > key);
+            }
+            if (r0 + r1 == k - 1) sh.tau = key;  // the unique rank k-1 entry
+          }
+          consumer_sync();
+          if (sh.tau > bound) bound = sh.tau;
+        }
         gstamp(P, t0 && i < 2, 20 + 3 * i);
       }
       gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 56 + warp);
@@ -542,7 +591,10 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         }
       }
       consumer_sync();  // the CTA's stores precede the arrive (release.cluster is cumulative)
-      if (tid == 0) mbar_arrive_cluster(mapa_rank(&sh.ready[b], lrank), kCluster / t);
+      if (tid == 0) {
+        mbar_arrive_cluster(mapa_rank(&sh.ready[b], lrank), kCluster / t);
+        sh.tau = 0ull;  // next slice (other warps read it only after the next slice's first barrier)
+      }
       gstamp(P, t0 && n == 0, 27);
     }
   }
@@ -562,6 +614,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
     gstamp(P, tid == 0, 29);
   }
+  if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[640 + blockIdx.x] = gtime();  // per-CTA work end (debug)
   // every CTA stays until the cluster is done with its shared memory (remote stores / arrives)
   cluster_sync_all();
   tl_end(P, layer);

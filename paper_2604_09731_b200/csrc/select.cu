@@ -36,8 +36,8 @@ __global__ void export_frontier_kernel(Params P, int parity, int32_t* out, int32
 
 }  // namespace
 
-size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks) {
-  return sel_smem_bytes(b_loc, b_all, sort_cap, nc_cap, nranks);
+size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks, int k) {
+  return sel_smem_bytes(b_loc, b_all, sort_cap, nc_cap, nranks, k);
 }
 
 cudaError_t select_set_smem(size_t bytes) {

@@ -165,6 +165,8 @@ __device__ void bitonic_sort(unsigned long long* keys, int P2) {
 }
 
 // ---- layout of the dynamic shared memory used by select_layer --------------------------------
+// Per candidate only its benefit (4 B) is staged; records are re-read from global (L2) at commit.
+// Admitted candidates are per-request bitmaps (bit c = candidate index within the request).
 struct SelLayout {
   int* cnt;       // [b_loc] frontier rows of the layer per request
   int* off;       // [b_loc] frontier offset
@@ -172,39 +174,47 @@ struct SelLayout {
   int* base;      // [b_loc] eligible base (A3), later next-frontier offsets
   int* adm;       // [b_loc] admitted per request
   int* nxt;       // [b_loc] next-frontier count per request
-  float* D;       // [b_loc] benefit divisor |P_r| (PATH_MEAN) or 1
-  int* crow;      // [nc_cap] request of each candidate
-  float* cb;      // [nc_cap] benefit of each candidate
-  int* pre;       // [nc_cap + 1] exclusive scan of admitted flags (flags first)
-  float* cum;     // [nc_cap] path score of each candidate
-  Cand* cd;       // [nc_cap] staged candidate records
-  int* nix;       // [nc_cap] node index of each admitted candidate (index among the request's admits)
-  double* pps;    // [nc_cap] path_sum of the parent (PATH_MEAN)
   int* fin;       // [b_loc] finished flag
-  double* ctab;   // [nc_cap + 2] cost(N0 + j)
-  double* dtab;   // [nc_cap + 2] marginal cost at N0 + j
-  double* E;      // [max(b_loc, b_glob)] E_r (global order in kSelGlobal)
-  unsigned long long* keys;  // [P2]
-  unsigned long long* keys2;  // [P2] rank-sort output
+  float* D;       // [b_loc] benefit divisor |P_r| (PATH_MEAN) or 1
+  unsigned* bm;   // [b_loc * nbw] admitted bitmaps
+  int* rreq;      // [cap_rows] request of each frontier row
+  float* cb;      // [nc_cap] benefit of each candidate
+  float* cslot;   // [b_loc * wf] cum of the request's admits (index order)
+  double* pslot;  // [b_loc * wf] parent path sum of the request's admits (PATH_MEAN)
+  double* ctab;   // [sort_cap + 2] cost(N0 + j)
+  double* dtab;   // [sort_cap + 2] marginal cost at N0 + j
+  double* E;      // [b_all] E_r (global order in kSelGlobal)
+  unsigned long long* keys;   // [sort_cap]
+  unsigned long long* keys2;  // [sort_cap] rank-sort output / scratch
+  int nbw, wf;
 };
 
-// cost-table window: global eligible count <= nranks * nc_cap
-__host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks = 1) {
-  size_t bytes = (size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4;
-  bytes = (bytes + 15) & ~size_t(15);
-  bytes += (size_t)nc_cap * sizeof(Cand);
-  bytes += (size_t)nc_cap * 4;
-  bytes = (bytes + 15) & ~size_t(15);
-  bytes += (size_t)nc_cap * 8;
-  bytes += ((size_t)nc_cap * nranks + 2) * 16;
-  bytes += (size_t)b_all * 8;
-  bytes = (bytes + 15) & ~size_t(15);
+__host__ __device__ inline size_t sel_align(size_t x) { return (x + 15) & ~size_t(15); }
+
+// nc_cap = cap_rows * k = b_loc * wf * k
+__host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks = 1,
+                                                 int k = 1) {
+  const int per_req = nc_cap / (b_loc > 0 ? b_loc : 1);  // wf * k
+  const int nbw = (per_req + 31) / 32;
+  const int wf = per_req / (k > 0 ? k : 1);
+  size_t bytes = sel_align((size_t)8 * b_loc * 4);
+  bytes += sel_align((size_t)b_loc * nbw * 4);
+  bytes += sel_align((size_t)(nc_cap / (k > 0 ? k : 1)) * 4);
+  bytes += sel_align((size_t)nc_cap * 4);
+  bytes += sel_align((size_t)b_loc * wf * 4);
+  bytes += sel_align((size_t)b_loc * wf * 8);
+  bytes += sel_align(((size_t)sort_cap + 2) * 16);
+  bytes += sel_align((size_t)b_all * 8);
   bytes += (size_t)sort_cap * 16;
+  (void)nranks;
   return bytes;
 }
 
-__device__ inline SelLayout sel_layout(char* smem, int b_loc, int b_all, int nc_cap, int nranks, int sort_cap) {
+__device__ inline SelLayout sel_layout(char* smem, int b_loc, int nc_cap, int k, int sort_cap) {
   SelLayout L;
+  const int per_req = nc_cap / b_loc;
+  L.nbw = (per_req + 31) / 32;
+  L.wf = per_req / k;
   int* ip = reinterpret_cast<int*>(smem);
   L.cnt = ip;
   L.off = ip + b_loc;
@@ -212,28 +222,23 @@ __device__ inline SelLayout sel_layout(char* smem, int b_loc, int b_all, int nc_
   L.base = ip + 3 * b_loc;
   L.adm = ip + 4 * b_loc;
   L.nxt = ip + 5 * b_loc;
-  L.D = reinterpret_cast<float*>(ip + 6 * b_loc);
-  L.crow = ip + 7 * b_loc;
-  L.cb = reinterpret_cast<float*>(L.crow + nc_cap);
-  L.pre = reinterpret_cast<int*>(L.cb + nc_cap);
-  L.cum = reinterpret_cast<float*>(L.pre + nc_cap + 1);
-  L.fin = reinterpret_cast<int*>(L.cum + nc_cap);
-  size_t bytes = ((size_t)8 * b_loc * 4 + (size_t)nc_cap * 4 * 4 + 4 + 15) & ~size_t(15);
-  L.cd = reinterpret_cast<Cand*>(smem + bytes);
-  bytes += (size_t)nc_cap * sizeof(Cand);
-  L.nix = reinterpret_cast<int*>(smem + bytes);
-  bytes += (size_t)nc_cap * 4;
-  bytes = (bytes + 15) & ~size_t(15);
-  L.pps = reinterpret_cast<double*>(smem + bytes);
-  bytes += (size_t)nc_cap * 8;
-  L.ctab = reinterpret_cast<double*>(smem + bytes);
-  L.dtab = L.ctab + (size_t)nc_cap * nranks + 2;
-  bytes += ((size_t)nc_cap * nranks + 2) * 16;
-  L.E = reinterpret_cast<double*>(smem + bytes);
-  bytes += (size_t)b_all * 8;
-  bytes = (bytes + 15) & ~size_t(15);
-  L.keys = reinterpret_cast<unsigned long long*>(smem + bytes);
-  L.keys2 = L.keys + sort_cap;
+  L.fin = ip + 6 * b_loc;
+  L.D = reinterpret_cast<float*>(ip + 7 * b_loc);
+  size_t o = sel_align((size_t)8 * b_loc * 4);
+  L.bm = reinterpret_cast<unsigned*>(smem + o);
+  o += sel_align((size_t)b_loc * L.nbw * 4);
+  L.rreq = reinterpret_cast<int*>(smem + o);
+  o += sel_align((size_t)(nc_cap / k) * 4);
+  L.cb = reinterpret_cast<float*>(smem + o);
+  o += sel_align((size_t)nc_cap * 4);
+  L.cslot = reinterpret_cast<float*>(smem + o);
+  o += sel_align((size_t)b_loc * L.wf * 4);
+  L.pslot = reinterpret_cast<double*>(smem + o);
+  o += sel_align((size_t)b_loc * L.wf * 8);
+  L.ctab = reinterpret_cast<double*>(smem + o);
+  L.dtab = L.ctab + sort_cap + 2;
+  o += sel_align(((size_t)sort_cap + 2) * 16);
+  L.E = reinterpret_cast<double*>(smem + o);
   return L;
 }
 
@@ -285,8 +290,27 @@ struct NoWait {
   __device__ void operator()() const {}
 };
 
-// `wait_rows` runs after the prefetch phase (per-request state, cost window, A3) and before the
-// layer's candidates are read: the fused layer kernel's select CTA waits there for the row merges.
+__device__ __forceinline__ Cand load_cand(const Cand* p) {  // L2 (written by other CTAs)
+  const int4 v = __ldcg(reinterpret_cast<const int4*>(p));
+  Cand c;
+  c.tok = v.x;
+  c.p = __int_as_float(v.y);
+  c.cum = __int_as_float(v.z);
+  c.parent = v.w;
+  return c;
+}
+
+// ---------------------------------------------------------------------------------------------
+// select_layer: A3-A6 for `layer`.  mode kSelFull: single rank (or LOCAL cost scope);
+// kSelLocal: A3 + local sort, pack the exchange record; kSelGlobal: merge gathered records,
+// A5 on the global list, commit own requests.
+// `wait_rows` runs after the prefetch phase (per-request state, cost window, A3, E0) and before
+// the layer's candidates are read: the fused layer kernel's select CTA waits there for the rows.
+// Scales with the batch: per candidate only the benefit is staged, per-request admit bitmaps
+// replace per-candidate flags, and every per-candidate / per-request step is spread over all NT
+// threads; warp 0 runs the A5 scan (lane-contiguous chunks: the fp64 prefix is a function of
+// the list length only, so any sharding reproduces it bit for bit).
+// ---------------------------------------------------------------------------------------------
 template <int NT, class Wait = NoWait>
 __device__ void select_layer(const Params& P, int layer, int mode, char* smem, Wait wait_rows = Wait()) {
   __shared__ SelScratch ss;
@@ -299,10 +323,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   DevTrace& tr = P.trace[layer - 1];
   const int R = *P.fr_total[par];
   const int nct = R * k;  // candidates of this layer (local)
-  SelLayout L = sel_layout(smem, bl, b_all, P.cap_rows * k, P.nranks, P.sort_cap);
+  SelLayout L = sel_layout(smem, bl, P.cap_rows * k, k, P.sort_cap);
+  L.keys = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<char*>(L.E) + sel_align((size_t)b_all * 8));
+  L.keys2 = L.keys + P.sort_cap;
+  const int nbw = L.nbw, wf = L.wf;
   stamp(P, tid == 0, 9);
 
-  // ---- stage per-request state, the cost window and the candidates (one wave) ----
+  // ---- prefetch: per-request state, the cost window, gathered records (global mode) ----
   for (int r = tid; r < bl; r += NT) {
     L.cnt[r] = P.fr_cnt[par][r];
     L.off[r] = P.fr_off[par][r];
@@ -311,10 +339,11 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     L.fin[r] = P.finished[r];
     if (mode != kSelGlobal) L.E[r] = P.E_r[r];
   }
+  for (int i = tid; i < bl * nbw; i += NT) L.bm[i] = 0u;
   {
     // cost window from N0 = drafted nodes before the layer; entries [0, max eligible + 1]
     const long long n0g = *P.N_glob;
-    const int ncw = (mode == kSelGlobal ? P.nranks * P.m_cap : nct) + 2;
+    const int ncw = min(mode == kSelGlobal ? P.nranks * P.m_cap : nct, P.sort_cap) + 2;
     for (int j = tid; j < ncw; j += NT) {
       const long long N = min(n0g + j, (long long)P.n_cost - 1);
       L.ctab[j] = P.cost_tab[N];
@@ -332,8 +361,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     }
   }
   blk_sync<NT>();  // B1
-  // ---- A3 (warp 0): e_r = min(B - n_r, W, |U_r|), eligible bases (independent of this layer's
-  // candidates: runs before the wait) ----
+
+  // ---- A3 (warp 0): e_r = min(B - n_r, W, |U_r|), eligible bases; E0 (warp 1) ----
   if (warp == 0) {
     long long nl = 0;
     for (int r = lane; r < bl; r += 32) {
@@ -351,50 +380,38 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       ss.bcast_i[2] = tot;
       ss.bcast_l[1] = nl;
     }
-  }
-  if (warp == 1) {
+  } else if (warp == 1) {
     const double E0p = warp_det_sum(L.E, b_all, lane);  // global request order (Q13)
     if (lane == 0) ss.bcast_d[2] = E0p;
   }
-  // ---- the layer's candidates (after the row merges) ----
+
+  // ---- the layer's candidates (after the row merges): benefits b = cum / D_r (Eq.(13)) ----
   wait_rows();
-  if (tid == 0) L.pre[nct] = 0;
   for (int q = tid; q < nct; q += NT) {
-    L.crow[q] = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
-    const int4 cr = __ldcg(reinterpret_cast<const int4*>(&P.cand[lbase + q]));
-    Cand c;
-    c.tok = cr.x;
-    c.p = __int_as_float(cr.y);
-    c.cum = __int_as_float(cr.z);
-    c.parent = cr.w;
-    L.cd[q] = c;
-    L.cum[q] = c.cum;
-    L.pre[q] = 0;
-    L.nix[q] = 0;
-  }
-  blk_sync<NT>();  // B1b
-  stamp(P, tid == 0, 10);
-  // benefits b = cum / D_r (Eq.(13))
-  for (int q = tid; q < nct; q += NT) {
-    const float D = L.D[L.crow[q]];
-    L.cb[q] = (D == 1.f) ? L.cum[q] : __fdiv_rn(L.cum[q], D);
+    const int r = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
+    const float cum = __ldcg(&P.cand[lbase + q].cum);
+    const float D = L.D[r];
+    const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
+    L.cb[q] = b;
+    P.cand_b[lbase + q] = b;
+    if (q % k == 0) L.rreq[q / k] = r;
   }
   blk_sync<NT>();  // B2
+  stamp(P, tid == 0, 10);
   int ne = ss.bcast_i[2];
   long long N0 = ss.bcast_l[1];
   if (mode != kSelGlobal) {
-    // within-request rank by (b desc, c asc); eligible if rank < e_r
+    // within-request rank by (b desc, c asc); eligible if rank < e_r (early exit past e_r)
     for (int q = tid; q < nct; q += NT) {
-      const int r = L.crow[q];
+      const int r = L.rreq[q / k];
       const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+      const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
       const float b = L.cb[q];
-      P.cand_b[lbase + q] = b;
       int rank = 0;
-      for (int j = s0; j < s1; ++j) {
+      for (int j = s0; j < s1 && rank < e_r; ++j) {
         const float bj = L.cb[j];
         rank += (bj > b) || (bj == b && j < q);
       }
-      const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
       if (rank < e_r) L.keys[L.base[r] + rank] = sel_key(b, P.b_off + r, q - s0);
     }
     blk_sync<NT>();  // B3
@@ -408,15 +425,16 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(L.keys);
     for (int i = tid; i < nsort; i += NT) {
       const unsigned long long key = L.keys[i];
-      int rank = 0;
+      int r0 = 0, r1 = 0;
       int f = 0;
 #pragma unroll 4
       for (; f + 1 < nsort; f += 2) {
         const ulonglong2 v = k2[f >> 1];
-        rank += (v.x < key) + (v.y < key);
+        r0 += (v.x < key);
+        r1 += (v.y < key);
       }
-      if (f < nsort) rank += (L.keys[f] < key);
-      L.keys2[rank] = key;
+      if (f < nsort) r0 += (L.keys[f] < key);
+      L.keys2[r0 + r1] = key;
     }
     blk_sync<NT>();  // B4
     unsigned long long* t = L.keys;
@@ -452,7 +470,6 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const double C = L.ctab[j];
     return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
   };
-
   // ---- A5 (warp 0): Eq.(16) scan over the sorted list, cut, argmax_j S_j ----
   if (warp == 0) {
     int R_all = R;
@@ -557,127 +574,107 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   stamp(P, tid == 0, 13);
 
   // ---- A6: commit (own requests) ----
+  // (1) admit bitmaps: bit c of request r <=> candidate c (= slot * k + rank) admitted
   for (int j = tid; j < js; j += NT) {
     const unsigned long long key = L.keys[j];
     const int r = sel_key_r(key) - P.b_off;
-    if (r >= 0 && r < bl) L.pre[L.off[r] * k + sel_key_c(key)] = 1;
+    if (r >= 0 && r < bl) {
+      const int c = sel_key_c(key);
+      atomicOr(&L.bm[r * nbw + (c >> 5)], 1u << (c & 31));
+    }
   }
   blk_sync<NT>();  // B6
-  if (warp == 0) {
-    // per request (lane-strided): admitted count, finish, next-frontier count, NODE_SUM E
-    for (int r = lane; r < bl; r += 32) {
-      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
-      int a = 0;
-      double esum = 0.0;
-      int q = s0;
-      auto one = [&](int qq) {
-        if (L.pre[qq]) {
-          ++a;
-          esum += (double)L.cum[qq];  // canonical order (c asc)
-        }
-      };
-      for (; q < s1 && (reinterpret_cast<uintptr_t>(L.pre + q) & 15); ++q) one(q);
-      for (; q + 4 <= s1; q += 4) {  // four flags per shared load; most are zero
-        const int4 f = *reinterpret_cast<const int4*>(L.pre + q);
-        if (f.x | f.y | f.z | f.w) {
-          one(q);
-          one(q + 1);
-          one(q + 2);
-          one(q + 3);
-        }
-      }
-      for (; q < s1; ++q) one(q);
-      L.adm[r] = a;
-      const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
-      L.nxt[r] = fin ? 0 : a;
-      L.base[r] = fin ? 0 : a;
-      P.fr_cnt[npar][r] = fin ? 0 : a;
-      if (fin && L.cnt[r] > 0) P.finished[r] = 1;
-      P.n_nodes[r] = L.nd[r] + 1 + a;
-      if (!pmean && a > 0) {
-        const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
-        L.E[gi] += esum;  // node sum (Q11)
-        P.E_r[r] = L.E[gi];
-      }
-    }
-    __syncwarp();
-    const int total = warp_excl_scan_smem(L.base, bl, lane);
-    for (int r = lane; r < bl; r += 32) P.fr_off[npar][r] = L.base[r];
-    if (lane == 0) *P.fr_total[npar] = total;
-  } else {
-    // per candidate: admitted flag, node records in canonical order (c asc), parent path sums
-    for (int q = tid - 32; q < nct; q += NT - 32) {
-      const int f = L.pre[q];
-      P.cand_adm[lbase + q] = f;
-      if (!f) continue;
-      const int r = L.crow[q];
-      const int s0 = L.off[r] * k;
-      int idx = 0;
-      int j = s0;
-      for (; j < q && (reinterpret_cast<uintptr_t>(L.pre + j) & 15); ++j) idx += L.pre[j];
-      for (; j + 4 <= q; j += 4) {
-        const int4 f = *reinterpret_cast<const int4*>(L.pre + j);
-        idx += f.x + f.y + f.z + f.w;
-      }
-      for (; j < q; ++j) idx += L.pre[j];
-      L.nix[q] = idx;
-      const Cand cd = L.cd[q];
-      const int node = L.nd[r] + 1 + idx;
-      const size_t o = (size_t)r * P.T + node;
-      P.tok[o] = cd.tok;
-      P.parent[o] = cd.parent;
-      P.depth[o] = layer;
-      P.p[o] = cd.p;
-      P.cum[o] = cd.cum;
-      if (pmean) {
-        const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
-        L.pps[q] = pps;
-        P.path_sum[o] = pps + (double)cd.cum;
-      }
+  auto bits_below = [&](int r, int c) {  // admitted candidates of r with index < c
+    int n = 0;
+    for (int w = 0; w < (c >> 5); ++w) n += __popc(L.bm[r * nbw + w]);
+    if (c & 31) n += __popc(L.bm[r * nbw + (c >> 5)] & ((1u << (c & 31)) - 1u));
+    return n;
+  };
+  // (2) per candidate: admitted flag; admitted ones write their node (index among the request's
+  // admits in canonical order = bits below) and stage cum / parent path sum for (3)
+  for (int q = tid; q < nct; q += NT) {
+    const int r = L.rreq[q / k];
+    const int c = q - L.off[r] * k;
+    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
+    P.cand_adm[lbase + q] = f;
+    if (!f) continue;
+    const int idx = bits_below(r, c);
+    const Cand cd = load_cand(&P.cand[lbase + q]);
+    const int node = L.nd[r] + 1 + idx;
+    const size_t o = (size_t)r * P.T + node;
+    P.tok[o] = cd.tok;
+    P.parent[o] = cd.parent;
+    P.depth[o] = layer;
+    P.p[o] = cd.p;
+    P.cum[o] = cd.cum;
+    L.cslot[r * wf + idx] = cd.cum;
+    if (pmean) {
+      const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
+      L.pslot[r * wf + idx] = pps;
+      P.path_sum[o] = pps + (double)cd.cum;
     }
   }
   blk_sync<NT>();  // B7
+  // (3) per request: admitted count, finish, next-frontier count, E (canonical order)
+  for (int r = tid; r < bl; r += NT) {
+    int a = 0;
+    for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
+    L.adm[r] = a;
+    const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
+    L.nxt[r] = fin ? 0 : a;
+    L.base[r] = fin ? 0 : a;
+    P.fr_cnt[npar][r] = fin ? 0 : a;
+    if (fin && L.cnt[r] > 0) P.finished[r] = 1;
+    P.n_nodes[r] = L.nd[r] + 1 + a;
+    if (a == 0) continue;
+    const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
+    if (!pmean) {
+      double esum = 0.0;
+      for (int u = 0; u < a; ++u) esum += (double)L.cslot[r * wf + u];
+      L.E[gi] += esum;  // node sum (Q11)
+    } else {
+      // Eq.(2) path mean of the committed tree: leaves lose their admitted-into parents
+      double psum_new = 0.0, psum_par = 0.0;
+      int nparents = 0, u = 0, prev_row = -1;
+      for (int w = 0; w < nbw; ++w) {
+        unsigned bits = L.bm[r * nbw + w];
+        while (bits) {
+          const int c = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1u;
+          const double pps = L.pslot[r * wf + u];
+          psum_new += pps + (double)L.cslot[r * wf + u];
+          if (c / k != prev_row) {  // first admitted child of this frontier row
+            psum_par += pps;
+            ++nparents;
+            prev_row = c / k;
+          }
+          ++u;
+        }
+      }
+      const int lc = P.leaf_cnt[r] - nparents + a;
+      const double ls = P.leaf_sum[r] - psum_par + psum_new;
+      P.leaf_cnt[r] = lc;
+      P.leaf_sum[r] = ls;
+      L.E[gi] = ls / (double)lc;
+    }
+    P.E_r[r] = L.E[gi];
+  }
+  blk_sync<NT>();  // B8
+  const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
   stamp(P, tid == 0, 14);
-  // next frontier (own requests that continue), with the cum of each node for the row merge
+  for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
+  if (tid == 0) *P.fr_total[npar] = total;
+  // (4) next frontier (own requests that continue), with the cum of each node for the row merge
   for (int q = tid; q < nct; q += NT) {
-    if (!L.pre[q]) continue;
-    const int r = L.crow[q];
+    const int r = L.rreq[q / k];
     if (L.nxt[r] == 0) continue;
-    const int idx = L.nix[q];
+    const int c = q - L.off[r] * k;
+    if (!((L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u)) continue;
+    const int idx = bits_below(r, c);
     P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
-    P.fr_cum[npar][L.base[r] + idx] = L.cum[q];
+    P.fr_cum[npar][L.base[r] + idx] = L.cslot[r * wf + idx];
   }
   if (warp == 0) {
-    if (pmean) {
-      // Eq.(2) path mean of the committed tree: leaves lose their admitted-into parents
-      for (int r = lane; r < bl; r += 32) {
-        if (L.adm[r] == 0) continue;
-        const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
-        double psum_new = 0.0, psum_par = 0.0;
-        int nparents = 0;
-        for (int q0 = s0; q0 < s1; q0 += k) {
-          bool any = false;
-          for (int q = q0; q < q0 + k; ++q) {
-            if (!L.pre[q]) continue;
-            const double pps = L.pps[q];
-            psum_new += pps + (double)L.cum[q];
-            if (!any) {
-              psum_par += pps;
-              ++nparents;
-            }
-            any = true;
-          }
-        }
-        const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
-        const int lc = P.leaf_cnt[r] - nparents + L.adm[r];
-        const double ls = P.leaf_sum[r] - psum_par + psum_new;
-        P.leaf_cnt[r] = lc;
-        P.leaf_sum[r] = ls;
-        L.E[gi] = ls / (double)lc;
-        P.E_r[r] = L.E[gi];
-      }
-      __syncwarp();
-    }
     // ---- totals after the layer (trace S_after) ----
     const double E0 = ss.bcast_d[2];
     const long long N0w = ss.bcast_l[0];

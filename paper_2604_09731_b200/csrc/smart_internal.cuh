@@ -100,6 +100,7 @@ struct Params {
 
   // ---- optional timing probes (SMART_TIMING=1): globaltimer ns, see probe() ----
   unsigned long long* dbg;
+  int debug_mode;     // SMART_DEBUG_MODE (timing experiments only; 0 in production)
 
   // ---- select / stats ----
   DevTrace* trace;    // [SMART_MAX_DEPTH]
@@ -158,6 +159,23 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ unsigned long long tk_key(float v, int i);
 __device__ __forceinline__ float tk_val(unsigned long long key);
 __device__ __forceinline__ int tk_idx(unsigned long long key);
+
+// packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): two lanes of work per instruction
+__device__ __forceinline__ unsigned long long f2pk(float a, float b) {
+  return ((unsigned long long)__float_as_uint(b) << 32) | __float_as_uint(a);
+}
+__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -289,7 +307,7 @@ void launch_expand(const Params& P, int layer, const void* logits, long long ld_
 size_t layer_smem_bytes(int cpr, int k);
 int expand_grid(int cpr, int k);
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
-size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks);
+size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks, int k);
 cudaError_t select_set_smem(size_t bytes);
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok,
                  int32_t* tree_len, cudaStream_t s);

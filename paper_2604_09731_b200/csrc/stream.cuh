@@ -13,7 +13,7 @@
 
 namespace smart {
 
-constexpr int kStages = 6;
+constexpr int kStages = 5;
 constexpr int kMinUnits = 4;   // chunks per CTA at least (64 KiB, all in flight)
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;      // 256 consumer threads
@@ -42,10 +42,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)  // suspend-time hint (ns): sleep in hardware instead of re-polling
       : "memory");
 }
 // 1-D bulk copy global -> shared (TMA engine; SASS UBLKCP), completes tx bytes on `bar`

@@ -131,6 +131,23 @@ def test_full_size_configs(name):
     _run(FULL[name])
 
 
+# cfg5-sized batches: b = 256 (standalone 1024-thread select, bitonic global sort over up to
+# 2048 eligible keys) and b = 64 with the PATH_MEAN model (fused select); a cost model cheap
+# enough per node that trees still grow at these batch sizes
+LARGE_B = {
+    "b256_node_sum": Case(V=20000, k=8, d=4, W=8, b=256, B_verify=2048, seed=41,
+                          cost=(0.0005, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0)),
+    "b64_path_mean": Case(V=30000, k=6, d=5, W=6, b=64, B_verify=512, seed=42, accept_model=1, omega=0,
+                          selection=1, cost=(0.0005, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0)),
+}
+
+
+@pytest.mark.parametrize("name", list(LARGE_B))
+def test_large_batch(name):
+    orc, gpu, layers = _run(LARGE_B[name])
+    assert orc.N > 2 * LARGE_B[name].b and layers >= 2  # non-trivial trees were compared
+
+
 def test_full_size_fp32_logits():
     c = FULL["cfg3_llama8b_b32"]
     _run(Case(**{**c.__dict__, "dtype": "fp32", "b": 8, "seed": 21}))

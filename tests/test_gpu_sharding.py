@@ -95,7 +95,11 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=["b8", "cfg3", "frozen_b4"])
+CASES.append(Case(V=20000, k=8, d=4, W=8, b=256, B_verify=2048, seed=34,
+                  cost=(0.0005, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0)))  # cfg5-sized batch (bitonic global sort)
+
+
+@pytest.mark.parametrize("case", CASES, ids=["b8", "cfg3", "frozen_b4", "b256"])
 @pytest.mark.parametrize("G", [2, 4])
 def test_sharded_equals_single(case, G):
     if case.b % G:
