@@ -75,6 +75,13 @@ def lib():
         L.orc_step.argtypes = ([C.POINTER(_Cfg), pc, vp, i64, i64, vp, i64, vp, vp]
                                + [vp] * 8 + [vp] * 3 + [vp, i64, vp, vp, vp])
         L.orc_step.restype = C.c_int
+        L.orc_verify_sample.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp,
+                                        d, C.c_uint64, vp, vp, vp, vp]
+        L.orc_verify_sample.restype = C.c_int
+        L.orc_hash.argtypes = [C.c_uint64, i64, i64, i64]
+        L.orc_hash.restype = C.c_uint64
+        L.orc_uniform.argtypes = [C.c_uint64, i64, i64, i64]
+        L.orc_uniform.restype = d
         _lib = L
     return _lib
 
@@ -296,3 +303,36 @@ def step(cfg: Config, cost: Cost, draft: np.ndarray, target: np.ndarray | None =
         bonus=out["bonus"], trace=out["trace"].reshape(D, TRACE_F),
         cand_i=cand_i.reshape(D, capc, 5) if dump else None,
         cand_d=cand_d.reshape(D, capc, 3) if dump else None, summary=out["summary"], T=T)
+
+
+def uniform(seed: int, r: int, u: int, v: int) -> float:
+    """The counter-based uniform of the T > 0 verification (orc_uniform)."""
+    return lib().orc_uniform(seed, r, u, v)
+
+
+def verify_sample(target: np.ndarray, n_nodes, parent, tok, tau: float, seed: int, d: int,
+                  r_off: int = 0, V: int | None = None):
+    """NEXT #1 (Q31): tree verification at temperature tau > 0 over an existing tree.
+
+    target: [b, T, ld] uint16 (bf16 bits) or float32; n_nodes [b]; parent/tok [b, T].
+    Returns (accept_len [b], accept_path [b, max(d,1)], bonus [b], margin [b])."""
+    target = np.ascontiguousarray(target)
+    dtype = BF16 if target.dtype == np.uint16 else FP32
+    b, T, ld = target.shape
+    D = max(d, 1)
+    V = ld if V is None else V
+    out_a = np.zeros(b, np.int32)
+    out_p = np.full(b * D, -1, np.int32)
+    out_b = np.zeros(b, np.int32)
+    mg = np.zeros(b)
+    nn = np.ascontiguousarray(n_nodes, np.int32)
+    pa = np.ascontiguousarray(parent, np.int32)
+    tk = np.ascontiguousarray(tok, np.int32)
+    rc = lib().orc_verify_sample(dtype, V, T, b, r_off, d, _ptr(target), ld, _ptr(nn), _ptr(pa), _ptr(tk),
+                                 float(tau), int(seed) & ((1 << 64) - 1), _ptr(out_a), _ptr(out_p),
+                                 _ptr(out_b), _ptr(mg))
+    if rc == 1:
+        raise ValueError("invalid arguments")
+    if rc == 2:
+        raise ValueError("invalid logits (NaN)")
+    return out_a, out_p.reshape(b, D), out_b, mg

@@ -517,3 +517,73 @@ done:
   free(topi); free(topp); free(cand); free(ord); free(elig); free(kid);
   return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT #1: tree verification at temperature tau > 0 (Q31)                   */
+/* ------------------------------------------------------------------------ */
+
+static uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ULL;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  return z;
+}
+
+/* SplitMix64 output for the state seed + key * golden-gamma (one finaliser) */
+uint64_t orc_hash(uint64_t seed, int64_t r, int64_t u, int64_t v) {
+  const uint64_t key = ((uint64_t)r << 42) | ((uint64_t)u << 20) | (uint64_t)v;
+  return mix64(seed + key * 0x9e3779b97f4a7c15ULL);
+}
+
+/* 23-bit uniform in (0, 1): (h >> 41) + 1/2 over 2^23 (exact in fp32 as well) */
+double orc_uniform(uint64_t seed, int64_t r, int64_t u, int64_t v) {
+  return ((double)(orc_hash(seed, r, u, v) >> 41) + 0.5) / 8388608.0;
+}
+
+int orc_verify_sample(int dtype, int V, int T, int b, int r_off, int d, const void* target, int64_t ld_t,
+                      const int32_t* n_nodes, const int32_t* parent, const int32_t* tok, double tau,
+                      uint64_t seed, int32_t* accept_len, int32_t* accept_path, int32_t* bonus,
+                      double* margin) {
+  if (!(tau > 0.0) || V < 1 || T < 1 || b < 0 || d < 0 || !target) return 1;
+  const int esz = dtype == ORC_BF16 ? 2 : 4;
+  const int D = d > 0 ? d : 1;
+  for (int r = 0; r < b; r++) {
+    const int64_t rg = (int64_t)r_off + r;
+    accept_len[r] = 0;
+    for (int i = 0; i < D; i++) accept_path[r * D + i] = -1;
+    bonus[r] = -1;
+    double mg = INFINITY;
+    int32_t cur = 0;
+    for (;;) {
+      /* one sample from softmax(logits/tau) at node cur: Gumbel-max */
+      const char* row = (const char*)target + ((int64_t)r * T + cur) * ld_t * esz;
+      int64_t best = -1;
+      double by = 0.0, second = -INFINITY;
+      for (int64_t v = 0; v < V; v++) {
+        const double x = logit_at(row, dtype, v);
+        if (isnan(x)) return 2;
+        const double U = orc_uniform(seed, rg, cur, v);
+        const double y = x / tau - log(-log(U));
+        if (best < 0 || y > by) {  /* ties keep the lower token id */
+          if (best >= 0) second = by;
+          best = v;
+          by = y;
+        } else if (y > second) {
+          second = y;
+        }
+      }
+      if (by - second < mg) mg = by - second;
+      int32_t next = -1;
+      for (int32_t j = cur + 1; j < n_nodes[r]; j++)
+        if (parent[r * T + j] == cur && tok[r * T + j] == best) { next = j; break; }
+      if (next < 0) { bonus[r] = (int32_t)best; break; }
+      if (accept_len[r] < D) accept_path[r * D + accept_len[r]] = next;
+      accept_len[r]++;
+      cur = next;
+    }
+    if (margin) margin[r] = mg;
+  }
+  return 0;
+}
