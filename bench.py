@@ -348,6 +348,18 @@ def main():
         kt["select"].append(d_[2:2 + 2 * wl["d"]:2])
         kt["mask"].append(d_[-2])
         kt["verify"].append(d_[-1])
+    # A8 at temperature 1 (NEXT #1) on the same tree, for the breakdown (not part of the step)
+    ver_t1 = []
+    for rep in range(reps):
+        o = p["out"]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            ctx.verify_sample(p["target"], 1.0, 1000 + rep, o["accept_len"], o["accept_path"], o["bonus"],
+                              stream=stream)
+            e1.record(stream)
+        stream.synchronize()
+        ver_t1.append(e0.elapsed_time(e1))
     if reps == 0:
         kt = {"expand": [[0.0] * wl["d"]], "select": [[0.0] * wl["d"]], "mask": [0.0], "verify": [1e-9], "begin": [0.0]}
     st0 = tree_stats[0]
@@ -458,7 +470,9 @@ def main():
             "cpu_baseline": cpu,
             "step_breakdown_ms": {"begin": beg_ms, "expand_per_layer": [float(x) for x in exp_ms],
                                   "select_per_layer": [float(x) for x in sel_ms], "mask": mask_ms,
-                                  "verify": ver_ms, "note": "eager launches, event-bracketed (not the graph)"},
+                                  "verify": ver_ms,
+                                  "verify_sample_T1": float(np.mean(ver_t1)) if ver_t1 else None,
+                                  "note": "eager launches, event-bracketed (not the graph)"},
             "kernels": {"expand": k_expand, "verify": k_verify},
             "step_algorithmic_bytes": step_alg_bytes,
             "step_hbm_gbs": step_alg_bytes / (ms_per_step / 1e3) / 1e9,

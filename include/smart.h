@@ -17,6 +17,7 @@
  *                      A6  commit A_l, S_l = S_{l-1} ∪ A_l, next frontier   (Eq.(7))
  *   smart_build_mask   A7  ancestor mask, position ids, parent indices, tokens
  *   smart_verify_accept A8 greedy (T=0) longest-accepted-path walk on target logits
+ *   smart_verify_sample    A8 at temperature T > 0 (NEXT #1; P:453 reports T in {0, 1})
  *
  * Readings of the paper where it is silent or ambiguous are listed in DESIGN.md §3 (Q1..);
  * they are shared with the fp64 oracle in oracle/ (which this library never links).
@@ -188,6 +189,20 @@ smart_status smart_build_mask(smart_ctx* ctx, uint32_t* d_mask, int32_t* d_pos, 
 smart_status smart_verify_accept(smart_ctx* ctx, const void* d_target, int64_t ld,
                                  int32_t* d_accept_len, int32_t* d_accept_path, int32_t* d_bonus,
                                  void* stream);
+
+/* A8 at temperature `temperature` > 0 (reading Q31): at every
+ * visited node one target token is drawn from softmax(logits / temperature) by Gumbel-max,
+ *   argmax_v  logit_v / temperature - ln(-ln U_v),
+ *   U_v = ((h >> 9) + 1/2) / 2^23,  h = lowbias32(rk + v * 0x9e3779b9) (mod 2^32),
+ *   rk = high half of SplitMix64(seed + ((batch_offset + r) << 22 | node) * 0x9e3779b97f4a7c15),
+ * and the walk follows the child holding that token, else stops with it as the bonus -- the
+ * sequential point-mass rejection scheme (accept child t with probability p(t) / remaining
+ * mass), lossless for deterministic top-k children.  Same layouts and preconditions as
+ * smart_verify_accept; `seed` selects the random stream (vary it per decode step).
+ * SMART_EINVAL if temperature is not > 0. */
+smart_status smart_verify_sample(smart_ctx* ctx, const void* d_target, int64_t ld, double temperature,
+                                 uint64_t seed, int32_t* d_accept_len, int32_t* d_accept_path,
+                                 int32_t* d_bonus, void* stream);
 
 /* Convenience: begin + d x (expand, select) + mask + verify for ROWS_NODE pools, enqueued on
  * one stream (graph-capturable).  Same semantics as the individual calls. */

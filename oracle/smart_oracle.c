@@ -531,15 +531,25 @@ static uint64_t mix64(uint64_t z) {
   return z;
 }
 
-/* SplitMix64 output for the state seed + key * golden-gamma (one finaliser) */
-uint64_t orc_hash(uint64_t seed, int64_t r, int64_t u, int64_t v) {
-  const uint64_t key = ((uint64_t)r << 42) | ((uint64_t)u << 20) | (uint64_t)v;
-  return mix64(seed + key * 0x9e3779b97f4a7c15ULL);
+/* counter-based generator: a per-(request, node) 32-bit row key from SplitMix64, then per token
+ * v the lowbias32 integer hash of rowkey + v * 0x9e3779b9 (all arithmetic mod 2^32 / 2^64) */
+static uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
 }
 
-/* 23-bit uniform in (0, 1): (h >> 41) + 1/2 over 2^23 (exact in fp32 as well) */
+uint64_t orc_hash(uint64_t seed, int64_t r, int64_t u, int64_t v) {
+  const uint64_t rk = mix64(seed + (((uint64_t)r << 22) | (uint64_t)u) * 0x9e3779b97f4a7c15ULL);
+  return lowbias32((uint32_t)(rk >> 32) + (uint32_t)v * 0x9e3779b9U);
+}
+
+/* 23-bit uniform in (0, 1): (h >> 9) + 1/2 over 2^23 (exact in fp32 as well) */
 double orc_uniform(uint64_t seed, int64_t r, int64_t u, int64_t v) {
-  return ((double)(orc_hash(seed, r, u, v) >> 41) + 0.5) / 8388608.0;
+  return ((double)(orc_hash(seed, r, u, v) >> 9) + 0.5) / 8388608.0;
 }
 
 int orc_verify_sample(int dtype, int V, int T, int b, int r_off, int d, const void* target, int64_t ld_t,

@@ -93,7 +93,7 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
 /* NEXT #1 (reading Q31): tree verification at temperature tau > 0.  Walk from the root of each
  * request: at node u draw the target token by Gumbel-max over the target row,
  *   x* = argmax_v ( logit_v / tau + G_v ),  G_v = -log(-log(U_v)),
- *   U_v = ((h >> 41) + 0.5) / 2^23,  h = orc_hash(seed, r_glob, u, v),
+ *   U_v = ((h >> 9) + 0.5) / 2^23,  h = orc_hash(seed, r_glob, u, v),
  * follow the child of u whose token is x*, else stop with bonus = x*.  This realises the
  * sequential point-mass rejection scheme (accept child t with probability p(t) / remaining mass,
  * zero t on rejection, bonus from the renormalised residual) with one sample
@@ -105,8 +105,9 @@ int orc_verify_sample(int dtype, int V, int T, int b, int r_off, int d, const vo
                       const int32_t* n_nodes, const int32_t* parent, const int32_t* tok, double tau,
                       uint64_t seed, int32_t* accept_len, int32_t* accept_path, int32_t* bonus,
                       double* margin);
-/* the counter-based generator: SplitMix64 output for the state seed + key * 0x9e3779b97f4a7c15,
- * key = r << 42 | u << 20 | v (r < 2^22, u < 2^22, v < 2^20), and the 23-bit uniform in (0, 1) */
+/* the counter-based generator: row key rk = SplitMix64(seed + (r << 22 | u) * 0x9e3779b97f4a7c15)
+ * (r < 2^42, u < 2^22), h = lowbias32((rk >> 32) + v * 0x9e3779b9) (32-bit), and the 23-bit
+ * uniform in (0, 1) it defines */
 uint64_t orc_hash(uint64_t seed, int64_t r, int64_t u, int64_t v);
 double orc_uniform(uint64_t seed, int64_t r, int64_t u, int64_t v);
 

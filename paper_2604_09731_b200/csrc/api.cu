@@ -602,6 +602,24 @@ smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld,
   return SMART_OK;
 }
 
+smart_status smart_verify_sample(smart_ctx* c, const void* d_target, int64_t ld, double temperature, uint64_t seed,
+                                 int32_t* d_accept_len, int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (!d_target) return fail(c, SMART_EINVAL, "null target logits");
+  if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld < vocab");
+  if (!(temperature > 0.0) || !(1.0 / temperature < 3.0e38)) return fail(c, SMART_EINVAL, "temperature must be > 0");
+  if (!c->masked) return fail(c, SMART_ESTATE, "verify_sample must follow build_mask");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long ld_bytes = (long long)ld * c->P.esz;
+  const bool tma = ((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ld_bytes % 16 == 0) &&
+                   (((long long)c->P.V * c->P.esz) % 16 == 0);
+  launch_verify(c->P, d_target, ld_bytes, tma, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s, true,
+                (float)(1.0 / temperature), (unsigned long long)seed);
+  CUDA_TRY(c, cudaGetLastError());
+  c->last_stream = s;
+  return SMART_OK;
+}
+
 smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32_t* d_root_pos, const void* d_draft,
                             int64_t ld, const void* d_target, int64_t ld_t, uint32_t* d_mask, int32_t* d_pos,
                             int32_t* d_parent, int32_t* d_tok, int32_t* d_tree_len, int32_t* d_accept_len,

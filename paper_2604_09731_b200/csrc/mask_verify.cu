@@ -163,10 +163,38 @@ struct VerifyShared {
 // K4: persistent TMA-staged stream over all tree rows (request r, node i < tree_len[r]) of the
 // target logits; exact argmax per row (value desc, index asc); the request whose last row
 // completes runs the greedy walk.
-template <bool BF16, bool TMA>
+// NEXT #1 (Q31): perturbed logit of token v at a verify row: x / tau + Gumbel(U_v), with
+// U_v = ((h >> 9) + 1/2) / 2^23, h = lowbias32(rowkey + v * 0x9e3779b9) and rowkey the high
+// half of SplitMix64(seed + (global request << 22 | node) * golden-gamma), computed once per
+// row.  U is exact in fp32; G is evaluated in fp32 (the oracle in fp64), decisions closer than
+// 1e-4 are tie-ambiguous (Q24).
+__device__ __forceinline__ uint32_t sample_rowkey(unsigned long long seed, unsigned long long r, unsigned long long node) {
+  unsigned long long z = seed + ((r << 22) | node) * 0x9e3779b97f4a7c15ull;
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return (uint32_t)(z >> 32);
+}
+__device__ __forceinline__ float perturbed(float x, float inv_tau, uint32_t rowkey, int v) {
+  uint32_t h = rowkey + (uint32_t)v * 0x9e3779b9u;
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  const float U = ((float)(h >> 9) + 0.5f) * 1.1920928955078125e-07f;
+  // -ln U: series in t = 1 - U (exact) near U = 1, fast log elsewhere (|error| in G < 3e-5)
+  const float t = 1.0f - U;
+  const float e = (t < 0.015625f) ? t * (1.0f + t * (0.5f + t * (0.33333334f + t * 0.25f))) : -__logf(U);
+  return fmaf(x, inv_tau, -__logf(e));
+}
+
+template <bool BF16, bool TMA, bool SAMPLE>
 __global__ void __launch_bounds__(kLayerThreads, 2)
 verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int32_t* accept_len,
-              int32_t* accept_path, int32_t* bonus) {
+              int32_t* accept_path, int32_t* bonus, float inv_tau, unsigned long long seed) {
   constexpr int EPV = BF16 ? 8 : 4;
   constexpr int ESZ = BF16 ? 2 : 4;
   extern __shared__ __align__(128) char dsm[];
@@ -264,11 +292,25 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
         }
       }
       // ---- exact argmax of this (chunk, warp): vector maxima on packed values (bf16x2 max),
-      // one-instruction warp max, then the index is searched only in the vectors holding it ----
+      // one-instruction warp max, then the index is searched only in the vectors holding it.
+      // SAMPLE (T > 0): the same on the perturbed logits x / tau + G (recomputed bit-identically
+      // for the index search) ----
+      const uint32_t rowkey = SAMPLE ? sample_rowkey(seed, (unsigned long long)(P.b_off + r), (unsigned long long)node) : 0u;
+      auto xat = [&](const uint32_t (&w)[4], int e) {
+        return BF16 ? __uint_as_float((e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16))
+                    : __uint_as_float(w[e]);
+      };
       float vm[kVecPerThread];
 #pragma unroll
       for (int j = 0; j < kVecPerThread; ++j) {
-        if (BF16) {
+        if (SAMPLE) {
+          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+          const int e0 = cbase + (j * kConsumers + tid) * EPV;
+          float mx = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) mx = fmax_nan(mx, perturbed(xat(w, e), inv_tau, rowkey, e0 + e));
+          vm[j] = mx;
+        } else if (BF16) {
           const uint32_t mw = bmax2_nan(bmax2_nan(raw[j].x, raw[j].y), bmax2_nan(raw[j].z, raw[j].w));
           vm[j] = fmax_nan(__uint_as_float(mw << 16), __uint_as_float(mw & 0xffff0000u));
         } else {
@@ -290,8 +332,7 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
           const int e0 = cbase + (j * kConsumers + tid) * EPV;
 #pragma unroll
           for (int e = 0; e < EPV; ++e) {
-            const float xv = BF16 ? __uint_as_float((e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16))
-                                  : __uint_as_float(w[e]);
+            const float xv = SAMPLE ? perturbed(xat(w, e), inv_tau, rowkey, e0 + e) : xat(w, e);
             if (xv == Mw && e0 + e < V) li = min(li, e0 + e);
           }
         }
@@ -429,28 +470,48 @@ size_t verify_smem_bytes(int T) {
   return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(VerifyShared) + (size_t)3 * T * 4;
 }
 
+template <bool BF16, bool TMA, bool SAMPLE>
+static void verify_attr(int sm) {
+  cudaFuncSetAttribute(verify_kernel<BF16, TMA, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+
 int verify_occupancy() {
   int n = 0;
   const int sm = (int)verify_smem_bytes(1024);
-  cudaFuncSetAttribute(verify_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(verify_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(verify_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(verify_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true>, kLayerThreads, verify_smem_bytes(1024));
+  verify_attr<true, true, false>(sm);
+  verify_attr<true, false, false>(sm);
+  verify_attr<false, true, false>(sm);
+  verify_attr<false, false, false>(sm);
+  verify_attr<true, true, true>(sm);
+  verify_attr<true, false, true>(sm);
+  verify_attr<false, true, true>(sm);
+  verify_attr<false, false, true>(sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true, false>, kLayerThreads,
+                                                verify_smem_bytes(1024));
   return n > 0 ? n : 1;
 }
 
-void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma, int32_t* accept_len,
-                   int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s) {
-  const char* t = static_cast<const char*>(target);
+template <bool SAMPLE>
+static void launch_verify_t(const Params& P, const char* t, long long ld_bytes, bool tma, int32_t* accept_len,
+                            int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s, float inv_tau,
+                            unsigned long long seed) {
   const size_t sm = verify_smem_bytes(P.T);
+  const dim3 g(grid), blk(kLayerThreads);
   if (P.dtype == SMART_BF16) {
-    if (tma) launch_k(verify_kernel<true, true>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
-    else launch_k(verify_kernel<true, false>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) launch_k(verify_kernel<true, true, SAMPLE>, g, blk, sm, s, P, t, ld_bytes, accept_len, accept_path, bonus, inv_tau, seed);
+    else launch_k(verify_kernel<true, false, SAMPLE>, g, blk, sm, s, P, t, ld_bytes, accept_len, accept_path, bonus, inv_tau, seed);
   } else {
-    if (tma) launch_k(verify_kernel<false, true>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
-    else launch_k(verify_kernel<false, false>, dim3(grid), dim3(kLayerThreads), sm, s, P, t, ld_bytes, accept_len, accept_path, bonus);
+    if (tma) launch_k(verify_kernel<false, true, SAMPLE>, g, blk, sm, s, P, t, ld_bytes, accept_len, accept_path, bonus, inv_tau, seed);
+    else launch_k(verify_kernel<false, false, SAMPLE>, g, blk, sm, s, P, t, ld_bytes, accept_len, accept_path, bonus, inv_tau, seed);
   }
+}
+
+void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma, int32_t* accept_len,
+                   int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s, bool sample, float inv_tau,
+                   unsigned long long seed) {
+  const char* t = static_cast<const char*>(target);
+  if (sample) launch_verify_t<true>(P, t, ld_bytes, tma, accept_len, accept_path, bonus, grid, s, inv_tau, seed);
+  else launch_verify_t<false>(P, t, ld_bytes, tma, accept_len, accept_path, bonus, grid, s, inv_tau, seed);
 }
 
 }  // namespace smart

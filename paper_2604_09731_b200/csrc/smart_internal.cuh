@@ -312,7 +312,8 @@ cudaError_t select_set_smem(size_t bytes);
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok,
                  int32_t* tree_len, cudaStream_t s);
 void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma,
-                   int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s);
+                   int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s,
+                   bool sample = false, float inv_tau = 1.f, unsigned long long seed = 0ull);
 size_t verify_smem_bytes(int T);
 int verify_occupancy();
 cudaError_t mask_set_smem();

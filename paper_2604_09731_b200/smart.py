@@ -30,7 +30,7 @@ MAX_DEPTH = 16
 EXPORTED = ["smart_query_sizes", "smart_create", "smart_nccl_unique_id", "smart_attach_nccl",
             "smart_exchange_record_bytes", "smart_attach_exchange", "smart_select_finish",
             "smart_destroy", "smart_begin_step", "smart_expand_step", "smart_select",
-            "smart_build_mask", "smart_verify_accept", "smart_run_step", "smart_get_stats",
+            "smart_build_mask", "smart_verify_accept", "smart_verify_sample", "smart_run_step", "smart_get_stats",
             "smart_get_tree", "smart_get_candidates", "smart_last_error", "smart_status_string"]
 
 
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         L.smart_select.argtypes = [vp, i32, vp, vp, vp]
         L.smart_build_mask.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.smart_verify_accept.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+        L.smart_verify_sample.argtypes = [vp, vp, i64, C.c_double, C.c_uint64, vp, vp, vp, vp]
         L.smart_run_step.argtypes = [vp, vp, vp, vp, i64, vp, i64] + [vp] * 8 + [vp]
         L.smart_get_stats.argtypes = [vp, C.POINTER(_Stats)]
         L.smart_get_tree.argtypes = [vp, vp, vp, vp, vp, vp, vp]
@@ -248,6 +249,14 @@ class Smart:
     def verify_accept(self, target, accept_len=None, accept_path=None, bonus=None, stream=None):
         ld = target.stride(-2)
         _check(lib().smart_verify_accept(self._h, _ptr(target), ld, _ptr(accept_len), _ptr(accept_path),
+                                         _ptr(bonus), _stream(stream)), self._h)
+
+    def verify_sample(self, target, temperature, seed, accept_len=None, accept_path=None, bonus=None,
+                      stream=None):
+        """A8 at temperature > 0 (NEXT #1): one Gumbel-max target sample per visited node."""
+        ld = target.stride(-2)
+        _check(lib().smart_verify_sample(self._h, _ptr(target), ld, float(temperature),
+                                         int(seed) & ((1 << 64) - 1), _ptr(accept_len), _ptr(accept_path),
                                          _ptr(bonus), _stream(stream)), self._h)
 
     def run_step(self, draft, target, out: dict, root_tok=None, root_pos=None, stream=None):
