@@ -574,14 +574,31 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   stamp(P, tid == 0, 13);
 
   // ---- A6: commit (own requests) ----
-  // (1) admit bitmaps: bit c of request r <=> candidate c (= slot * k + rank) admitted
-  for (int j = tid; j < js; j += NT) {
+  // (1) admit bitmaps (bit c of request r <=> candidate c = slot * k + rank admitted); the
+  // admitted records (and parent path sums) are fetched here so their latency hides behind B6
+  constexpr int kPre = 4;
+  Cand cdr[kPre];
+  double ppr[kPre];
+  int qr[kPre];
+#pragma unroll
+  for (int it = 0; it < kPre; ++it) qr[it] = -1;
+  for (int j = tid, it = 0; j < js; j += NT, ++it) {
     const unsigned long long key = L.keys[j];
     const int r = sel_key_r(key) - P.b_off;
-    if (r >= 0 && r < bl) {
-      const int c = sel_key_c(key);
-      atomicOr(&L.bm[r * nbw + (c >> 5)], 1u << (c & 31));
-    }
+    if (r < 0 || r >= bl) continue;
+    const int c = sel_key_c(key);
+    atomicOr(&L.bm[r * nbw + (c >> 5)], 1u << (c & 31));
+#pragma unroll
+    for (int u = 0; u < kPre; ++u)
+      if (u == it) {
+        qr[u] = L.off[r] * k + c;
+        cdr[u] = load_cand(&P.cand[lbase + qr[u]]);
+      }
+  }
+  if (pmean) {
+#pragma unroll
+    for (int u = 0; u < kPre; ++u)
+      if (qr[u] >= 0) ppr[u] = P.path_sum[(size_t)L.rreq[qr[u] / k] * P.T + cdr[u].parent];
   }
   blk_sync<NT>();  // B6
   auto bits_below = [&](int r, int c) {  // admitted candidates of r with index < c
@@ -590,16 +607,12 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     if (c & 31) n += __popc(L.bm[r * nbw + (c >> 5)] & ((1u << (c & 31)) - 1u));
     return n;
   };
-  // (2) per candidate: admitted flag; admitted ones write their node (index among the request's
-  // admits in canonical order = bits below) and stage cum / parent path sum for (3)
-  for (int q = tid; q < nct; q += NT) {
+  // (2) admitted candidates write their node (index among the request's admits in canonical
+  // order = admit bits below) and stage cum / parent path sum for (3)
+  auto commit_node = [&](int q, const Cand& cd, double pps) {
     const int r = L.rreq[q / k];
     const int c = q - L.off[r] * k;
-    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
-    P.cand_adm[lbase + q] = f;
-    if (!f) continue;
     const int idx = bits_below(r, c);
-    const Cand cd = load_cand(&P.cand[lbase + q]);
     const int node = L.nd[r] + 1 + idx;
     const size_t o = (size_t)r * P.T + node;
     P.tok[o] = cd.tok;
@@ -609,14 +622,26 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     P.cum[o] = cd.cum;
     L.cslot[r * wf + idx] = cd.cum;
     if (pmean) {
-      const double pps = P.path_sum[(size_t)r * P.T + cd.parent];
       L.pslot[r * wf + idx] = pps;
       P.path_sum[o] = pps + (double)cd.cum;
     }
+  };
+#pragma unroll
+  for (int u = 0; u < kPre; ++u)
+    if (qr[u] >= 0) commit_node(qr[u], cdr[u], pmean ? ppr[u] : 0.0);
+  for (int j = tid + kPre * NT; j < js; j += NT) {  // beyond the register prefetch (large lists)
+    const unsigned long long key = L.keys[j];
+    const int r = sel_key_r(key) - P.b_off;
+    if (r < 0 || r >= bl) continue;
+    const int q = L.off[r] * k + sel_key_c(key);
+    const Cand cd = load_cand(&P.cand[lbase + q]);
+    commit_node(q, cd, pmean ? P.path_sum[(size_t)r * P.T + cd.parent] : 0.0);
   }
   blk_sync<NT>();  // B7
-  // (3) per request: admitted count, finish, next-frontier count, E (canonical order)
-  for (int r = tid; r < bl; r += NT) {
+  // (3) per request: admitted count, finish, next-frontier count, E (canonical order).  Up to
+  // 32 requests: warp 0 alone, scan by shuffles (no block barriers); else all threads + scan.
+  const bool one_warp = bl <= 32;
+  for (int r = tid; r < bl && (!one_warp || warp == 0); r += NT) {
     int a = 0;
     for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
     L.adm[r] = a;
@@ -659,17 +684,36 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     }
     P.E_r[r] = L.E[gi];
   }
-  blk_sync<NT>();  // B8
-  const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
+  if (one_warp) {
+    if (warp == 0) {
+      const int v = lane < bl ? L.base[lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < bl) {
+        L.base[lane] = incl - v;
+        P.fr_off[npar][lane] = incl - v;
+      }
+      if (lane == 31) *P.fr_total[npar] = incl;
+    }
+    blk_sync<NT>();  // B8
+  } else {
+    blk_sync<NT>();  // B8
+    const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
+    for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
+    if (tid == 0) *P.fr_total[npar] = total;
+  }
   stamp(P, tid == 0, 14);
-  for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
-  if (tid == 0) *P.fr_total[npar] = total;
   // (4) next frontier (own requests that continue), with the cum of each node for the row merge
   for (int q = tid; q < nct; q += NT) {
     const int r = L.rreq[q / k];
-    if (L.nxt[r] == 0) continue;
     const int c = q - L.off[r] * k;
-    if (!((L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u)) continue;
+    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
+    P.cand_adm[lbase + q] = f;
+    if (!f || L.nxt[r] == 0) continue;
     const int idx = bits_below(r, c);
     P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
     P.fr_cum[npar][L.base[r] + idx] = L.cslot[r * wf + idx];
