@@ -112,28 +112,42 @@ struct __align__(16) ExpandShared {
   WarpTopk w[kConsumerWarps];
 };
 
-// team buffers (double-buffered by row parity), carved after ExpandShared, written remotely by
-// the members into the leader's copy: softmax partials [cpr][8 warps] and lists [kCluster][k]
+// team buffers, carved after ExpandShared.  Receive side (the team leader's copy, double-
+// buffered by row parity): softmax partials [cpr][8 warps] and lists [kCluster][kp].  Send side
+// (every CTA): its slice's partials and top-k list, staged locally and moved to the leader with
+// one shared::cluster bulk copy each (completion counted on the leader's mbarrier).
+// kp = k rounded up to even, so every bulk copy is a multiple of 16 bytes.
+__host__ __device__ inline int list_stride(int k) { return (k + 1) & ~1; }
+
 struct TeamBuf {
   float2* ms[2];
   unsigned long long* lists[2];
-  unsigned long long* surv;  // merge scratch [kCluster * k]
+  unsigned long long* surv;  // merge scratch [kCluster * kp]
+  float2* msl;               // send staging: this CTA's partials [cpr][8]
+  unsigned long long* listl; // send staging: this CTA's top-k [kp]
 };
 
 __host__ __device__ inline size_t team_buf_bytes(int cpr, int k) {
-  return 2 * ((size_t)cpr * kConsumerWarps * 8 + (size_t)kCluster * k * 8) + (size_t)kCluster * k * 8;
+  const size_t kp = (size_t)list_stride(k);
+  return 2 * ((size_t)cpr * kConsumerWarps * 8 + (size_t)kCluster * kp * 8) + (size_t)kCluster * kp * 8 +
+         (size_t)cpr * kConsumerWarps * 8 + kp * 8;
 }
 
 __device__ inline TeamBuf team_buf(char* base, int cpr, int k) {
+  const int kp = list_stride(k);
   TeamBuf t;
   char* p = base;
   for (int b = 0; b < 2; ++b) {
     t.ms[b] = reinterpret_cast<float2*>(p);
     p += (size_t)cpr * kConsumerWarps * 8;
     t.lists[b] = reinterpret_cast<unsigned long long*>(p);
-    p += (size_t)kCluster * k * 8;
+    p += (size_t)kCluster * kp * 8;
   }
   t.surv = reinterpret_cast<unsigned long long*>(p);
+  p += (size_t)kCluster * kp * 8;
+  t.msl = reinterpret_cast<float2*>(p);
+  p += (size_t)cpr * kConsumerWarps * 8;
+  t.listl = reinterpret_cast<unsigned long long*>(p);
   return t;
 }
 
@@ -147,12 +161,6 @@ __device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {  /
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
   return a;
-}
-__device__ __forceinline__ void st_cluster_f2(uint32_t a, float2 v) {
-  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u64(uint32_t a, unsigned long long v) {
-  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t a, uint32_t count) {  // remote, release.cluster
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -168,6 +176,15 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
       "r"(parity), "r"(0x989680)  // suspend-time hint: sleep instead of re-polling (each poll invalidates L1)
       : "memory");
 }
+// bulk copy of `bytes` (multiple of 16) from this CTA's shared memory to a cluster address,
+// completion (tx bytes) signalled on the destination CTA's mbarrier
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "r"(smem_u32(src)), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -194,7 +211,7 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
 // T = the best k-th entry over the members' lists (each list is its slice's top-k, so T bounds the
 // row's k-th best key from below); the entries >= T are ranked among themselves and the top k
 // written with p (A1) and cum (A2, Eq.(3)).
-__device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int t,
+__device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int slot, int t,
                                const float2* ms, const unsigned long long* lists, unsigned long long* surv) {
   const int lane = threadIdx.x & 31;
   const int k = P.k, cpr = P.cpr;
@@ -211,12 +228,13 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
   }
   const float Z = warp_sum(z);
   // (2) threshold: best tail over the members' lists
-  const unsigned long long tail = lane < t ? lists[lane * k + k - 1] : 0ull;
+  const int kp = list_stride(k);
+  const unsigned long long tail = lane < t ? lists[lane * kp + k - 1] : 0ull;
   const unsigned th = __reduce_max_sync(kFull, (unsigned)(tail >> 32));
   const unsigned tl = __reduce_max_sync(kFull, (unsigned)(tail >> 32) == th ? (unsigned)tail : 0u);
   const unsigned long long T = ((unsigned long long)th << 32) | tl;
   // (3) survivors, compacted by ballot
-  const int nkey = t * k;
+  const int nkey = t * kp;  // the padding slot of an odd k holds a key below every real one
   int ns = 0;
   for (int e0 = 0; e0 < nkey; e0 += 32) {
     const int e = e0 + lane;
@@ -250,7 +268,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
     }
   }
   if (lane == 0) {
-    P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, row - P.fr_off[par][fe.x]);
+    P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, slot);
     P.rowstat[row] = make_float2(M, Z);
     if (!(Z >= 1.0f) || isinf(Z) || isnan(M)) atomicOr(P.err, kErrDraftNaN);  // Q23
   }
@@ -275,8 +293,8 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       mbar_init(&pipe.full[s], 1);
       mbar_init(&pipe.empty[s], kConsumerWarps);
     }
-    mbar_init(&sh.ready[0], kCluster);  // members arrive with count kCluster / t
-    mbar_init(&sh.ready[1], kCluster);
+    mbar_init(&sh.ready[0], 1);  // the leader's arrive.expect_tx; members complete the bytes
+    mbar_init(&sh.ready[1], 1);
     mbar_init(&sh.freeb[0], 1);
     mbar_init(&sh.freeb[1], 1);
     mbar_fence_init();
@@ -288,6 +306,17 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   pdl_wait();
   pdl_trigger();
   tl_start(P, layer);
+  // the first row's frontier entry for each possible team size t = 8 >> tid, fetched together
+  // with the row count (the team layout is only known once R is)
+  int2 sfe = make_int2(0, 0);
+  float scum = 0.f;
+  if (tid < 4) {
+    const int row = (int)blockIdx.x / (kCluster >> tid);
+    if (row < P.cap_rows) {
+      sfe = P.fr[par][row];
+      scum = P.fr_cum[par][row];
+    }
+  }
   const int R = *P.fr_total[par];
   const bool t0 = (blockIdx.x == 0 && tid == 0);
   gstamp(P, t0, 16);
@@ -310,10 +339,16 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   const int nrows = ((int)blockIdx.x < S && team < R) ? (R - team + nteams - 1) / nteams : 0;
   const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;  // this CTA's chunks of each row
   const int nstage = min(nrows, kStageRows);
-  if (tid < nstage) {
-    const int row = team + tid * nteams;
-    sh.rfe[tid] = P.fr[par][row];
-    sh.rcum[tid] = P.fr_cum[par][row];
+  const int tsel = (t == 8) ? 0 : (t == 4) ? 1 : (t == 2) ? 2 : 3;
+  if (nstage > 0 && tid == tsel) {
+    sh.rfe[0] = sfe;
+    sh.rcum[0] = scum;
+  }
+  if (tid >= 4 && tid - 3 < nstage) {  // further rows (large layers)
+    const int n = tid - 3;
+    const int row = team + n * nteams;
+    sh.rfe[n] = P.fr[par][row];
+    sh.rcum[n] = P.fr_cum[par][row];
   }
   __syncthreads();
   gstamp(P, t0, 17);
@@ -351,9 +386,12 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         const int b = n & 1;
         const int2 fe = rowfe(n, row);
         const float pc = n < kStageRows ? sh.rcum[n] : P.fr_cum[par][row];
+        const int slot = row - P.fr_off[par][fe.x];  // frontier slot within the request (loaded while waiting)
+        if (lane == 0)  // this row's bytes: all chunk partials + t lists
+          mbar_expect_tx(&sh.ready[b], (uint32_t)(cpr * kConsumerWarps * 8 + t * list_stride(k) * 8));
         mbar_wait_acq_cluster(&sh.ready[b], (uint32_t)(n >> 1) & 1u);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 24);
-        merge_row_team(P, layer, par, row, fe, pc, t, tb.ms[b], tb.lists[b], tb.surv);
+        merge_row_team(P, layer, par, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 25);
         if (lane < t) mbar_arrive_cluster(mapa_rank(&sh.freeb[b], lrank + lane), 1);  // buffer b is free
         if (lane == 0) {
@@ -372,7 +410,10 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       const int row = team + n * nteams;
       const int b = n & 1;
       if (n >= 2) mbar_wait_acq_cluster(&sh.freeb[b], (uint32_t)((n - 2) >> 1) & 1u);  // leader done with b
-      const uint32_t ms_remote = mapa_rank(tb.ms[b], lrank);
+      if (n >= 1) {  // the previous slice's bulk copies have read the send staging
+        if (tid == 0) bulk_wait_read();
+        consumer_sync();
+      }
       unsigned long long bound = 0ull;  // lower bound of the slice's k-th best key
       for (int c = mlo; c < mhi; ++c, ++i) {
         uint4 raw[kVecPerThread];
@@ -426,7 +467,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         }
         const float sacc = warp_sum((f2lo(acc2[0]) + f2hi(acc2[0])) + (f2lo(acc2[1]) + f2hi(acc2[1])));
         gstamp(P, t0 && i < 2, 19 + 3 * i);
-        if (lane == 0) st_cluster_f2(ms_remote + (uint32_t)((c * kConsumerWarps + warp) * 8), make_float2(Mw, sacc));
+        if (lane == 0) tb.msl[(c - mlo) * kConsumerWarps + warp] = make_float2(Mw, sacc);
 
         // ---- top-k candidates of this warp-chunk ----
         // CTA-wide bound at the slice's first chunk: every warp publishes its top-j lane maxima
@@ -575,6 +616,8 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       consumer_sync();
       gstamp(P, t0 && n == 0, 31);
       {
+        // rank of each of the nl = 8k entries against the whole list (broadcast 16-byte reads:
+        // one shared-memory wavefront per load)
         const int nl = kConsumerWarps * k;  // even
         if (tid < nl) {
           const unsigned long long key = sh.cl[tid];
@@ -587,12 +630,23 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
             r1 += (v.y > key);
           }
           const int rank = r0 + r1;
-          if (rank < k) st_cluster_u64(mapa_rank(tb.lists[b] + member * k + rank, lrank), key);
+          if (rank < k) tb.listl[rank] = key;
         }
+        if ((k & 1) && tid == 0) tb.listl[k] = kKeySentinel - 1000;  // even-k padding slot
       }
-      consumer_sync();  // the CTA's stores precede the arrive (release.cluster is cumulative)
+      gstamp(P, t0 && n == 0, 96);
+      consumer_sync();  // staging complete
+      gstamp(P, t0 && n == 0, 97);
       if (tid == 0) {
-        mbar_arrive_cluster(mapa_rank(&sh.ready[b], lrank), kCluster / t);
+        // two bulk copies into the leader's buffers; their bytes complete its ready barrier
+        fence_proxy_async_smem();
+        const uint32_t bar = mapa_rank(&sh.ready[b], lrank);
+        const int kp = list_stride(k);
+        bulk_s2cluster(mapa_rank(tb.ms[b] + mlo * kConsumerWarps, lrank), tb.msl,
+                       (uint32_t)((mhi - mlo) * kConsumerWarps * 8), bar);
+        bulk_s2cluster(mapa_rank(tb.lists[b] + member * kp, lrank), tb.listl, (uint32_t)(kp * 8), bar);
+        bulk_commit();
+        gstamp(P, t0 && n == 0, 98);
         sh.tau = 0ull;  // next slice (other warps read it only after the next slice's first barrier)
       }
       gstamp(P, t0 && n == 0, 27);
@@ -614,6 +668,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
     gstamp(P, tid == 0, 29);
   }
+  if (tid == 0) bulk_wait_read();  // staging buffers stay valid until the copies have read them
   if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[640 + blockIdx.x] = gtime();  // per-CTA work end (debug)
   // every CTA stays until the cluster is done with its shared memory (remote stores / arrives)
   cluster_sync_all();

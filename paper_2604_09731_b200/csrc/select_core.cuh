@@ -470,35 +470,42 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const double C = L.ctab[j];
     return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
   };
-  // ---- A5 (warp 0): Eq.(16) scan over the sorted list, cut, argmax_j S_j ----
-  if (warp == 0) {
-    int R_all = R;
-    if (mode == kSelGlobal) {
-      long long nloc = 0, eloc = 0, rloc = 0;
-      for (int i = lane; i < P.b_glob; i += 32) {
-        const int g = i / bl, r = i - g * bl;
-        nloc += reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8)[r];
-      }
-      for (int g = lane; g < P.nranks; g += 32) {
-        const int* h = reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8);
-        eloc += h[bl];
-        rloc += h[bl + 1];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        nloc += __shfl_xor_sync(kFull, nloc, o);
-        eloc += __shfl_xor_sync(kFull, eloc, o);
-        rloc += __shfl_xor_sync(kFull, rloc, o);
-      }
-      N0 = nloc;
-      ne = (int)eloc;
-      R_all = (int)rloc;
+  // ---- A5 (warp 0): Eq.(16) scan over the sorted list -> the cut js (the only result the
+  // commit waits for); argmax_j S_j and the admitted benefit sum are computed by warp 1 during
+  // the commit's tail (a5_report below) ----
+  if (mode == kSelGlobal && warp == 0) {
+    long long nloc = 0, eloc = 0, rloc = 0;
+    for (int i = lane; i < P.b_glob; i += 32) {
+      const int g = i / bl, r = i - g * bl;
+      nloc += reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8)[r];
     }
-    const double E0 = ss.bcast_d[2];  // precomputed before the wait
-    const double Sb0 = sp(E0, 0);
-    const double dc0 = L.dtab[0];
-    const double ac = P.alpha * P.c_T;
-    const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
+    for (int g = lane; g < P.nranks; g += 32) {
+      const int* h = reinterpret_cast<const int*>(P.xr + (size_t)g * P.xstride + (size_t)P.m_cap * 8 + (size_t)bl * 8);
+      eloc += h[bl];
+      rloc += h[bl + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      nloc += __shfl_xor_sync(kFull, nloc, o);
+      eloc += __shfl_xor_sync(kFull, eloc, o);
+      rloc += __shfl_xor_sync(kFull, rloc, o);
+    }
+    if (lane == 0) {
+      ss.bcast_l[1] = nloc;
+      ss.bcast_i[2] = (int)eloc;
+      ss.bcast_i[4] = (int)rloc;
+    }
+    __syncwarp();
+  }
+  const double E0 = ss.bcast_d[2];  // precomputed before the wait
+  const double ac = P.alpha * P.c_T;
+  const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
+  const double dc0 = L.dtab[0];
+  if (warp == 0) {
+    if (mode == kSelGlobal) {
+      N0 = ss.bcast_l[1];
+      ne = ss.bcast_i[2];
+    }
     // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
     const int per = (ne + 31) >> 5;
     const int j0 = min(ne, lane * per), j1 = min(ne, j0 + per);
@@ -512,8 +519,6 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     }
     lex -= lt;
     int first_fail = ne;
-    double bestS = Sb0;
-    int bestj = 0;
     double before = lex;
     for (int j = j0; j < j1; ++j) {
       const double bj = (double)sel_key_b(L.keys[j]);
@@ -526,47 +531,17 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         const double C = L.ctab[j];
         ok = (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
       }
-      if (!ok && j < first_fail) first_fail = j;
-      const double Sa = sp(E0 + before + bj, j + 1);
-      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
-        bestS = Sa;
-        bestj = j + 1;
+      if (!ok) {
+        first_fail = j;
+        break;
       }
       before += bj;
     }
     first_fail = __reduce_min_sync(kFull, first_fail);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double os = __shfl_xor_sync(kFull, bestS, o);
-      const int oj = __shfl_xor_sync(kFull, bestj, o);
-      if (os > bestS || (os == bestS && oj < bestj)) {
-        bestS = os;
-        bestj = oj;
-      }
-    }
-    const int js = first_fail;
-    // sum of the admitted benefits (lane chunks, xor tree: a function of (ne, js) only)
-    double ab = 0.0;
-    for (int j = j0; j < min(j1, js); ++j) ab += (double)sel_key_b(L.keys[j]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ab += __shfl_xor_sync(kFull, ab, o);
     if (lane == 0) {
-      ss.bcast_i[3] = js;
-      ss.bcast_d[1] = ab;
-      ss.bcast_d[2] = E0;
+      ss.bcast_i[3] = first_fail;
+      ss.bcast_i[5] = ne;
       ss.bcast_l[0] = N0;
-      tr.executed = R_all > 0 ? 1 : 0;
-      tr.n_rows = R;
-      tr.n_cand = nct;
-      tr.n_elig = ne;
-      tr.n_admit = js;
-      tr.argmax_j = bestj;
-      tr.N0 = (int)N0;
-      tr.E0 = E0;
-      tr.S0 = Sb0 / bc;
-      tr.dc0 = dc0;
-      tr.saturated = (N0 + ne >= P.sat_from) ? 1 : 0;
-      if (tr.saturated) atomicOr(P.err, kErrSaturated);
     }
   }
   blk_sync<NT>();  // B5
@@ -718,26 +693,76 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
     P.fr_cum[npar][L.base[r] + idx] = L.cslot[r * wf + idx];
   }
-  if (warp == 0) {
-    // ---- totals after the layer (trace S_after) ----
-    const double E0 = ss.bcast_d[2];
-    const long long N0w = ss.bcast_l[0];
-    if (mode == kSelFull) {
-      const double Ea = warp_det_sum(L.E, bl, lane);
-      if (lane == 0) {
-        tr.S_after = sp(Ea, js) / bc;
-        *P.N_glob = (int)(N0w + js);
-        *P.E_glob = Ea;
-      }
-    } else if (lane == 0) {
-      // NODE_SUM: E after = E0 + sum of admitted benefits (exact); PATH_MEAN: approximate
-      const double Ea = E0 + ss.bcast_d[1];
+  // ---- totals after the layer (trace S_after) ∥ the A5 report (argmax_j S_j, trace) ----
+  if (warp == 0 && mode == kSelFull) {
+    const double Ea = warp_det_sum(L.E, bl, lane);
+    if (lane == 0) {
       tr.S_after = sp(Ea, js) / bc;
-      *P.N_glob = (int)(N0w + js);
+      *P.N_glob = (int)(ss.bcast_l[0] + js);
       *P.E_glob = Ea;
     }
-    stamp(P, lane == 0, 22);
   }
+  if (warp == 1) {
+    const int ne_r = ss.bcast_i[5];
+    const long long N0r = ss.bcast_l[0];
+    const int R_all = (mode == kSelGlobal) ? ss.bcast_i[4] : R;
+    const double Sb0 = sp(E0, 0);
+    const int per = (ne_r + 31) >> 5;
+    const int j0 = min(ne_r, lane * per), j1 = min(ne_r, j0 + per);
+    double lt = 0.0;
+    for (int j = j0; j < j1; ++j) lt += (double)sel_key_b(L.keys[j]);
+    double lex = lt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(kFull, lex, o);
+      if (lane >= o) lex += u;
+    }
+    lex -= lt;
+    double bestS = Sb0, before = lex, ab = 0.0;
+    int bestj = 0;
+    for (int j = j0; j < j1; ++j) {
+      const double bj = (double)sel_key_b(L.keys[j]);
+      const double Sa = sp(E0 + before + bj, j + 1);
+      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+        bestS = Sa;
+        bestj = j + 1;
+      }
+      if (j < js) ab += bj;
+      before += bj;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_xor_sync(kFull, bestS, o);
+      const int oj = __shfl_xor_sync(kFull, bestj, o);
+      if (os > bestS || (os == bestS && oj < bestj)) {
+        bestS = os;
+        bestj = oj;
+      }
+      ab += __shfl_xor_sync(kFull, ab, o);
+    }
+    if (lane == 0) {
+      tr.executed = R_all > 0 ? 1 : 0;
+      tr.n_rows = R;
+      tr.n_cand = nct;
+      tr.n_elig = ne_r;
+      tr.n_admit = js;
+      tr.argmax_j = bestj;
+      tr.N0 = (int)N0r;
+      tr.E0 = E0;
+      tr.S0 = Sb0 / bc;
+      tr.dc0 = dc0;
+      tr.saturated = (N0r + ne_r >= P.sat_from) ? 1 : 0;
+      if (tr.saturated) atomicOr(P.err, kErrSaturated);
+      if (mode != kSelFull) {
+        // NODE_SUM: E after = E0 + sum of admitted benefits (exact); PATH_MEAN: approximate
+        const double Ea = E0 + ab;
+        tr.S_after = sp(Ea, js) / bc;
+        *P.N_glob = (int)(N0r + js);
+        *P.E_glob = Ea;
+      }
+    }
+  }
+  stamp(P, tid == 0, 22);
 }
 
 }  // namespace smart
