@@ -164,6 +164,59 @@ __device__ void bitonic_sort(unsigned long long* keys, int P2) {
   }
 }
 
+// ascending bitonic sort of keys[0..P2) with two keys per thread (P2 <= 2*NT, power of two):
+// strides < 32 exchange by shuffles, stride 32 inside the thread, strides >= 64 through shared
+// memory (2 barriers each).  Element i lives in warp i/64, register (i%64)/32, lane i%32.
+template <int NT>
+__device__ void bitonic_sort_reg(unsigned long long* keys, int P2) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = warp * 64 + lane, i1 = i0 + 32;
+  const bool act = i0 < P2;
+  unsigned long long v0 = act ? keys[i0] : ~0ull, v1 = act ? keys[i1] : ~0ull;
+  auto cx_reg = [](unsigned long long& a, unsigned long long& b, bool asc) {  // a at lower index
+    const bool sw = (a > b) == asc;
+    const unsigned long long t = sw ? b : a;
+    b = sw ? a : b;
+    a = t;
+  };
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 64) {
+        blk_sync<NT>();  // previous readers done
+        if (act) {
+          keys[i0] = v0;
+          keys[i1] = v1;
+        }
+        blk_sync<NT>();
+        if (act) {
+          const int p0 = i0 ^ stride, p1 = i1 ^ stride;
+          const unsigned long long o0 = keys[p0], o1 = keys[p1];
+          const bool asc0 = (i0 & size) == 0, asc1 = (i1 & size) == 0;
+          // keep min if (lower index) == asc, else max
+          v0 = ((i0 < p0) == asc0) ? (v0 < o0 ? v0 : o0) : (v0 > o0 ? v0 : o0);
+          v1 = ((i1 < p1) == asc1) ? (v1 < o1 ? v1 : o1) : (v1 > o1 ? v1 : o1);
+        }
+      } else if (stride == 32) {
+        const bool asc = (i0 & size) == 0;  // i0 and i1 = i0 + 32 share the direction bit (size >= 64)
+        cx_reg(v0, v1, asc);
+      } else {
+        const unsigned long long o0 = __shfl_xor_sync(kFull, v0, stride);
+        const unsigned long long o1 = __shfl_xor_sync(kFull, v1, stride);
+        const bool lo = (lane & stride) == 0;
+        const bool asc0 = (i0 & size) == 0, asc1 = (i1 & size) == 0;
+        v0 = (lo == asc0) ? (v0 < o0 ? v0 : o0) : (v0 > o0 ? v0 : o0);
+        v1 = (lo == asc1) ? (v1 < o1 ? v1 : o1) : (v1 > o1 ? v1 : o1);
+      }
+    }
+  }
+  blk_sync<NT>();
+  if (act) {
+    keys[i0] = v0;
+    keys[i1] = v1;
+  }
+  blk_sync<NT>();
+}
+
 // ---- layout of the dynamic shared memory used by select_layer --------------------------------
 // Per candidate only its benefit (4 B) is staged; records are re-read from global (L2) at commit.
 // Admitted candidates are per-request bitmaps (bit c = candidate index within the request).
@@ -445,7 +498,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     while (P2 < nsort) P2 <<= 1;
     for (int i = nsort + tid; i < P2; i += NT) L.keys[i] = ~0ull;
     blk_sync<NT>();
-    bitonic_sort<NT>(L.keys, P2);
+    if (P2 <= 2 * NT) bitonic_sort_reg<NT>(L.keys, P2);
+    else bitonic_sort<NT>(L.keys, P2);
   }
   stamp(P, tid == 0, 12);
 
@@ -501,11 +555,92 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   const double ac = P.alpha * P.c_T;
   const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
   const double dc0 = L.dtab[0];
-  if (warp == 0) {
-    if (mode == kSelGlobal) {
-      N0 = ss.bcast_l[1];
-      ne = ss.bcast_i[2];
+  if (mode == kSelGlobal) {
+    blk_sync<NT>();
+    N0 = ss.bcast_l[1];
+    ne = ss.bcast_i[2];
+  }
+  // long lists (>= 512 eligible): 8 warps, group-contiguous then lane-contiguous chunks; short
+  // lists: warp 0 alone.  Either way the fp64 association is a function of ne only.
+  const bool big = ne >= 512;
+  auto rule_ok = [&](double bj, double before, int j) {
+    // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
+    // cost == 0 means S := 0, i.e. admit any positive benefit)
+    if (P.selection == SMART_FROZEN)
+      return (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > rhs0 * dc0) : (bj > 0.0);
+    const double C = L.ctab[j];
+    return (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
+  };
+  if (big) {
+    constexpr int kA5 = 8;
+    const int gper = (ne + kA5 - 1) / kA5;
+    const int g0 = min(ne, warp * gper), g1 = min(ne, g0 + gper);
+    const int per = (gper + 31) >> 5;
+    const int j0 = min(g1, g0 + lane * per), j1 = min(g1, j0 + per);
+    double lt = 0.0, lex = 0.0;
+    if (warp < kA5) {
+      for (int j = j0; j < j1; ++j) lt += (double)sel_key_b(L.keys[j]);
+      lex = lt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(kFull, lex, o);
+        if (lane >= o) lex += u;
+      }
+      if (lane == 31) ss.tile_d[warp] = lex;  // group total
+      lex -= lt;
     }
+    blk_sync<NT>();
+    if (warp < kA5) {
+      double before = lex;
+      for (int w = 0; w < warp; ++w) before += ss.tile_d[w];  // groups in order
+      int ff = ne;
+      double bestS = -1.0;
+      int bestj = ne + 1;
+      for (int j = j0; j < j1; ++j) {
+        const double bj = (double)sel_key_b(L.keys[j]);
+        if (ff == ne && !rule_ok(bj, before, j)) ff = j;
+        const double Sa = sp(E0 + before + bj, j + 1);
+        if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+          bestS = Sa;
+          bestj = j + 1;
+        }
+        before += bj;
+      }
+      ff = __reduce_min_sync(kFull, ff);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(kFull, bestS, o);
+        const int oj = __shfl_xor_sync(kFull, bestj, o);
+        if (os > bestS || (os == bestS && oj < bestj)) {
+          bestS = os;
+          bestj = oj;
+        }
+      }
+      if (lane == 0) {
+        ss.wred_i[warp] = ff;
+        ss.wred_d[warp] = bestS;
+        ss.tile_i[warp] = bestj;
+      }
+    }
+    blk_sync<NT>();
+    if (warp == 0 && lane == 0) {
+      int js0 = ne, bj = 0;
+      double bs = sp(E0, 0);
+      for (int w = 0; w < kA5; ++w) {
+        js0 = min(js0, ss.wred_i[w]);
+        const double os = ss.wred_d[w];
+        const int oj = ss.tile_i[w];
+        if (oj <= ne && (os > bs || (os == bs && oj < bj))) {
+          bs = os;
+          bj = oj;
+        }
+      }
+      ss.bcast_i[3] = js0;
+      ss.bcast_i[5] = ne;
+      ss.bcast_i[6] = bj;  // argmax_j, reported by warp 1 in the tail
+      ss.bcast_l[0] = N0;
+    }
+  } else if (warp == 0) {
     // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
     const int per = (ne + 31) >> 5;
     const int j0 = min(ne, lane * per), j1 = min(ne, j0 + per);
@@ -522,16 +657,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     double before = lex;
     for (int j = j0; j < j1; ++j) {
       const double bj = (double)sel_key_b(L.keys[j]);
-      // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
-      // cost == 0 means S := 0, i.e. admit any positive benefit)
-      bool ok;
-      if (P.selection == SMART_FROZEN) {
-        ok = (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > rhs0 * dc0) : (bj > 0.0);
-      } else {
-        const double C = L.ctab[j];
-        ok = (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
-      }
-      if (!ok) {
+      if (!rule_ok(bj, before, j)) {
         first_fail = j;
         break;
       }
@@ -541,6 +667,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     if (lane == 0) {
       ss.bcast_i[3] = first_fail;
       ss.bcast_i[5] = ne;
+      ss.bcast_i[6] = -1;  // argmax_j computed by warp 1 in the tail
       ss.bcast_l[0] = N0;
     }
   }
@@ -557,7 +684,11 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   int qr[kPre];
 #pragma unroll
   for (int it = 0; it < kPre; ++it) qr[it] = -1;
-  for (int j = tid, it = 0; j < js; j += NT, ++it) {
+  // NODE_SUM with <= 32 requests: warp 0 runs the per-request step (3) right after the bitmaps
+  // (E from the staged benefits, b == cum) while warps 1.. write the nodes
+  const bool fast3 = (bl <= 32) && !pmean;
+  const int c0t = fast3 ? 32 : 0, cstep = fast3 ? NT - 32 : NT;
+  for (int j = tid - c0t, it = 0; j < js && tid >= c0t; j += cstep, ++it) {
     const unsigned long long key = L.keys[j];
     const int r = sel_key_r(key) - P.b_off;
     if (r < 0 || r >= bl) continue;
@@ -604,7 +735,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
 #pragma unroll
   for (int u = 0; u < kPre; ++u)
     if (qr[u] >= 0) commit_node(qr[u], cdr[u], pmean ? ppr[u] : 0.0);
-  for (int j = tid + kPre * NT; j < js; j += NT) {  // beyond the register prefetch (large lists)
+  for (int j = tid - c0t + kPre * cstep; j < js && tid >= c0t; j += cstep) {  // beyond the register prefetch
     const unsigned long long key = L.keys[j];
     const int r = sel_key_r(key) - P.b_off;
     if (r < 0 || r >= bl) continue;
@@ -612,7 +743,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const Cand cd = load_cand(&P.cand[lbase + q]);
     commit_node(q, cd, pmean ? P.path_sum[(size_t)r * P.T + cd.parent] : 0.0);
   }
-  blk_sync<NT>();  // B7
+  if (!fast3) blk_sync<NT>();  // B7
   // (3) per request: admitted count, finish, next-frontier count, E (canonical order).  Up to
   // 32 requests: warp 0 alone, scan by shuffles (no block barriers); else all threads + scan.
   const bool one_warp = bl <= 32;
@@ -630,7 +761,18 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
     if (!pmean) {
       double esum = 0.0;
-      for (int u = 0; u < a; ++u) esum += (double)L.cslot[r * wf + u];
+      if (fast3) {  // staged benefits (b == cum), canonical order
+        const int s0 = L.off[r] * k;
+        for (int w = 0; w < nbw; ++w) {
+          unsigned bits = L.bm[r * nbw + w];
+          while (bits) {
+            esum += (double)L.cb[s0 + w * 32 + __ffs(bits) - 1];
+            bits &= bits - 1u;
+          }
+        }
+      } else {
+        for (int u = 0; u < a; ++u) esum += (double)L.cslot[r * wf + u];
+      }
       L.E[gi] += esum;  // node sum (Q11)
     } else {
       // Eq.(2) path mean of the committed tree: leaves lose their admitted-into parents
@@ -704,6 +846,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   }
   if (warp == 1) {
     const int ne_r = ss.bcast_i[5];
+    const int argmax_pre = ss.bcast_i[6];  // long lists: already reduced by the A5 groups
     const long long N0r = ss.bcast_l[0];
     const int R_all = (mode == kSelGlobal) ? ss.bcast_i[4] : R;
     const double Sb0 = sp(E0, 0);
@@ -722,10 +865,12 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     int bestj = 0;
     for (int j = j0; j < j1; ++j) {
       const double bj = (double)sel_key_b(L.keys[j]);
-      const double Sa = sp(E0 + before + bj, j + 1);
-      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
-        bestS = Sa;
-        bestj = j + 1;
+      if (argmax_pre < 0) {
+        const double Sa = sp(E0 + before + bj, j + 1);
+        if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+          bestS = Sa;
+          bestj = j + 1;
+        }
       }
       if (j < js) ab += bj;
       before += bj;
@@ -746,7 +891,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       tr.n_cand = nct;
       tr.n_elig = ne_r;
       tr.n_admit = js;
-      tr.argmax_j = bestj;
+      tr.argmax_j = argmax_pre >= 0 ? argmax_pre : bestj;
       tr.N0 = (int)N0r;
       tr.E0 = E0;
       tr.S0 = Sb0 / bc;
