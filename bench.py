@@ -198,13 +198,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg3_llama8b_b32", choices=list(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cost", default="roofline", choices=["roofline", "measured"],
+                    help="cost-model fixture: roofline-fitted (default) or measured on a B200 (NEXT #2)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     wl = WORKLOADS[args.workload]
     import make_cost_fixture as mcf
-    cost_fx = mcf.load(wl["fixture"])
+    cost_fx = mcf.load(wl["fixture"] if args.cost == "roofline" else "measured_" + wl["fixture"])
     if args.impl == "reference":
         return run_reference(args, wl, cost_fx)
 
@@ -460,7 +462,7 @@ def main():
             "config": {"workload": args.workload, "desc": wl["desc"], "V": V, "batch_per_gpu": b,
                        "global_batch": b * world, "depth": wl["d"], "top_k": wl["k"], "max_frontier": wl["W"],
                        "B_verify": wl["B_verify"] * world, "alpha": ALPHA, "preset": "HOTPATH (PREFIX, NODE_SUM, omega=1)",
-                       "cost_fixture": f"fixtures/cost_b200_{wl['fixture']}.txt", "synth": SYNTH,
+                       "cost_fixture": f"fixtures/cost_b200_{wl['fixture'] if args.cost == 'roofline' else 'measured_' + wl['fixture']}.txt", "synth": SYNTH,
                        "l2": f"{n_pools} rotating input pools x {set_bytes / 1e6:.1f} MB (> 4x L2 {l2 / 1e6:.0f} MB)",
                        "parallelism": f"requests sharded dp{world}" + (", NCCL all-gather per layer" if world > 1 else "")},
             "clocks": clocks,

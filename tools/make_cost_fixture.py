@@ -37,45 +37,32 @@ def peaks():
 
 
 def fit_verify(xs, ys):
-    """grid over (delta, rho), closed-form gamma, then golden-section refinement."""
+    """grid over (delta, rho) with gamma in closed form, then a local refinement of
+    the best grid point (Nelder-Mead in (log delta, rho), gamma still closed form)."""
     xs, ys = np.asarray(xs, float), np.asarray(ys, float)
 
-    def sse(d, r):
-        g = np.expm1(np.minimum(d * xs ** r, 50.0))
+    def sse(ld, r):
+        g = np.expm1(np.minimum(math.exp(ld) * xs ** r, 50.0))
         den = float(g @ g)
         gam = max(0.0, float(g @ ys) / den) if den > 0 else 0.0
         return float(((gam * g - ys) ** 2).sum()), gam
 
     best = None
-    xmax = float(xs.max())
-    for d in np.logspace(-6, 0, 96):
-        for r in np.linspace(0.3, 2.5, 60):
-            if d * xmax ** r > 10.0:   # keep the fitted curve sane just past the samples
-                continue
-            e, g = sse(d, r)
+    for ld in np.linspace(math.log(1e-9), math.log(1.0), 241):
+        for r in np.linspace(0.3, 3.0, 136):
+            e, g = sse(ld, r)
             if best is None or e < best[0]:
-                best = (e, d, r, g)
-    _, d, r, g = best
-    phi = (math.sqrt(5) - 1) / 2
-    for _ in range(3):
-        for which in ("d", "r"):
-            lo, hi = (d / 2, min(d * 2, 10.0 / xmax ** r)) if which == "d" else (
-                max(0.3, r - 0.2), min(r + 0.2, math.log(10.0 / d) / math.log(xmax)))
-            a, b = lo, hi
-            for _ in range(40):
-                c1, c2 = b - phi * (b - a), a + phi * (b - a)
-                f1 = sse(c1, r)[0] if which == "d" else sse(d, c1)[0]
-                f2 = sse(c2, r)[0] if which == "d" else sse(d, c2)[0]
-                if f1 < f2:
-                    b = c2
-                else:
-                    a = c1
-            if which == "d":
-                d = (a + b) / 2
-            else:
-                r = (a + b) / 2
-    e, g = sse(d, r)
-    return g, d, r, math.sqrt(e / len(xs))
+                best = (e, ld, r, g)
+    _, ld, r, g = best
+    # refinement of the grid optimum: Nelder-Mead on (log delta, rho), gamma in closed form (the
+    # valley is narrow and curved, where per-coordinate golden-section search stalls)
+    from scipy.optimize import minimize
+    res = minimize(lambda v: sse(v[0], v[1])[0], x0=[ld, r], method="Nelder-Mead",
+                   options=dict(xatol=1e-10, fatol=1e-18, maxiter=20000, maxfev=40000))
+    if res.fun <= sse(ld, r)[0] and res.x[1] > 0:
+        ld, r = float(res.x[0]), float(res.x[1])
+    e, g = sse(ld, r)
+    return g, math.exp(ld), r, math.sqrt(e / len(xs))
 
 
 def fixture(name, b, d, P, W_bytes, Pd, Wd_bytes, B_verify, t0=0.010, samples=None):
