@@ -191,6 +191,11 @@ __device__ __forceinline__ float perturbed(float x, float inv_tau, uint32_t rowk
   return fmaf(x, inv_tau, -__logf(e));
 }
 
+// the verify stream: 3 stages x 16 KiB per CTA, 3 CTAs per SM (more warps in flight per SM than
+// the layer kernel's 2 x 5 stages: the argmax work per element is smaller)
+constexpr int kVStages = 3;
+using VPipe = StreamPipeT<kVStages>;
+
 template <bool BF16, bool TMA, bool SAMPLE>
 __global__ void __launch_bounds__(kLayerThreads, 2)
 verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int32_t* accept_len,
@@ -199,11 +204,11 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
   constexpr int ESZ = BF16 ? 2 : 4;
   extern __shared__ __align__(128) char dsm[];
   char* ring = dsm;
-  StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
-  VerifyShared& sh = *reinterpret_cast<VerifyShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
+  VPipe& pipe = *reinterpret_cast<VPipe*>(dsm + kVStages * kChunkBytes);
+  VerifyShared& sh = *reinterpret_cast<VerifyShared*>(dsm + kVStages * kChunkBytes + sizeof(VPipe));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kVStages; ++s) {
       mbar_init(&pipe.full[s], 1);
       mbar_init(&pipe.empty[s], kConsumerWarps);
     }
@@ -249,8 +254,8 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
       const int cbase = c * CE;
       uint4 raw[kVecPerThread];
       if (TMA) {
-        const int s = (int)(i % kStages);
-        mbar_wait(&pipe.full[s], (uint32_t)((i / kStages) & 1));
+        const int s = (int)(i % kVStages);
+        mbar_wait(&pipe.full[s], (uint32_t)((i / kVStages) & 1));
         const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
 #pragma unroll
         for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
@@ -467,7 +472,7 @@ cudaError_t mask_set_smem() {
 }
 
 size_t verify_smem_bytes(int T) {
-  return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(VerifyShared) + (size_t)3 * T * 4;
+  return (size_t)kVStages * kChunkBytes + sizeof(VPipe) + sizeof(VerifyShared) + (size_t)3 * T * 4;
 }
 
 template <bool BF16, bool TMA, bool SAMPLE>

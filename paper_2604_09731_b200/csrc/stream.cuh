@@ -61,10 +61,12 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
-struct StreamPipe {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+template <int S>
+struct StreamPipeT {
+  uint64_t full[S];
+  uint64_t empty[S];
 };
+using StreamPipe = StreamPipeT<kStages>;
 
 // smem layout of a streaming CTA: [ring kStages x 16 KiB][pipe][kernel-specific]
 struct RowRange {
@@ -91,15 +93,15 @@ __device__ __forceinline__ RowRange cta_range_min(int total, int min_units) {
 // Producer loop (one elected lane): stream chunks [lo, hi) of rows whose base pointer is given
 // by `row_base(row)`; each row is `row_bytes` long (16-byte multiple).  (row, chunk) advance
 // incrementally (no division per chunk).
-template <class RowBase>
-__device__ __forceinline__ void produce(StreamPipe& pipe, char* ring, RowRange rr, int cpr, long long row_bytes,
+template <int S, class RowBase>
+__device__ __forceinline__ void produce(StreamPipeT<S>& pipe, char* ring, RowRange rr, int cpr, long long row_bytes,
                                         RowBase row_base) {
   int row = rr.lo / cpr, c = rr.lo - row * cpr;
   const char* base = row_base(row);
   int i = 0;
   for (int q = rr.lo; q < rr.hi; ++q, ++i) {
-    const int s = i % kStages;
-    const uint32_t n = (uint32_t)(i / kStages);
+    const int s = i % S;
+    const uint32_t n = (uint32_t)(i / S);
     mbar_wait(&pipe.empty[s], (n & 1u) ^ 1u);
     const long long off = (long long)c * kChunkBytes;
     const uint32_t bytes = (uint32_t)min((long long)kChunkBytes, row_bytes - off);
