@@ -75,6 +75,8 @@ def lib():
         L.orc_step.argtypes = ([C.POINTER(_Cfg), pc, vp, i64, i64, vp, i64, vp, vp]
                                + [vp] * 8 + [vp] * 3 + [vp, i64, vp, vp, vp])
         L.orc_step.restype = C.c_int
+        L.orc_baseline_step.argtypes = [C.POINTER(_Cfg), vp, i64, vp, i64, vp, vp] + [vp] * 12
+        L.orc_baseline_step.restype = C.c_int
         L.orc_verify_sample.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, i64, vp, vp, vp,
                                         d, C.c_uint64, vp, vp, vp, vp]
         L.orc_verify_sample.restype = C.c_int
@@ -336,3 +338,48 @@ def verify_sample(target: np.ndarray, n_nodes, parent, tok, tau: float, seed: in
     if rc == 2:
         raise ValueError("invalid logits (NaN)")
     return out_a, out_p.reshape(b, D), out_b, mg
+
+
+def baseline_T(cfg: Config) -> int:
+    """tree capacity of the two-stage baseline: expanded nodes (1 + W d) and the final top-g tree."""
+    g = cfg.B_verify // cfg.b
+    return max(1 + g, 1 + cfg.W * max(cfg.d, 1))
+
+
+def baseline_step(cfg: Config, draft: np.ndarray, target: np.ndarray | None = None, root_tok=None, root_pos=None):
+    """NEXT #3 (Q32): the likelihood-maximising two-stage baseline (EAGLE-3 / MSD, Fig. 2(a)(b)).
+
+    draft/target: [b, T, ld] (T = baseline_T(cfg); draft rows at (r, expanded node), target rows at
+    (r, final node)).  cfg.W = nodes expanded per layer, cfg.k = children per node, g = B_verify // b.
+    Returns a StepResult (trace/candidates empty) with extra['n_exp'] = expanded nodes per request."""
+    b, d = cfg.b, cfg.d
+    T = baseline_T(cfg)
+    draft = np.ascontiguousarray(draft)
+    assert draft.shape[0] == b and draft.shape[1] == T, (draft.shape, b, T)
+    ld = draft.shape[-1]
+    if target is not None:
+        target = np.ascontiguousarray(target)
+        assert target.shape[:2] == (b, T)
+    MW = (T + 31) // 32
+    D = max(d, 1)
+    out = dict(n_nodes=np.zeros(b, np.int32), tok=np.zeros(b * T, np.int32), parent=np.zeros(b * T, np.int32),
+               depth=np.zeros(b * T, np.int32), pos=np.zeros(b * T, np.int32), p=np.zeros(b * T), cum=np.zeros(b * T),
+               mask=np.zeros(b * T * MW, np.uint32), accept_len=np.zeros(b, np.int32),
+               accept_path=np.full(b * D, -1, np.int32), bonus=np.zeros(b, np.int32), n_exp=np.zeros(b, np.int32))
+    rt = np.ascontiguousarray(root_tok if root_tok is not None else np.full(b, -1), np.int32)
+    rp = np.ascontiguousarray(root_pos if root_pos is not None else np.zeros(b), np.int32)
+    c_cfg = Config(**{**cfg.__dict__}).c()
+    c_cfg.T = T
+    rc = lib().orc_baseline_step(C.byref(c_cfg), _ptr(draft), ld, _ptr(target), target.shape[-1] if target is not None else 0,
+                                 _ptr(rt), _ptr(rp), *[_ptr(out[x]) for x in ("n_nodes", "tok", "parent", "depth", "pos",
+                                                                            "p", "cum", "mask", "accept_len",
+                                                                            "accept_path", "bonus", "n_exp")])
+    if rc == 1:
+        raise ValueError("invalid config")
+    if rc == 2:
+        raise ValueError("invalid logits")
+    return StepResult(n_nodes=out["n_nodes"], tok=out["tok"].reshape(b, T), parent=out["parent"].reshape(b, T),
+                      depth=out["depth"].reshape(b, T), pos=out["pos"].reshape(b, T), p=out["p"].reshape(b, T),
+                      cum=out["cum"].reshape(b, T), mask=out["mask"].reshape(b, T, MW), accept_len=out["accept_len"],
+                      accept_path=out["accept_path"].reshape(b, D), bonus=out["bonus"], trace=np.zeros((D, TRACE_F)),
+                      cand_i=None, cand_d=None, summary=np.zeros(SUM_F), T=T, extra=dict(n_exp=out["n_exp"]))

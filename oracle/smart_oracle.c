@@ -597,3 +597,165 @@ int orc_verify_sample(int dtype, int V, int T, int b, int r_off, int d, const vo
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT #3: the likelihood-maximising two-stage baseline (Q32)               */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+  int32_t layer, c, parent_e, tok, exp_node; /* exp_node: expanded-tree index, -1 if not expanded */
+  double p, cum;
+} bcand_t;
+
+/* rerank order: cum desc, layer asc, c asc */
+static int before_rerank(const bcand_t* a, const bcand_t* b) {
+  if (a->cum > b->cum) return 1;
+  if (a->cum < b->cum) return 0;
+  if (a->layer != b->layer) return a->layer < b->layer;
+  return a->c < b->c;
+}
+
+int orc_baseline_step(const orc_config* cfg, const void* draft, int64_t ld, const void* target, int64_t ld_t,
+                      const int32_t* root_tok, const int32_t* root_pos, int32_t* n_nodes, int32_t* tok,
+                      int32_t* parent, int32_t* depth, int32_t* pos, double* p, double* cum, uint32_t* mask,
+                      int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int32_t* n_exp) {
+  const int b = cfg->b, k = cfg->k, d = cfg->d, T = cfg->T, V = cfg->V, w = cfg->W;
+  const int esz = cfg->dtype == ORC_BF16 ? 2 : 4;
+  const int MW = (T + 31) / 32;
+  const int D = d > 0 ? d : 1;
+  if (b < 1 || k < 1 || k > V || d < 0 || T < 1 || w < 1) return 1;
+  const int64_t g = cfg->B_verify / b;
+  if (g < 1 || T < 1 + g) return 1;
+  const int64_t cap = (int64_t)(d > 0 ? d : 1) * w * k + 1;
+  bcand_t* all = malloc(sizeof(bcand_t) * cap);
+  bcand_t** ord = malloc(sizeof(bcand_t*) * cap);
+  int32_t* topi = malloc(sizeof(int32_t) * k);
+  double* topp = malloc(sizeof(double) * k);
+  /* expanded tree (per request): cum and the candidate it came from */
+  const int64_t te = 1 + (int64_t)w * (d > 0 ? d : 1);
+  double* ecum = malloc(sizeof(double) * te);
+  int32_t* efront = malloc(sizeof(int32_t) * te);
+  int32_t* newidx = malloc(sizeof(int32_t) * te);
+  int rc = 0;
+  for (int r = 0; r < b; r++) {
+    int64_t na = 0;
+    int32_t ne = 1, nf = 1;
+    ecum[0] = 1.0;
+    efront[0] = 0;
+    for (int l = 1; l <= d && nf > 0; l++) {
+      const int64_t l0 = na;
+      for (int i = 0; i < nf; i++) {
+        const int32_t u = efront[i];
+        const char* row = (const char*)draft + ((int64_t)r * T + u) * ld * esz;
+        rc = orc_topk_softmax(row, cfg->dtype, V, k, topi, topp, NULL, NULL);
+        if (rc) goto done;
+        for (int j = 0; j < k; j++) {
+          bcand_t* c = &all[na++];
+          c->layer = l;
+          c->c = i * k + j;
+          c->parent_e = u;
+          c->tok = topi[j];
+          c->p = topp[j];
+          c->cum = ecum[u] * topp[j]; /* Eq.(3) */
+          c->exp_node = -1;
+        }
+      }
+      /* the layer's top-w by (cum desc, c asc) are expanded next */
+      const int64_t nl = na - l0;
+      for (int64_t q = 0; q < nl; q++) ord[q] = &all[l0 + q];
+      for (int64_t x = 1; x < nl; x++) { /* insertion sort: cum desc, c asc */
+        bcand_t* y = ord[x];
+        int64_t z;
+        for (z = x; z > 0 && (y->cum > ord[z - 1]->cum || (y->cum == ord[z - 1]->cum && y->c < ord[z - 1]->c)); z--)
+          ord[z] = ord[z - 1];
+        ord[z] = y;
+      }
+      const int64_t take = nl < w ? nl : w;
+      /* commit in canonical (c asc) order */
+      nf = 0;
+      for (int64_t q = 0; q < nl; q++) {
+        bcand_t* c = &all[l0 + q];
+        int sel = 0;
+        for (int64_t z = 0; z < take; z++) sel |= (ord[z] == c);
+        if (!sel) continue;
+        c->exp_node = ne;
+        ecum[ne] = c->cum;
+        efront[nf++] = ne;
+        ne++;
+      }
+    }
+    n_exp[r] = ne;
+    /* rerank: top-g of all generated candidates */
+    for (int64_t q = 0; q < na; q++) ord[q] = &all[q];
+    for (int64_t x = 1; x < na; x++) {
+      bcand_t* y = ord[x];
+      int64_t z;
+      for (z = x; z > 0 && before_rerank(y, ord[z - 1]); z--) ord[z] = ord[z - 1];
+      ord[z] = y;
+    }
+    const int64_t keep = na < g ? na : g;
+    /* final numbering in (layer, c) order = the order of `all` */
+    for (int64_t e = 0; e < te; e++) newidx[e] = -1;
+    newidx[0] = 0;
+    int32_t nn = 1;
+    const int64_t o = (int64_t)r * T;
+    tok[o] = root_tok ? root_tok[r] : -1;
+    parent[o] = -1;
+    depth[o] = 0;
+    p[o] = 1.0;
+    cum[o] = 1.0;
+    for (int64_t q = 0; q < na; q++) {
+      bcand_t* c = &all[q];
+      int kept = 0;
+      for (int64_t z = 0; z < keep; z++) kept |= (ord[z] == c);
+      if (!kept) continue;
+      if (newidx[c->parent_e] < 0) { rc = 1; goto done; } /* closure violated (cannot happen) */
+      tok[o + nn] = c->tok;
+      parent[o + nn] = newidx[c->parent_e];
+      depth[o + nn] = c->layer;
+      p[o + nn] = c->p;
+      cum[o + nn] = c->cum;
+      if (c->exp_node >= 0) newidx[c->exp_node] = nn;
+      nn++;
+    }
+    n_nodes[r] = nn;
+    /* A7: mask rows and positions (padding rows zero) */
+    for (int32_t i = 0; i < T; i++) {
+      uint32_t* mrow = mask + (o + i) * MW;
+      for (int ww = 0; ww < MW; ww++) mrow[ww] = 0u;
+      if (i >= nn) {
+        pos[o + i] = 0;
+        if (i > 0) { tok[o + i] = -1; parent[o + i] = -1; depth[o + i] = 0; }
+        continue;
+      }
+      for (int32_t j = i; j >= 0; j = parent[o + j]) mrow[j / 32] |= 1u << (j % 32);
+      pos[o + i] = (root_pos ? root_pos[r] : 0) + depth[o + i];
+    }
+    /* A8: greedy walk */
+    accept_len[r] = 0;
+    for (int i = 0; i < D; i++) accept_path[r * D + i] = -1;
+    bonus[r] = -1;
+    if (!target) continue;
+    int32_t cur = 0;
+    for (;;) {
+      const char* row = (const char*)target + (o + cur) * ld_t * esz;
+      int64_t best = -1;
+      double bx = 0.0;
+      for (int64_t v = 0; v < V; v++) {
+        const double x = logit_at(row, cfg->dtype, v);
+        if (isnan(x)) { rc = 2; goto done; }
+        if (best < 0 || better_xi(x, v, bx, best)) { best = v; bx = x; }
+      }
+      int32_t next = -1;
+      for (int32_t j = cur + 1; j < nn; j++)
+        if (parent[o + j] == cur && tok[o + j] == best) { next = j; break; }
+      if (next < 0) { bonus[r] = (int32_t)best; break; }
+      if (accept_len[r] < D) accept_path[r * D + accept_len[r]] = next;
+      accept_len[r]++;
+      cur = next;
+    }
+  }
+done:
+  free(all); free(ord); free(topi); free(topp); free(ecum); free(efront); free(newidx);
+  return rc;
+}

@@ -90,6 +90,23 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
              /* summary [ORC_SUM_F] */
              double* summary);
 
+/* NEXT #3 (reading Q32): the likelihood-maximising two-stage baseline of EAGLE-3 / MSD
+ * (Fig. 2(a)(b)), per request r:
+ *  expand: for l = 1..d, every frontier node (layer l-1, canonical order; A_0 = {root}) gets
+ *          its top-k children (A1/A2 as orc_step); the top-w candidates of the layer by
+ *          (cum desc, c asc) are committed as expanded nodes (node indices in canonical c order)
+ *          and form the next frontier (w = cfg->W, the "global top-k nodes"; Fig. 2: w = k = 2);
+ *  rerank: all generated candidates are reranked by (cum desc, layer asc, c asc) and the top
+ *          g = floor(B_verify / b) kept (cum never increases along a path, so the kept set is
+ *          ancestor-closed by construction); the final tree numbers them in (layer, c) order.
+ * Draft rows: NODE layout at (r, expanded node).  Outputs: the final tree, its mask/pos (A7)
+ * and the greedy walk (A8, target rows at (r, final node)); n_exp[r] = expanded nodes incl.
+ * the root.  Returns 0, 1 bad config, 2 invalid logits. */
+int orc_baseline_step(const orc_config* cfg, const void* draft, int64_t ld, const void* target, int64_t ld_t,
+                      const int32_t* root_tok, const int32_t* root_pos, int32_t* n_nodes, int32_t* tok,
+                      int32_t* parent, int32_t* depth, int32_t* pos, double* p, double* cum, uint32_t* mask,
+                      int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int32_t* n_exp);
+
 /* NEXT #1 (reading Q31): tree verification at temperature tau > 0.  Walk from the root of each
  * request: at node u draw the target token by Gumbel-max over the target row,
  *   x* = argmax_v ( logit_v / tau + G_v ),  G_v = -log(-log(U_v)),
