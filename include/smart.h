@@ -55,7 +55,12 @@ typedef enum {
 } smart_status;
 
 typedef enum { SMART_BF16 = 0, SMART_FP32 = 1 } smart_dtype;
-typedef enum { SMART_PREFIX = 0, SMART_FROZEN = 1 } smart_selection;          /* Q7  */
+/* PREFIX / FROZEN: SMART's rule (Q7).  BASELINE (NEXT #3, Q32): the likelihood-maximising
+ * two-stage policy of EAGLE-3 / MSD (Fig. 2(a)(b)): every layer expands the request's top-
+ * max_frontier candidates by cum (no cost model); smart_build_mask first reranks all generated
+ * candidates and keeps the top floor(budget_verify / batch) by cum (ancestor-closed by
+ * construction).  BASELINE needs max_frontier >= 1 and a single rank (batch_local == batch_global). */
+typedef enum { SMART_PREFIX = 0, SMART_FROZEN = 1, SMART_BASELINE = 2 } smart_selection;
 typedef enum { SMART_NODE_SUM = 0, SMART_PATH_MEAN = 1 } smart_accept_model;  /* Q11 */
 typedef enum { SMART_DERIVATIVE = 0, SMART_DIFFERENCE = 1 } smart_marginal;   /* Q5  */
 typedef enum { SMART_COST_GLOBAL = 0, SMART_COST_LOCAL = 1 } smart_cost_scope;/* Q13 */
@@ -90,6 +95,7 @@ typedef struct {
   int32_t logits_dtype;   /* smart_dtype (draft and target logits)                          */
   int32_t row_mode;       /* smart_row_mode                                                 */
   int32_t tree_capacity;  /* T: nodes per request incl. root; 0 = 1 + min(B, d*W)           */
+                          /* (BASELINE: 0 = 1 + max(B, d*W))                                */
 } smart_config;
 
 typedef struct smart_ctx smart_ctx;

@@ -97,7 +97,16 @@ struct NcclApi {
 long long derive_T(const smart_config* c, int B) {
   long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
   long long t = 1 + std::min<long long>(B, (long long)c->max_depth * Wq);
+  if (c->selection == SMART_BASELINE)  // expanded nodes (W per layer) and the final top-B tree
+    t = 1 + std::max<long long>(B, (long long)std::max(c->max_depth, 1) * c->max_frontier);
   return c->tree_capacity > 0 ? c->tree_capacity : t;
+}
+
+// frontier rows per request per layer: SMART caps them by W and the budget, BASELINE by W only
+static long long frontier_width(const smart_config* c, long long B, long long T) {
+  long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
+  if (c->selection == SMART_BASELINE) return std::max<long long>(1, std::min<long long>(Wq, T - 1));
+  return std::max<long long>(1, std::min<long long>(Wq, std::min<long long>(B, T - 1)));
 }
 
 smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s, std::string& why) {
@@ -116,7 +125,9 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
   if (c->batch_local > 4096) return bad("batch_local > 4096");
   if (!(c->alpha > 0.0 && c->alpha <= 1.0)) return bad("alpha must be in (0, 1]");
   if (c->bonus != 0 && c->bonus != 1) return bad("bonus must be 0 or 1");
-  if (c->selection < 0 || c->selection > 1 || c->accept_model < 0 || c->accept_model > 1 || c->marginal < 0 ||
+  if (c->selection == SMART_BASELINE && (c->max_frontier < 1 || c->batch_local != c->batch_global))
+    return bad("BASELINE needs max_frontier >= 1 and a single rank");
+  if (c->selection < 0 || c->selection > 2 || c->accept_model < 0 || c->accept_model > 1 || c->marginal < 0 ||
       c->marginal > 1 || c->cost_scope < 0 || c->cost_scope > 1 || c->logits_dtype < 0 || c->logits_dtype > 1 ||
       c->row_mode < 0 || c->row_mode > 1)
     return bad("enum field out of range");
@@ -130,8 +141,12 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
   }
   long long T = derive_T(c, B);
   if (T < 1 || T > 1024) return bad("tree capacity T must be in [1, 1024]");
-  long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
-  long long wf = std::max<long long>(1, std::min<long long>(Wq, std::min<long long>(B, T - 1)));
+  long long wf = frontier_width(c, B, T);
+  if (c->selection == SMART_BASELINE && T < 1 + std::max<long long>(B, (long long)std::max(c->max_depth, 1) * c->max_frontier))
+    return bad("BASELINE tree capacity must hold 1 + max(B, d * W) nodes");
+  if (c->selection == SMART_BASELINE &&
+      (long long)std::max(c->max_depth, 1) * wf * c->top_k * 16 + T * 4 > 200 * 1024)
+    return bad("BASELINE rerank: d * W * k candidates per request exceed shared memory");
   long long cap_rows = (long long)c->batch_local * wf;
   if (cap_rows * c->top_k > 65536ll * 8) return bad("frontier capacity too large");
   if (wf * c->top_k > 65535) return bad("candidates per request exceed 16-bit index");
@@ -275,6 +290,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.cand, d * cap * k * sizeof(Cand));
   add(&P.cand_b, d * cap * k * 4);
   add(&P.cand_adm, d * cap * k * 4);
+  add(&P.cand_node, d * cap * k * 4);
   add(&P.cand_rs, d * cap * 8);
   add(&P.trace, SMART_MAX_DEPTH * sizeof(DevTrace));
   add(&P.err, 4);
@@ -352,7 +368,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   c->grid_verify = c->num_sms * verify_occupancy();
   // selection: fused into the layer kernel when its scratch fits the stream ring, else the
   // standalone 1024-thread select kernel
-  long long elig_cap = b * std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, T - 1)));
+  long long elig_cap = b * frontier_width(&c->cfg, P.B, T);
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
   P.sort_cap = sort_cap;
   c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1, (int)k);
@@ -367,6 +383,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     fprintf(stderr, "[smart] grid_expand %d (layer smem %zu B) grid_verify %d select_smem %zu B fused %d\n",
             c->grid_expand, layer_smem_bytes(P.cpr, P.k), c->grid_verify, c->select_smem, (int)c->fused_select);
   mask_set_smem();
+  if (P.selection == SMART_BASELINE) rerank_set_smem(rerank_smem_bytes(P));
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {
     cudaFree(c->ws);
@@ -404,7 +421,7 @@ static smart_status setup_exchange(smart_ctx* c, int rank, int nranks, void* sen
   P.nranks = nranks;
   P.rank = rank;
   const long long b = P.b_loc;
-  const long long wf = std::max<long long>(1, std::min<long long>(P.Wq, std::min<long long>(P.B, P.T - 1)));
+  const long long wf = frontier_width(&c->cfg, P.B, P.T);
   P.m_cap = (int)(b * wf);
   P.xstride = exchange_record_bytes(b, wf);
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -579,6 +596,7 @@ smart_status smart_build_mask(smart_ctx* c, uint32_t* d_mask, int32_t* d_pos, in
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
   if (c->next_layer == 0 || c->phase != 0) return fail(c, SMART_ESTATE, "build_mask needs a begun step between layers");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P.selection == SMART_BASELINE) launch_rerank(c->P, s);  // stage 2 of the baseline (Q32)
   launch_mask(c->P, d_mask, d_pos, d_parent, d_tok, d_tree_len, s);
   CUDA_TRY(c, cudaGetLastError());
   c->masked = true;

@@ -461,6 +461,96 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
 
 }  // namespace
 
+// ---- NEXT #3 stage 2: rerank of the two-stage likelihood-maximising baseline (Q32) ----------
+// EAGLE-3 / MSD (Fig. 2(a)(b)): the expansion stage (select_layer in BASELINE mode) kept the
+// top-W candidates of every layer by (cum desc, c asc); here every candidate generated in the step
+// (admitted or not) competes for the g = floor(B_verify / b) verification slots by (cum desc,
+// layer asc, c asc), and the kept set is renumbered in (layer, c) order.  A kept candidate's parent
+// has a larger-or-equal cum at a lower layer, so it ranks earlier and is kept too (closure).
+// One CTA per request; keys (~bits(cum) << 32 | layer << 16 | c) rank in O(n^2) shared-memory
+// counting (n <= d W k candidates).
+constexpr int kRerankThreads = 256;
+
+__global__ void __launch_bounds__(kRerankThreads) rerank_kernel(Params P) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int nmax = max(P.d, 1) * P.Wq * P.k;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(sm);
+  int* qi = reinterpret_cast<int*>(key + nmax);
+  int* fpos = qi + nmax;
+  int* newidx = fpos + nmax;
+  __shared__ int cnt;
+  const int r = blockIdx.x, tid = threadIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) cnt = 0;
+  for (int i = tid; i < P.T; i += kRerankThreads) newidx[i] = i == 0 ? 0 : -1;
+  __syncthreads();
+  for (int l = 1; l <= P.d; ++l) {
+    const DevTrace& tr = P.trace[l - 1];
+    const int R = tr.executed ? tr.n_rows : 0;
+    for (int row = tid; row < R; row += kRerankThreads) {
+      const int2 rs = __ldcg(&P.cand_rs[(size_t)(l - 1) * P.cap_rows + row]);
+      if (rs.x != r) continue;
+      const int s = atomicAdd(&cnt, P.k);
+      const size_t q0 = (size_t)(l - 1) * P.cap_rows * P.k + (size_t)row * P.k;
+      for (int j = 0; j < P.k; ++j) {
+        const float c = __ldcg(&P.cand[q0 + j].cum);
+        key[s + j] = ((unsigned long long)(~__float_as_uint(c)) << 32) |
+                     ((unsigned long long)l << 16) | (unsigned)(rs.y * P.k + j);
+        qi[s + j] = (int)(q0 + j);
+      }
+    }
+  }
+  __syncthreads();
+  const int n = cnt;
+  const int keep = min(n, P.B);
+  // rank by (cum desc, layer asc, c asc); kept if rank < g
+  for (int i = tid; i < n; i += kRerankThreads) {
+    const unsigned long long ki = key[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += key[j] < ki;
+    fpos[i] = rank < keep ? 0 : -1;
+  }
+  __syncthreads();
+  // final index: 1 + kept candidates before it in (layer, c) order; expanded ones map their node
+  for (int i = tid; i < n; i += kRerankThreads) {
+    if (fpos[i] < 0) continue;
+    const unsigned lo = (unsigned)key[i];
+    int pos = 1;
+    for (int j = 0; j < n; ++j) pos += (fpos[j] >= 0) && ((unsigned)key[j] < lo);
+    fpos[i] = pos;
+    const int q = qi[i];
+    if (__ldcg(&P.cand_adm[q])) newidx[__ldcg(&P.cand_node[q])] = pos;
+  }
+  __syncthreads();
+  const size_t o = (size_t)r * P.T;
+  for (int i = tid; i < n; i += kRerankThreads) {
+    const int pos = fpos[i];
+    if (pos < 0) continue;
+    const Cand cd = P.cand[qi[i]];
+    const int par = newidx[cd.parent];
+    if (par < 0) atomicExch(P.err, 1);  // closure violated (cannot happen)
+    P.tok[o + pos] = cd.tok;
+    P.parent[o + pos] = par;
+    P.depth[o + pos] = (int)((key[i] >> 16) & 0xffffu);
+    P.p[o + pos] = cd.p;
+    P.cum[o + pos] = cd.cum;
+  }
+  if (tid == 0) P.n_nodes[r] = 1 + keep;
+}
+
+size_t rerank_smem_bytes(const Params& P) {
+  return (size_t)std::max(P.d, 1) * P.Wq * P.k * 16 + (size_t)P.T * 4;
+}
+
+cudaError_t rerank_set_smem(size_t bytes) {
+  return cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_rerank(const Params& P, cudaStream_t s) {
+  launch_k(rerank_kernel, dim3(P.b_loc), dim3(kRerankThreads), rerank_smem_bytes(P), s, P);
+}
+
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok, int32_t* tree_len,
                  cudaStream_t s) {
   const size_t smem = (size_t)32 * 3 * P.T * sizeof(int);

@@ -372,7 +372,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   const int k = P.k, bl = P.b_loc;
   const int b_all = (mode == kSelGlobal) ? P.b_glob : bl;
   const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
-  const bool pmean = (P.accept_model == SMART_PATH_MEAN);
+  const bool base = (P.selection == SMART_BASELINE);  // NEXT #3 two-stage baseline (Q32)
+  const bool pmean = (P.accept_model == SMART_PATH_MEAN) && !base;
   DevTrace& tr = P.trace[layer - 1];
   const int R = *P.fr_total[par];
   const int nct = R * k;  // candidates of this layer (local)
@@ -419,7 +420,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   if (warp == 0) {
     long long nl = 0;
     for (int r = lane; r < bl; r += 32) {
-      int q = P.B - L.nd[r];
+      int q = base ? P.Wq : P.B - L.nd[r];  // the baseline expands W per layer, no budget
       if (q > P.Wq) q = P.Wq;
       if (q < 0) q = 0;
       L.base[r] = min(q, L.cnt[r] * k);
@@ -472,8 +473,10 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   stamp(P, tid == 0, 11);
 
   // ---- A4: sort (local list, or the gathered lists of all ranks) ----
-  const int nsort = (mode == kSelGlobal) ? P.nranks * P.m_cap : ne;
-  if (nsort <= 1024) {
+  const int nsort = base ? 0 : (mode == kSelGlobal) ? P.nranks * P.m_cap : ne;
+  if (base) {
+    // the baseline admits every eligible candidate: no global order, no rule (Q32)
+  } else if (nsort <= 1024) {
     // rank sort (keys unique; padding ~0 keys sort to the end); two keys per shared load
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(L.keys);
     for (int i = tid; i < nsort; i += NT) {
@@ -562,7 +565,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   }
   // long lists (>= 512 eligible): 8 warps, group-contiguous then lane-contiguous chunks; short
   // lists: warp 0 alone.  Either way the fp64 association is a function of ne only.
-  const bool big = ne >= 512;
+  const bool big = !base && ne >= 512;
   auto rule_ok = [&](double bj, double before, int j) {
     // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
     // cost == 0 means S := 0, i.e. admit any positive benefit)
@@ -638,6 +641,13 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       ss.bcast_i[3] = js0;
       ss.bcast_i[5] = ne;
       ss.bcast_i[6] = bj;  // argmax_j, reported by warp 1 in the tail
+      ss.bcast_l[0] = N0;
+    }
+  } else if (base) {
+    if (tid == 0) {
+      ss.bcast_i[3] = ne;  // all eligible admitted
+      ss.bcast_i[5] = ne;
+      ss.bcast_i[6] = 0;
       ss.bcast_l[0] = N0;
     }
   } else if (warp == 0) {
@@ -721,6 +731,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const int idx = bits_below(r, c);
     const int node = L.nd[r] + 1 + idx;
     const size_t o = (size_t)r * P.T + node;
+    P.cand_node[lbase + q] = node;
     P.tok[o] = cd.tok;
     P.parent[o] = cd.parent;
     P.depth[o] = layer;
@@ -751,7 +762,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     int a = 0;
     for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
     L.adm[r] = a;
-    const bool fin = L.fin[r] || a == 0 || L.nd[r] + a >= P.B;  // Alg.1 line 10
+    const bool fin = L.fin[r] || a == 0 || (!base && L.nd[r] + a >= P.B);  // Alg.1 line 10
     L.nxt[r] = fin ? 0 : a;
     L.base[r] = fin ? 0 : a;
     P.fr_cnt[npar][r] = fin ? 0 : a;
@@ -891,7 +902,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       tr.n_cand = nct;
       tr.n_elig = ne_r;
       tr.n_admit = js;
-      tr.argmax_j = argmax_pre >= 0 ? argmax_pre : bestj;
+      tr.argmax_j = base ? 0 : argmax_pre >= 0 ? argmax_pre : bestj;
       tr.N0 = (int)N0r;
       tr.E0 = E0;
       tr.S0 = Sb0 / bc;

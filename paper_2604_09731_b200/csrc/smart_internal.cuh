@@ -88,6 +88,7 @@ struct Params {
   Cand* cand;         // [d][cap_rows*k]
   float* cand_b;      // [d][cap_rows*k] benefit
   int* cand_adm;      // [d][cap_rows*k] admitted flag
+  int* cand_node;     // [d][cap_rows*k] node index of an admitted candidate (BASELINE rerank)
   int2* cand_rs;      // [d][cap_rows] (local request, frontier slot) of each candidate row
 
   // ---- cost model tables (fp64, host-built with the same formula; N in [0, n_cost)) ----
@@ -309,6 +310,9 @@ int expand_grid(int cpr, int k);
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
 size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks, int k);
 cudaError_t select_set_smem(size_t bytes);
+void launch_rerank(const Params& P, cudaStream_t s);
+cudaError_t rerank_set_smem(size_t bytes);
+size_t rerank_smem_bytes(const Params& P);
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok,
                  int32_t* tree_len, cudaStream_t s);
 void launch_verify(const Params& P, const void* target, long long ld_bytes, bool tma,

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(PKG, "libsmart.so")
 
 OK, EINVAL, ECUDA, ENCCL, ECAPACITY, EDEVICE, ESTATE = range(7)
 BF16, FP32 = 0, 1
-PREFIX, FROZEN = 0, 1
+PREFIX, FROZEN, BASELINE = 0, 1, 2  # BASELINE: two-stage likelihood-maximising tree (Q32)
 NODE_SUM, PATH_MEAN = 0, 1
 DERIVATIVE, DIFFERENCE = 0, 1
 COST_GLOBAL, COST_LOCAL = 0, 1

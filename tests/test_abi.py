@@ -51,9 +51,27 @@ def test_query_sizes(sm):
     assert sm.query_sizes(cfg2)["T"] == 61 and sm.query_sizes(cfg2)["mask_words"] == 2
 
 
+def test_query_sizes_baseline(sm):
+    """NEXT #3 (Q32): the baseline pool holds the expanded tree (1 + W d) and the final top-g tree."""
+    from oracle import oracle as O
+    for (V, k, d, W, b, Bv) in ((128256, 10, 6, 10, 1, 60), (32001, 8, 5, 16, 32, 2048), (2000, 3, 2, 2, 2, 200)):
+        cfg = sm.Config(vocab=V, top_k=k, max_depth=d, max_frontier=W, batch_local=b, budget_verify=Bv,
+                        selection=sm.BASELINE)
+        s = sm.query_sizes(cfg)
+        assert s["T"] == O.baseline_T(O.Config(V=V, k=k, d=d, W=W, b=b, B_verify=Bv))
+        assert s["frontier_cap"] == b * W
+    bad = [dict(max_frontier=0, batch_local=2),                       # no expansion width
+           dict(max_frontier=4, batch_local=1, batch_global=2),      # multi-rank
+           dict(max_frontier=4, batch_local=2, tree_capacity=8)]     # pool below 1 + d W
+    for kw in bad:
+        cfg = sm.Config(vocab=1000, top_k=4, max_depth=3, budget_verify=40, selection=sm.BASELINE, **kw)
+        with pytest.raises(sm.SmartError):
+            sm.query_sizes(cfg)
+
+
 @pytest.mark.parametrize("field,value", [("top_k", 0), ("top_k", 33), ("max_depth", 17), ("alpha", 0.0),
                                          ("alpha", 1.5), ("budget_verify", 0), ("vocab", 1),
-                                         ("selection", 2), ("bonus", 2)])
+                                         ("selection", 3), ("bonus", 2)])
 def test_validation_rejects(sm, field, value):
     cfg = sm.Config(vocab=1000, top_k=4, max_depth=4, batch_local=2, budget_verify=16)
     setattr(cfg, field, value)
