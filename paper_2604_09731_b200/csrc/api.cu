@@ -34,6 +34,7 @@ struct smart_ctx {
   int grid_expand = 0, grid_verify = 0;
   size_t select_smem = 0;
   bool fused_select = true;  // selection runs in the layer kernel's last CTA
+  bool no_early = false;     // SMART_NO_EARLY=1: every layer kernel waits for the previous grid
   double* cost_dev = nullptr;
   Params P{};
   void* ws = nullptr;      // single device allocation
@@ -286,6 +287,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.seglen, cap * cpr * 4);
   add(&P.row_done, rd * 4);
   add(&P.layer_done, SMART_MAX_DEPTH * 4);
+  add(&P.fr_ready, (SMART_MAX_DEPTH + 1) * 4);
   add(&P.rowstat, cap * 8);
   add(&P.cand, d * cap * k * sizeof(Cand));
   add(&P.cand_b, d * cap * k * 4);
@@ -359,6 +361,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   P.min_units = getenv("SMART_MIN_UNITS") ? atoi(getenv("SMART_MIN_UNITS")) : 2;
   if (P.min_units < 1) P.min_units = 1;
   P.debug_mode = getenv("SMART_DEBUG_MODE") ? atoi(getenv("SMART_DEBUG_MODE")) : 0;
+  c->no_early = getenv("SMART_NO_EARLY") != nullptr;
   if (getenv("SMART_TIMING")) {
     e = cudaMalloc(&P.dbg, 1024 * sizeof(unsigned long long));
     if (e != cudaSuccess) P.dbg = nullptr;
@@ -372,6 +375,14 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   int sort_cap = next_pow2(std::max<long long>(elig_cap, 1));
   P.sort_cap = sort_cap;
   c->select_smem = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1, (int)k);
+  {
+    // stage the candidate records in the selection's scratch when it still fits the ring (fused)
+    // or the standalone kernel's limit
+    const size_t rec = select_rec_bytes((int)(cap * k));
+    const size_t lim = c->select_smem <= (size_t)kStages * kChunkBytes ? (size_t)kStages * kChunkBytes : 220 * 1024;
+    P.sel_rec = (c->select_smem + rec <= lim) ? 1 : 0;
+    if (P.sel_rec) c->select_smem += rec;
+  }
   c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && c->grid_expand >= 16 && !getenv("SMART_NO_FUSE");
   if (c->select_smem > 220 * 1024) {
     cudaFree(c->ws);
@@ -441,7 +452,10 @@ static smart_status setup_exchange(smart_ctx* c, int rank, int nranks, void* sen
   CUDA_TRY(c, cudaMemset(P.xs, 0, P.xstride));
   const int sort_cap = next_pow2((long long)P.m_cap * nranks);
   P.sort_cap = sort_cap;
-  const size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks, P.k);
+  size_t need = select_smem_bytes((int)b, (int)P.b_glob, sort_cap, P.cap_rows * P.k, nranks, P.k);
+  const size_t rec = select_rec_bytes(P.cap_rows * P.k);
+  P.sel_rec = (need + rec <= 220 * 1024) ? 1 : 0;
+  if (P.sel_rec) need += rec;
   if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
   c->select_smem = std::max(c->select_smem, need);
   c->fused_select = false;
@@ -537,7 +551,9 @@ smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits
   // TMA bulk copies need 16-byte aligned rows and 16-byte multiple row lengths
   const bool tma = ((reinterpret_cast<uintptr_t>(d_logits) & 15) == 0) && (ld_bytes % 16 == 0) &&
                    (((long long)c->P.V * c->P.esz) % 16 == 0);
-  launch_expand(c->P, layer, d_logits, ld_bytes, tma, c->fused_select, c->grid_expand, s);
+  // early start: the previous layer's fused selection publishes its frontier before its kernel ends
+  const bool early = layer >= 2 && c->fused_select && c->P.nranks <= 1 && !c->no_early;
+  launch_expand(c->P, layer, d_logits, ld_bytes, tma, c->fused_select, early, c->grid_expand, s);
   CUDA_TRY(c, cudaGetLastError());
   c->phase = 1;
   c->last_stream = s;

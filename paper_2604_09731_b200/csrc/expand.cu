@@ -212,8 +212,10 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
 // row's k-th best key from below); the entries >= T are ranked among themselves and the top k
 // written with p (A1) and cum (A2, Eq.(3)).
 __device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int slot, int t,
-                               const float2* ms, const unsigned long long* lists, unsigned long long* surv) {
+                               const float2* ms, const unsigned long long* lists, unsigned long long* surv,
+                               bool pr) {
   const int lane = threadIdx.x & 31;
+  stamp(P, pr, 1);
   const int k = P.k, cpr = P.cpr;
   const int npart = cpr * kConsumerWarps;  // <= 512
   // (1) softmax normaliser
@@ -227,6 +229,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
     if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
   }
   const float Z = warp_sum(z);
+  stamp(P, pr, 2);
   // (2) threshold: best tail over the members' lists
   const int kp = list_stride(k);
   const unsigned long long tail = lane < t ? lists[lane * kp + k - 1] : 0ull;
@@ -245,6 +248,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
     ns += __popc(bal);
   }
   __syncwarp();
+  stamp(P, pr, 3);
   // (4) exact top-k among the survivors; A1 p and A2 cum
   for (int s0 = lane; s0 < ns; s0 += 32) {
     const unsigned long long key = surv[s0];
@@ -267,6 +271,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
       P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
     }
   }
+  stamp(P, pr, 4);
   if (lane == 0) {
     P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, slot);
     P.rowstat[row] = make_float2(M, Z);
@@ -277,7 +282,14 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
 
 template <bool BF16, bool TMA>
 __global__ void __launch_bounds__(kLayerThreadsT, 2)
-layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_bytes, int fuse_select) {
+layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_bytes, int flags) {
+  // flags bit 0: the layer's selection is fused (the grid's last cluster); bit 1: early start —
+  // the previous layer's selection was fused and publishes its frontier with a release flag
+  // (P.fr_ready[layer - 1]) before its kernel ends, so streaming CTAs wait on that flag instead of
+  // the previous grid's completion (the select CTA still waits for the completion: it reads the
+  // per-request state the previous selection writes after the frontier)
+  const int fuse_select = flags & 1;
+  const bool early = (flags & 2) != 0;
   constexpr int EPT = Traits<BF16>::EPT;
   constexpr int EPV = Traits<BF16>::EPV;
   extern __shared__ __align__(128) char dsm[];
@@ -303,8 +315,13 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   cluster_sync_all();  // barriers initialised cluster-wide before any remote arrive
   tl_start(P, 32 + layer);
   if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA start (debug)
-  pdl_wait();
+  const bool sel_cta0 = fuse_select && (int)blockIdx.x == (int)gridDim.x - kCluster;
+  if (!early || sel_cta0) pdl_wait();
   pdl_trigger();
+  if (early && !sel_cta0) {
+    if (tid == 0) wait_flag(&P.fr_ready[layer - 1]);
+    __syncthreads();
+  }
   tl_start(P, layer);
   // the first row's frontier entry for each possible team size t = 8 >> tid, fetched together
   // with the row count (the team layout is only known once R is)
@@ -313,16 +330,19 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   if (tid < 4) {
     const int row = (int)blockIdx.x / (kCluster >> tid);
     if (row < P.cap_rows) {
-      sfe = P.fr[par][row];
-      scum = P.fr_cum[par][row];
+      sfe = __ldcg(&P.fr[par][row]);
+      scum = __ldcg(&P.fr_cum[par][row]);
     }
   }
-  const int R = *P.fr_total[par];
+  const int R = __ldcg(P.fr_total[par]);
   const bool t0 = (blockIdx.x == 0 && tid == 0);
   gstamp(P, t0, 16);
   if (R == 0) {
     // A_{l-1} is empty for every request: the step has terminated at this layer
-    if (fuse_select && blockIdx.x == 0 && tid == 0) *P.fr_total[layer & 1] = 0;
+    if (fuse_select && blockIdx.x == 0 && tid == 0) {
+      *P.fr_total[layer & 1] = 0;
+      publish_flag(&P.fr_ready[layer]);
+    }
     return;  // no remote traffic in this launch: early exit is safe
   }
   const int k = P.k, cpr = P.cpr, CE = P.chunk_elems, V = P.V;
@@ -347,12 +367,12 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   if (tid >= 4 && tid - 3 < nstage) {  // further rows (large layers)
     const int n = tid - 3;
     const int row = team + n * nteams;
-    sh.rfe[n] = P.fr[par][row];
-    sh.rcum[n] = P.fr_cum[par][row];
+    sh.rfe[n] = __ldcg(&P.fr[par][row]);
+    sh.rcum[n] = __ldcg(&P.fr_cum[par][row]);
   }
   __syncthreads();
   gstamp(P, t0, 17);
-  auto rowfe = [&](int n, int row) { return n < kStageRows ? sh.rfe[n] : P.fr[par][row]; };
+  auto rowfe = [&](int n, int row) { return n < kStageRows ? sh.rfe[n] : __ldcg(&P.fr[par][row]); };
   auto rowp = [&](int n, int row) -> const char* {
     if (P.row_mode == SMART_ROWS_NODE) {
       const int2 fe = rowfe(n, row);
@@ -385,17 +405,20 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         const int row = team + n * nteams;
         const int b = n & 1;
         const int2 fe = rowfe(n, row);
-        const float pc = n < kStageRows ? sh.rcum[n] : P.fr_cum[par][row];
-        const int slot = row - P.fr_off[par][fe.x];  // frontier slot within the request (loaded while waiting)
+        const float pc = n < kStageRows ? sh.rcum[n] : __ldcg(&P.fr_cum[par][row]);
+        const int slot = row - __ldcg(&P.fr_off[par][fe.x]);  // frontier slot within the request (loaded while waiting)
         if (lane == 0)  // this row's bytes: all chunk partials + t lists
           mbar_expect_tx(&sh.ready[b], (uint32_t)(cpr * kConsumerWarps * 8 + t * list_stride(k) * 8));
         mbar_wait_acq_cluster(&sh.ready[b], (uint32_t)(n >> 1) & 1u);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 24);
-        merge_row_team(P, layer, par, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv);
+        merge_row_team(P, layer, par, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv,
+                       blockIdx.x == 0 && lane == 0 && n == 0);
+        stamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 5);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 25);
         if (lane < t) mbar_arrive_cluster(mapa_rank(&sh.freeb[b], lrank + lane), 1);  // buffer b is free
         if (lane == 0) {
           red_add_release_gpu(&P.layer_done[layer - 1], 1);  // row done (the select CTA polls)
+          stamp(P, blockIdx.x == 0 && n == 0, 6);
           gstamp(P, blockIdx.x == 0 && n == 0, 26);
         }
         __syncwarp();
@@ -656,8 +679,9 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     // ---- the layer's selection: prefetch + A3 now, then wait for the R row merges ----
     gstamp(P, tid == 0, 28);
     const int* done = &P.layer_done[layer - 1];
+    int pass = 0;
     auto wait_rows = [&]() {
-      if (tid == 0) {
+      if (tid == 0 && pass == 0) {
         while (ld_acquire_gpu(done) < R) {
         }
         P.layer_done[layer - 1] = 0;  // no further arrivals this launch
@@ -665,7 +689,12 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       consumer_sync();
       gstamp(P, tid == 0, 30);
     };
-    select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
+    // (P.debug_mode == 2: timing experiment only, a second pass through the same code)
+    const int npass = P.debug_mode == 2 ? 2 : 1;
+    for (; pass < npass; ++pass) {
+      if (pass) consumer_sync();
+      select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
+    }
     gstamp(P, tid == 0, 29);
   }
   if (tid == 0) bulk_wait_read();  // staging buffers stay valid until the copies have read them
@@ -709,10 +738,10 @@ int expand_grid(int cpr, int k) {
 }
 
 void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool tma, bool fuse_select,
-                   int grid, cudaStream_t s) {
+                   bool early, int grid, cudaStream_t s) {
   const char* base = static_cast<const char*>(logits);
   const size_t smem = layer_smem_bytes(P.cpr, P.k);
-  const int f = fuse_select ? 1 : 0;
+  const int f = (fuse_select ? 1 : 0) | (early && pdl_enabled() ? 2 : 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLayerThreadsT);

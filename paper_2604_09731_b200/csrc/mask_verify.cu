@@ -54,6 +54,7 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
     P.trace[threadIdx.x] = t;
     P.layer_done[threadIdx.x] = 0;
   }
+  if (blockIdx.x == 0 && threadIdx.x <= SMART_MAX_DEPTH) P.fr_ready[threadIdx.x] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *P.fr_total[0] = P.b_loc;
     *P.err = 0;

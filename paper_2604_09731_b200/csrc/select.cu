@@ -40,6 +40,8 @@ size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nra
   return sel_smem_bytes(b_loc, b_all, sort_cap, nc_cap, nranks, k);
 }
 
+size_t select_rec_bytes(int nc_cap) { return sel_rec_bytes(nc_cap); }
+
 cudaError_t select_set_smem(size_t bytes) {
   return cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }

@@ -24,6 +24,7 @@ __device__ __forceinline__ void blk_sync() {
 }
 
 enum SelectMode { kSelFull = 0, kSelLocal = 1, kSelGlobal = 2 };
+constexpr int kA5Par = 256;  // A5 lists up to this length: one entry per thread (<= every NT used)
 
 __device__ __forceinline__ unsigned long long sel_key(float b, int r_glob, int c) {
   return ((unsigned long long)(~float_orderable(b)) << 32) | ((unsigned long long)(unsigned)r_glob << 16) |
@@ -245,6 +246,9 @@ struct SelLayout {
 __host__ __device__ inline size_t sel_align(size_t x) { return (x + 15) & ~size_t(15); }
 
 // nc_cap = cap_rows * k = b_loc * wf * k
+// staged candidate records (P.sel_rec): 16 B per candidate, after keys2
+__host__ __device__ inline size_t sel_rec_bytes(int nc_cap) { return (size_t)nc_cap * 16; }
+
 __host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks = 1,
                                                  int k = 1) {
   const int per_req = nc_cap / (b_loc > 0 ? b_loc : 1);  // wf * k
@@ -381,6 +385,20 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   L.keys = reinterpret_cast<unsigned long long*>(
       reinterpret_cast<char*>(L.E) + sel_align((size_t)b_all * 8));
   L.keys2 = L.keys + P.sort_cap;
+  // optional staging of the layer's candidate records (when the scratch has room, P.sel_rec)
+  int4* const crec = P.sel_rec ? reinterpret_cast<int4*>(L.keys + 2 * (size_t)P.sort_cap) : nullptr;
+  auto get_cand = [&](int q) {
+    if (crec) {
+      const int4 v = crec[q];
+      Cand c;
+      c.tok = v.x;
+      c.p = __int_as_float(v.y);
+      c.cum = __int_as_float(v.z);
+      c.parent = v.w;
+      return c;
+    }
+    return load_cand(&P.cand[lbase + q]);
+  };
   const int nbw = L.nbw, wf = L.wf;
   stamp(P, tid == 0, 9);
 
@@ -443,7 +461,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   wait_rows();
   for (int q = tid; q < nct; q += NT) {
     const int r = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
-    const float cum = __ldcg(&P.cand[lbase + q].cum);
+    const int4 rec = __ldcg(reinterpret_cast<const int4*>(&P.cand[lbase + q]));  // whole record
+    const float cum = __int_as_float(rec.z);
+    if (crec) crec[q] = rec;  // staged for the commit (no second L2 round trip)
     const float D = L.D[r];
     const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
     L.cb[q] = b;
@@ -650,6 +670,71 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       ss.bcast_i[6] = 0;
       ss.bcast_l[0] = N0;
     }
+  } else if (ne <= kA5Par) {
+    // short lists: one entry per thread.  fp64 prefix = 32-wide up-scan inside each tile of 32
+    // entries plus the preceding tiles' totals in order (a function of the entry index only, so
+    // any block size and any sharding give the same bits); the cut is the first failing entry
+    // (ballots), and argmax_j S_j is reduced here as well (tile winners, then in tile order).
+    const int j = tid;
+    const bool act = j < ne;
+    const double bj = act ? (double)sel_key_b(L.keys[j]) : 0.0;
+    double incl = bj;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    double excl = __shfl_up_sync(kFull, incl, 1);
+    if (lane == 0) excl = 0.0;
+    if (lane == 31 && tid < kA5Par) ss.tile_d[warp] = incl;
+    blk_sync<NT>();
+    int ff = ne;
+    double bestS = -1.0;
+    int bestj = ne + 1;
+    if (tid < kA5Par) {
+      double before = 0.0;
+      for (int w = 0; w < warp; ++w) before += ss.tile_d[w];  // tiles in order
+      before += excl;
+      if (act) {
+        if (!rule_ok(bj, before, j)) ff = j;
+        bestS = sp(E0 + before + bj, j + 1);
+        bestj = j + 1;
+      }
+      const unsigned bal = __ballot_sync(kFull, ff < ne);
+      ff = bal ? warp * 32 + __ffs(bal) - 1 : ne;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(kFull, bestS, o);
+        const int oj = __shfl_xor_sync(kFull, bestj, o);
+        if (os > bestS || (os == bestS && oj < bestj)) {
+          bestS = os;
+          bestj = oj;
+        }
+      }
+      if (lane == 0) {
+        ss.wred_i[warp] = ff;
+        ss.wred_d[warp] = bestS;
+        ss.tile_i[warp] = bestj;
+      }
+    }
+    blk_sync<NT>();
+    if (tid == 0) {
+      int js0 = ne, bj0 = 0;
+      double bs = sp(E0, 0);
+      for (int w = 0; w < (ne + 31) / 32; ++w) {
+        js0 = min(js0, ss.wred_i[w]);
+        const double os = ss.wred_d[w];
+        const int oj = ss.tile_i[w];
+        if (oj <= ne && (os > bs || (os == bs && oj < bj0))) {
+          bs = os;
+          bj0 = oj;
+        }
+      }
+      ss.bcast_i[3] = js0;
+      ss.bcast_i[5] = ne;
+      ss.bcast_i[6] = bj0;  // argmax_j (the tail only sums the admitted benefits)
+      ss.bcast_l[0] = N0;
+    }
   } else if (warp == 0) {
     // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
     const int per = (ne + 31) >> 5;
@@ -708,7 +793,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     for (int u = 0; u < kPre; ++u)
       if (u == it) {
         qr[u] = L.off[r] * k + c;
-        cdr[u] = load_cand(&P.cand[lbase + qr[u]]);
+        cdr[u] = get_cand(qr[u]);
       }
   }
   if (pmean) {
@@ -723,8 +808,61 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     if (c & 31) n += __popc(L.bm[r * nbw + (c >> 5)] & ((1u << (c & 31)) - 1u));
     return n;
   };
+  // The next frontier depends on the bitmaps only, so it is built and published first (the
+  // next layer kernel's streaming CTAs start on the flag); node records, E and the trace follow.
+  // (3a) per request: admitted count, finish, next-frontier count and offsets.  Up to 32 requests:
+  // warp 0 alone, scan by shuffles; else all threads + block scan.
+  const bool one_warp = bl <= 32;
+  auto finished_r = [&](int r, int a) {  // Alg.1 line 10
+    return L.fin[r] || a == 0 || (!base && L.nd[r] + a >= P.B);
+  };
+  for (int r = tid; r < bl && (!one_warp || warp == 0); r += NT) {
+    int a = 0;
+    for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
+    L.adm[r] = a;
+    const int nx = finished_r(r, a) ? 0 : a;
+    L.nxt[r] = nx;
+    L.base[r] = nx;
+    P.fr_cnt[npar][r] = nx;
+  }
+  if (one_warp) {
+    if (warp == 0) {
+      const int v = lane < bl ? L.base[lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < bl) {
+        L.base[lane] = incl - v;
+        P.fr_off[npar][lane] = incl - v;
+      }
+      if (lane == 31) *P.fr_total[npar] = incl;
+    }
+    blk_sync<NT>();  // B7
+  } else {
+    blk_sync<NT>();  // B7
+    const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
+    for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
+    if (tid == 0) *P.fr_total[npar] = total;
+  }
+  // (4) next frontier (own requests that continue), with the cum of each node for the row merge
+  for (int q = tid; q < nct; q += NT) {
+    const int r = L.rreq[q / k];
+    const int c = q - L.off[r] * k;
+    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
+    P.cand_adm[lbase + q] = f;
+    if (!f || L.nxt[r] == 0) continue;
+    const int idx = bits_below(r, c);
+    P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+    P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
+  }
+  blk_sync<NT>();  // B8: the next frontier is complete
+  if (tid == 0) publish_flag(&P.fr_ready[layer]);
+  stamp(P, tid == 0, 14);
   // (2) admitted candidates write their node (index among the request's admits in canonical
-  // order = admit bits below) and stage cum / parent path sum for (3)
+  // order = admit bits below) and stage cum / parent path sum for (3b)
   auto commit_node = [&](int q, const Cand& cd, double pps) {
     const int r = L.rreq[q / k];
     const int c = q - L.off[r] * k;
@@ -751,22 +889,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     const int r = sel_key_r(key) - P.b_off;
     if (r < 0 || r >= bl) continue;
     const int q = L.off[r] * k + sel_key_c(key);
-    const Cand cd = load_cand(&P.cand[lbase + q]);
+    const Cand cd = get_cand(q);
     commit_node(q, cd, pmean ? P.path_sum[(size_t)r * P.T + cd.parent] : 0.0);
   }
-  if (!fast3) blk_sync<NT>();  // B7
-  // (3) per request: admitted count, finish, next-frontier count, E (canonical order).  Up to
-  // 32 requests: warp 0 alone, scan by shuffles (no block barriers); else all threads + scan.
-  const bool one_warp = bl <= 32;
+  if (!fast3) blk_sync<NT>();  // B9 (fast3: warp 0 needs only the staged benefits)
+  // (3b) per request: finished flag, node count, E (canonical order)
   for (int r = tid; r < bl && (!one_warp || warp == 0); r += NT) {
-    int a = 0;
-    for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
-    L.adm[r] = a;
-    const bool fin = L.fin[r] || a == 0 || (!base && L.nd[r] + a >= P.B);  // Alg.1 line 10
-    L.nxt[r] = fin ? 0 : a;
-    L.base[r] = fin ? 0 : a;
-    P.fr_cnt[npar][r] = fin ? 0 : a;
-    if (fin && L.cnt[r] > 0) P.finished[r] = 1;
+    const int a = L.adm[r];
+    if (finished_r(r, a) && L.cnt[r] > 0) P.finished[r] = 1;
     P.n_nodes[r] = L.nd[r] + 1 + a;
     if (a == 0) continue;
     const int gi = (mode == kSelGlobal ? P.b_off : 0) + r;
@@ -812,40 +942,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     }
     P.E_r[r] = L.E[gi];
   }
-  if (one_warp) {
-    if (warp == 0) {
-      const int v = lane < bl ? L.base[lane] : 0;
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane < bl) {
-        L.base[lane] = incl - v;
-        P.fr_off[npar][lane] = incl - v;
-      }
-      if (lane == 31) *P.fr_total[npar] = incl;
-    }
-    blk_sync<NT>();  // B8
-  } else {
-    blk_sync<NT>();  // B8
-    const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
-    for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
-    if (tid == 0) *P.fr_total[npar] = total;
-  }
-  stamp(P, tid == 0, 14);
-  // (4) next frontier (own requests that continue), with the cum of each node for the row merge
-  for (int q = tid; q < nct; q += NT) {
-    const int r = L.rreq[q / k];
-    const int c = q - L.off[r] * k;
-    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
-    P.cand_adm[lbase + q] = f;
-    if (!f || L.nxt[r] == 0) continue;
-    const int idx = bits_below(r, c);
-    P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
-    P.fr_cum[npar][L.base[r] + idx] = L.cslot[r * wf + idx];
-  }
+  if (one_warp) __syncwarp();
+  else blk_sync<NT>();  // B10: E complete for the totals
   // ---- totals after the layer (trace S_after) ∥ the A5 report (argmax_j S_j, trace) ----
   if (warp == 0 && mode == kSelFull) {
     const double Ea = warp_det_sum(L.E, bl, lane);

@@ -84,6 +84,7 @@ struct Params {
   int* seglen;        // [cap_rows*cpr] segment length in chunks (at its first chunk)
   int* row_done;      // [max(cap_rows, b_loc*T)] arrival counters (self-resetting)
   int* layer_done;    // [SMART_MAX_DEPTH] rows merged per layer (self-resetting)
+  int* fr_ready;      // [SMART_MAX_DEPTH + 1] frontier of layer l published (reset by begin_step)
   float2* rowstat;    // [cap_rows] (M, Z) of the last expanded layer
   Cand* cand;         // [d][cap_rows*k]
   float* cand_b;      // [d][cap_rows*k] benefit
@@ -96,6 +97,7 @@ struct Params {
   const double* dc_tab;     // marginal cost at N (DERIVATIVE Eq.(15) / DIFFERENCE)
   int n_cost;
   int sort_cap;             // key capacity of the selection sort (power of two)
+  int sel_rec;              // 1: the selection stages the layer's candidate records in smem
   int min_units;            // chunks per CTA at least in the streaming kernels
   long long sat_from;       // smallest N whose exponent was clamped (Q17)
 
@@ -225,6 +227,18 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
+// frontier-ready flag: one thread publishes after a CTA barrier (release, cumulative over the
+// barrier); pollers acquire.  A poll that never completes traps instead of hanging the device.
+__device__ __forceinline__ void publish_flag(int* f) {
+  asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.s32 [%0], 1;" ::"l"(f) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const int* f) {
+  for (unsigned it = 0; ld_acquire_gpu(f) == 0; ++it) {
+    if (it > (1u << 24)) __trap();  // ~seconds: a broken launch sequence, never a valid wait
+    __nanosleep(32);
+  }
+}
+
 // Programmatic dependent launch: every kernel of the step is launched with programmatic stream
 // serialization, runs its shared-memory prologue, then waits for the previous kernel of the
 // stream (griddepcontrol.wait: full completion + memory visibility) before its first global read,
@@ -304,11 +318,12 @@ __device__ __forceinline__ double speed_b(const Params& P, double E, long long N
 // ---- kernels (host launchers in api.cu) ----
 __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32_t* root_pos);
 void launch_expand(const Params& P, int layer, const void* logits, long long ld_bytes, bool tma,
-                   bool fuse_select, int grid, cudaStream_t s);
+                   bool fuse_select, bool early, int grid, cudaStream_t s);
 size_t layer_smem_bytes(int cpr, int k);
 int expand_grid(int cpr, int k);
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
 size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks, int k);
+size_t select_rec_bytes(int nc_cap);
 cudaError_t select_set_smem(size_t bytes);
 void launch_rerank(const Params& P, cudaStream_t s);
 cudaError_t rerank_set_smem(size_t bytes);

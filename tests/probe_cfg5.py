@@ -21,6 +21,11 @@ d, tg, rt, rp = bench.make_set(0, wl, T, 0)
 dd = bench.bf16_dev(d, torch.device("cuda"))
 s = torch.cuda.current_stream()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+for _ in range(int(os.environ.get("WARM", "0"))):  # let the clocks ramp before timing
+    ctx.begin_step()
+    ctx.expand_step(1, dd)
+    ctx.select(1)
+torch.cuda.synchronize()
 for rep in range(int(os.environ.get("REPS", "5"))):
     ctx.begin_step()
     ev[0].record(s)

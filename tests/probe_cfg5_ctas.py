@@ -25,6 +25,10 @@ dd = bench.bf16_dev(d, torch.device("cuda"))
 L = S.lib()
 L.smart_debug_probes.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
 buf = np.zeros(1024, np.uint64)
+for _ in range(int(os.environ.get("WARM", "300"))):  # clocks ramp
+    ctx.begin_step()
+    ctx.expand_step(1, dd)
+torch.cuda.synchronize()
 for rep in range(3):
     ctx.begin_step()
     torch.cuda.synchronize()
@@ -41,3 +45,5 @@ e_ = (en[ok] - t0) / 1000
 print("CTAs", ok.sum(), "start min/p50/max", s_.min(), np.median(s_), s_.max())
 print("end   min/p50/p90/max", e_.min(), np.median(e_), np.percentile(e_, 90), e_.max())
 print("work dur min/p50/max", (e_ - s_).min(), np.median(e_ - s_), (e_ - s_).max())
+print("kernel start/end", (int(buf[66]) - t0) / 1000, (int(buf[67]) - t0) / 1000, "launch", (int(buf[64 + 66]) - t0) / 1000)
+print("sorted ends", np.round(np.sort(e_)[::16], 2))

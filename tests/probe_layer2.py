@@ -44,6 +44,6 @@ for rep in range(3):
                   f" chunk1 {rel(21)} {rel(22)} {rel(23)} | slice arrive {rel(27)} | merge {rel(24)}->{rel(25)} atomic {rel(26)}"
                   f" | select {rel(28)} rows-in {rel(30)} done {rel(29)} end {rel(65 + 2 * layer)}")
             print("   CTA0 chunk-loop end per warp", [rel(56 + w) for w in range(8)], "list sync", rel(31), "ranked", rel(96), "sync2", rel(97), "arrived", rel(98))
-            print("   hand-off cycles: setup->rank", dd_(24, 25), "shfl", dd_(25, 26), "mapa", dd_(26, 27))
+            print("   merge cycles: Z", dd_(1, 2), "thresh+surv", dd_(2, 3), "rank+store", dd_(3, 4), "tail", dd_(4, 5), "arrive", dd_(5, 6))
             print("   select cycles: stage", dd_(9, 10), "elig+rank", dd_(10, 11), "sort", dd_(11, 12), "rule", dd_(12, 13),
                   "commit", dd_(13, 14), "tail", dd_(14, 22))

@@ -76,9 +76,33 @@ __global__ void k(unsigned long long* out, int n, const unsigned long long* g) {
   for (int i = 0; i < n; ++i) { unsigned long long c = clock64(); a += (int)c; }
   t1 = clock64();
   if (lane == 0) out[10] = (t1 - t0) / n + (a == 12345);
+  // (l) double division chain
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) d = 3.0 / (d + 1.0);
+  t1 = clock64();
+  if (lane == 0) out[11] = (t1 - t0) / n + (d == 12345.0);
+  // (m) float division chain
+  float f = lane + 1.f;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) f = 3.f / (f + 1.f);
+  t1 = clock64();
+  if (lane == 0) out[12] = (t1 - t0) / n + (f == 12345.f);
+  // (n) smem atomicOr
+  __shared__ unsigned bm[64];
+  if (lane < 64) bm[lane] = 0;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) atomicOr(&bm[(lane + i) & 63], 1u << (i & 31));
+  t1 = clock64();
+  if (lane == 0) out[13] = (t1 - t0) / n;
+  // (o) F2F f32->f64 + DMUL dep
+  float q = lane;
+  t0 = clock64();
+  for (int i = 0; i < n; ++i) q = (float)((double)q * 1.0000001);
+  t1 = clock64();
+  if (lane == 0) out[14] = (t1 - t0) / n + (q == 12345.f);
 }
 int main() {
-  unsigned long long *o, *g, h[16];
+  unsigned long long *o, *g, h[16] = {};
   cudaMalloc(&o, 16 * 8);
   cudaMalloc(&g, 4096 * 8);
   unsigned long long hg[4096];
@@ -88,7 +112,7 @@ int main() {
   cudaDeviceSynchronize();
   cudaMemcpy(h, o, 16 * 8, cudaMemcpyDeviceToHost);
   const char* nm[] = {"LDS dep", "LDS indep/elem", "SHFL dep", "VOTE+POPC dep", "REDUX dep", "IMAD dep",
-                      "LDG.cg dep (L2)", "DFMA dep", "SHFL.f64+DADD dep", "BAR 1 warp", "CS2R clock"};
-  for (int i = 0; i < 11; ++i) printf("%-22s %llu cycles\n", nm[i], h[i]);
+                      "LDG.cg dep (L2)", "DFMA dep", "SHFL.f64+DADD dep", "BAR 1 warp", "CS2R clock", "DDIV dep", "FDIV dep", "ATOMS.OR", "F2F+DMUL+F2F dep"};
+  for (int i = 0; i < 15; ++i) printf("%-22s %llu cycles\n", nm[i], h[i]);
   return 0;
 }

@@ -58,7 +58,8 @@ void run(int G, long long bytes, const char* src, unsigned long long* out, float
   for (int rep = 0; rep < 3; ++rep) stream<S><<<G, 288, smem>>>(src, bytes, out, sink);
   cudaEventRecord(e0);
   const int R = 10;
-  for (int rep = 0; rep < R; ++rep) stream<S><<<G, 288, smem>>>(src + (rep % 2) * 0, bytes, out, sink);
+  const long long span = (long long)G * bytes; const int nrot = (int)((1ll << 30) / span);
+  for (int rep = 0; rep < R; ++rep) stream<S><<<G, 288, smem>>>(src + (nrot > 1 ? (rep % nrot) * span : 0), bytes, out, sink);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -73,11 +74,12 @@ int main() {
   cudaMemset(src, 0, maxb);
   unsigned long long* out; cudaMalloc(&out, 4096 * 8);
   float* sink; cudaMalloc(&sink, 4096 * 4);
-  for (long long kb : {256, 1024}) {
-    for (int G : {1, 32, 102, 148, 296}) {
+  for (long long kb : {304, 1216}) {
+    for (int G : {148, 256, 296, 444}) {
       if ((long long)G * kb * 1024 > maxb) continue;
-      run<6>(G, kb * 1024, src, out, sink);
-      run<12>(G, kb * 1024, src, out, sink);
+      run<4>(G, kb * 1024, src, out, sink);
+      run<5>(G, kb * 1024, src, out, sink);
+      run<8>(G, kb * 1024, src, out, sink);
     }
   }
   return 0;
