@@ -102,10 +102,10 @@ constexpr int kMergeWarp = kConsumerWarps + 1;       // warp 9: row merges in te
 constexpr int kLayerThreadsT = kLayerThreads + 32;   // 320 threads: consumers, producer, merger
 
 struct __align__(16) ExpandShared {
-  unsigned long long tau;                         // slice-wide bound hint (best warp k-th key)
+  unsigned long long tau;                         // slice-wide bound: max over warps of their k-th best
   int2 rfe[kStageRows];                           // frontier entries of the team's rows
   float rcum[kStageRows];                         // their path scores (cum of the parent node)
-  __align__(16) unsigned pub[2][kConsumerWarps * 4];            // slice start: top-j lane maxima per warp
+  __align__(16) unsigned pub[2][kConsumerWarps * kMaxK];        // slice start: top-k lane maxima per warp
   __align__(16) unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k
   uint64_t ready[2];  // leader: all members' partials of the team's n-th row are in (parity n & 1)
   uint64_t freeb[2];  // every CTA: the leader has consumed buffer parity p (remote arrive)
@@ -314,7 +314,9 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   }
   cluster_sync_all();  // barriers initialised cluster-wide before any remote arrive
   tl_start(P, 32 + layer);
-  if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA start (debug)
+#if SMART_PROBES
+  if (SMART_PROBES && P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA start
+#endif
   const bool sel_cta0 = fuse_select && (int)blockIdx.x == (int)gridDim.x - kCluster;
   if (!early || sel_cta0) pdl_wait();
   pdl_trigger();
@@ -351,13 +353,18 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   // with the fused selection the grid's last cluster is reserved: its rank-0 CTA runs A3-A6
   const int S = fuse_select ? (int)gridDim.x - kCluster : (int)gridDim.x;
   const bool sel_cta = fuse_select && (int)blockIdx.x == S;
-  int t = kCluster;
-  while (t > 1 && (R > S / t || t > cpr)) t >>= 1;
-  const int nteams = S / t;
-  const int team = blockIdx.x / t, member = blockIdx.x % t;
+  // (t is a power of two: shifts, no integer division in the prologue)
+  int lt = 3;  // log2 t
+  while (lt > 0 && (R > (S >> lt) || (1 << lt) > cpr)) --lt;
+  const int t = 1 << lt;
+  const int nteams = S >> lt;
+  const int team = (int)blockIdx.x >> lt, member = (int)blockIdx.x & (t - 1);
   const uint32_t lrank = crank - (uint32_t)member;  // the team leader's rank in the cluster
-  const int nrows = ((int)blockIdx.x < S && team < R) ? (R - team + nteams - 1) / nteams : 0;
-  const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;  // this CTA's chunks of each row
+  const int nrows = ((int)blockIdx.x < S && team < R)
+                        ? ((nteams & (nteams - 1)) == 0 ? (R - team + nteams - 1) >> (31 - __clz(nteams))
+                                                        : (R - team + nteams - 1) / nteams)
+                        : 0;
+  const int mlo = (member * cpr) >> lt, mhi = ((member + 1) * cpr) >> lt;  // this CTA's chunks of each row
   const int nstage = min(nrows, kStageRows);
   const int tsel = (t == 8) ? 0 : (t == 4) ? 1 : (t == 2) ? 2 : 3;
   if (nstage > 0 && tid == tsel) {
@@ -479,7 +486,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         const float Mw = warp_max_fast(m);
         // exp2(x*log2e - M*log2e) on element pairs: FFMA2 + 2 MUFU + FADD2 (two pair accumulators)
         unsigned long long acc2[2] = {0ull, 0ull};
-        if (Mw != -INFINITY) {
+        if (Mw != -INFINITY && P.debug_mode != 4) {  // (debug_mode 4: timing experiment, no exps)
           const float ML = Mw * kLog2e;
           const unsigned long long l2e2 = f2pk(kLog2e, kLog2e), nml2 = f2pk(-ML, -ML);
 #pragma unroll
@@ -491,7 +498,14 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         const float sacc = warp_sum((f2lo(acc2[0]) + f2hi(acc2[0])) + (f2lo(acc2[1]) + f2hi(acc2[1])));
         gstamp(P, t0 && i < 2, 19 + 3 * i);
         if (lane == 0) tb.msl[(c - mlo) * kConsumerWarps + warp] = make_float2(Mw, sacc);
+        if (P.debug_mode == 3) {  // timing experiment only: softmax without the top-k filter
+          __syncwarp();
+          if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);
+          continue;
+        }
 
+        const bool pq = t0 && i < 2;  // probe: CTA 0, warp 0 lane 0, first two chunks
+        stamp(P, pq, 24 + 4 * i);
         // ---- top-k candidates of this warp-chunk ----
         // CTA-wide bound at the slice's first chunk: every warp publishes its top-j lane maxima
         // (j = ceil(k/8), one lane per round, so ties keep their multiplicity); these 8j values
@@ -499,7 +513,10 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         // value from below and key(v_k, INT_MAX) bounds the slice's k-th best key.  Later chunks
         // run barrier-free on the warp's own bound (tightened by compaction).
         if (c == mlo) {
-          const int jr = (k + kConsumerWarps - 1) / kConsumerWarps;
+          // every warp publishes its top-j lane maxima (j >= 2 rounds of a warp max; ties keep
+          // their multiplicity); v_k, the k-th largest of these 8j values, bounds the slice's
+          // k-th best value from below
+          const int jr = max((k + kConsumerWarps - 1) / kConsumerWarps, 2);
           unsigned* pub = sh.pub[i & 1];
           unsigned rem = (m == m) ? float_orderable(m) : 0u;
           for (int r = 0; r < jr; ++r) {
@@ -509,14 +526,18 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
             if (lane == 0) pub[warp * jr + r] = cur;
           }
           consumer_sync();
-          const int np = kConsumerWarps * jr;
-          const unsigned u = lane < np ? pub[lane] : 0u;
-          int gt = 0;
-          for (int o = 0; o < np; o += 4) {
-            const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
-            gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+          const int np = kConsumerWarps * jr;  // multiple of 8
+          unsigned vc = 0xffffffffu;
+          for (int e = lane; e < np; e += 32) {
+            const unsigned u = pub[e];
+            int gt = 0;
+            for (int o = 0; o < np; o += 4) {
+              const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
+              gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+            }
+            if (gt < k && u < vc) vc = u;
           }
-          const unsigned vk = __reduce_min_sync(kFull, (lane < np && gt < k) ? u : 0xffffffffu);
+          const unsigned vk = __reduce_min_sync(kFull, vc);
           if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)
             const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
             if (b0 > bound) bound = b0;
@@ -525,109 +546,74 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         // elements whose value reaches the bound are appended to the warp buffer at positions from
         // a warp prefix sum (no shared atomics); when the buffer would overflow it is compacted to
         // its top-k, the bound tightened and the remaining elements re-filtered
-        float bv = bound ? tk_val(bound) : -INFINITY;
-        unsigned pend = 0u;
-        if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
-#pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j)
-            if (vm[j] >= bv) {
-#pragma unroll
-              for (int e = 0; e < EPV; ++e) pend |= (x[j * EPV + e] >= bv ? 1u : 0u) << (j * EPV + e);
-            }
+        stamp(P, pq && i == 0, 31);
+        {
+          // barrier-free CTA bound: every warp posts its k-th best after each compaction (a lower
+          // bound of the slice's k-th best) with a shared atomic max; all warps adopt the maximum
+          const unsigned long long tt = *reinterpret_cast<volatile unsigned long long*>(&sh.tau);
+          if (tt > bound) bound = tt;
         }
-        while (__any_sync(kFull, pend != 0u)) {
-          const int cnt = __popc(pend);
-          int incl, total;
-          if (!__any_sync(kFull, cnt > 1)) {  // common case: at most one candidate per lane
-            const unsigned bal = __ballot_sync(kFull, cnt > 0);
-            incl = __popc(bal & (0xffffffffu >> (31 - lane)));
-            total = __popc(bal);
-          } else {
-            incl = cnt;
+        float bv = bound ? tk_val(bound) : -INFINITY;
+        if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
+          // vectors whose max reaches the bound are expanded cooperatively: each group of EPV
+          // lanes takes one such vector (its elements re-read from the still-held ring stage),
+          // compares them with the bound and appends the survivors at ballot-prefix positions
+          constexpr int G = 32 / EPV;  // vectors per pass
+          stamp(P, pq, 25 + 4 * i);
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int tt = __shfl_up_sync(kFull, incl, o);
-              if (lane >= o) incl += tt;
-            }
-            total = __shfl_sync(kFull, incl, 31);
-          }
-          if (total == 0) break;
-          if (pend) {
-            int pos = wcnt + incl - cnt;
-            unsigned bits = pend;
-            while (bits) {
-              const int e = __ffs(bits) - 1;
-              bits &= bits - 1u;
-              if (pos < kSegBuf) {
-                const int idx = elem_index<BF16>(cbase, tid, e);
-                float v;
-                if (idx >= V) {
-                  v = -INFINITY;
-                } else if (TMA) {  // the stage is still held: reload the element from shared memory
-                  const char* sp = ring + (size_t)s * kChunkBytes +
-                                   ((size_t)((e / EPV) * kConsumers + tid) * EPV + (e % EPV)) * (BF16 ? 2 : 4);
+          for (int j = 0; j < kVecPerThread; ++j) {
+            unsigned bal = __ballot_sync(kFull, vm[j] >= bv);
+            while (bal) {
+              if (wcnt > kSegBuf - 32) {  // keep room for a full pass: compact, tighten, re-filter
+                __syncwarp();
+                warp_compact(W, wcnt, k, lane);
+                wcnt = k;
+                if (W.list[k - 1] > bound) bound = W.list[k - 1];
+                if (lane == 0) atomicMax(&sh.tau, W.list[k - 1]);
+                bv = tk_val(bound);
+                bal &= __ballot_sync(kFull, vm[j] >= bv);
+                if (!bal) break;
+              }
+              unsigned bb = bal;
+              for (int g = 0; g < lane / EPV; ++g) bb &= bb - 1u;
+              const int L = bb ? __ffs(bb) - 1 : -1;  // owner lane of this group's vector
+#pragma unroll
+              for (int g = 0; g < G; ++g) bal &= bal - 1u;
+              bool q = false;
+              float v = -INFINITY;
+              int idx = 0;
+              if (L >= 0) {
+                const int tl = warp * 32 + L;  // the owner's consumer thread id
+                const int e = j * EPV + lane % EPV;
+                idx = elem_index<BF16>(cbase, tl, e);
+                if (idx < V) {  // past the row end: stale stage bytes, never a candidate
+                  const char* sp = TMA ? ring + (size_t)s * kChunkBytes +
+                                             ((size_t)(j * kConsumers + tl) * EPV + (e % EPV)) * (BF16 ? 2 : 4)
+                                       : rowp(n, row) + (size_t)idx * (BF16 ? 2 : 4);
                   v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(sp)) << 16)
                            : *reinterpret_cast<const float*>(sp);
-                } else {
-                  const char* rp = rowp(n, row) + (size_t)idx * (BF16 ? 2 : 4);
-                  v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(rp)) << 16)
-                           : *reinterpret_cast<const float*>(rp);
                 }
-                W.buf[pos] = tk_key(v, idx);
-                pend &= ~(1u << e);
+                q = v >= bv;  // NaN never qualifies (the row merge flags it)
               }
-              ++pos;
+              const unsigned qb = __ballot_sync(kFull, q);
+              if (q) W.buf[wcnt + __popc(qb & ((1u << lane) - 1u))] = tk_key(v, idx);
+              wcnt += __popc(qb);
             }
           }
-          if (wcnt + total <= kSegBuf) {
-            wcnt += total;
-            break;
-          }
-          __syncwarp();
-          warp_compact(W, kSegBuf, k, lane);
-          wcnt = k;
-          if (W.list[k - 1] > bound) bound = W.list[k - 1];
-          bv = tk_val(bound);
-#pragma unroll
-          for (int e = 0; e < EPT; ++e)
-            if (!(x[e] >= bv)) pend &= ~(1u << e);
         }
+        stamp(P, pq, 26 + 4 * i);
         if (wcnt >= 2 * k && c + 1 < mhi) {  // keep the warp's buffer short
           __syncwarp();
           warp_compact(W, wcnt, k, lane);
           wcnt = k;
           if (W.list[k - 1] > bound) bound = W.list[k - 1];
+          if (lane == 0) atomicMax(&sh.tau, W.list[k - 1]);
         }
         __syncwarp();
+        stamp(P, pq && i == 0, 27);
         if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
-        if (((c - mlo) & 3) == 3 && c + 1 < mhi) {
-          // every 4 chunks of a long slice: the CTA's k-th best so far (rank merge of the warps'
-          // lists) becomes everyone's bound, so later chunks rarely hold a candidate
-          if (wcnt > k) {
-            warp_compact(W, wcnt, k, lane);
-            wcnt = k;
-          }
-          if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
-          consumer_sync();
-          const int nl = kConsumerWarps * k;
-          if (tid < nl) {
-            const unsigned long long key = sh.cl[tid];
-            const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
-            int r0 = 0, r1 = 0;
-#pragma unroll 4
-            for (int f = 0; f < nl / 2; ++f) {
-              const ulonglong2 v = c2[f];
-              r0 += (v.x > key);
-              r1 += (v.y > key);
-            }
-            if (r0 + r1 == k - 1) sh.tau = key;  // the unique rank k-1 entry
-          }
-          consumer_sync();
-          if (sh.tau > bound) bound = sh.tau;
-        }
         gstamp(P, t0 && i < 2, 20 + 3 * i);
       }
-      gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 56 + warp);
       // ---- slice end: warp buffers (top-k only if longer) -> CTA list (rank merge) -> leader ----
       if (wcnt > k) {
         warp_compact(W, wcnt, k, lane);
@@ -698,7 +684,9 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     gstamp(P, tid == 0, 29);
   }
   if (tid == 0) bulk_wait_read();  // staging buffers stay valid until the copies have read them
-  if (P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[640 + blockIdx.x] = gtime();  // per-CTA work end (debug)
+#if SMART_PROBES
+  if (SMART_PROBES && P.dbg && tid == 0 && blockIdx.x < 384) P.dbg[640 + blockIdx.x] = gtime();  // per-CTA work end
+#endif
   // every CTA stays until the cluster is done with its shared memory (remote stores / arrives)
   cluster_sync_all();
   tl_end(P, layer);

@@ -457,7 +457,7 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
   }
   if (nanf) atomicOr(P.err, kErrTargetNaN);
   tl_end(P, 21);
-  if (P.dbg && tid == 0) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA end (debug timeline)
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA end (debug timeline)
 }
 
 }  // namespace

@@ -687,7 +687,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     double excl = __shfl_up_sync(kFull, incl, 1);
     if (lane == 0) excl = 0.0;
     if (lane == 31 && tid < kA5Par) ss.tile_d[warp] = incl;
+    stamp(P, tid == 0, 15);
     blk_sync<NT>();
+    stamp(P, tid == 0, 16);
     int ff = ne;
     double bestS = -1.0;
     int bestj = ne + 1;
@@ -700,6 +702,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         bestS = sp(E0 + before + bj, j + 1);
         bestj = j + 1;
       }
+      stamp(P, tid == 0, 17);
       const unsigned bal = __ballot_sync(kFull, ff < ne);
       ff = bal ? warp * 32 + __ffs(bal) - 1 : ne;
 #pragma unroll
@@ -717,7 +720,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         ss.tile_i[warp] = bestj;
       }
     }
+    stamp(P, tid == 0, 18);
     blk_sync<NT>();
+    stamp(P, tid == 0, 19);
     if (tid == 0) {
       int js0 = ne, bj0 = 0;
       double bs = sp(E0, 0);
@@ -735,6 +740,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       ss.bcast_i[6] = bj0;  // argmax_j (the tail only sums the admitted benefits)
       ss.bcast_l[0] = N0;
     }
+    stamp(P, tid == 0, 20);
   } else if (warp == 0) {
     // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
     const int per = (ne + 31) >> 5;

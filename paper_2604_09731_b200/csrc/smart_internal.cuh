@@ -271,28 +271,33 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 // probe slots: 0 min CTA start, 1 max CTA start, 2 max stream end, 3 last merge start,
 // 4 last merge end, 5 select start, 6 select end, 7 max CTA end, 8 first merge start
+// Probes are compiled in only with -DSMART_PROBES=1 (`SMART_PROBES=1 python -m
+// paper_2604_09731_b200._build --force`): in the product build they cost nothing in the hot loops.
+#ifndef SMART_PROBES
+#define SMART_PROBES 0
+#endif
 __device__ __forceinline__ void probe_min(const Params& P, int slot) {
-  if (P.dbg) atomicMin(&P.dbg[slot], gtime());
+  if (SMART_PROBES && P.dbg) atomicMin(&P.dbg[slot], gtime());
 }
 __device__ __forceinline__ void probe_max(const Params& P, int slot) {
-  if (P.dbg) atomicMax(&P.dbg[slot], gtime());
+  if (SMART_PROBES && P.dbg) atomicMax(&P.dbg[slot], gtime());
 }
 // kernel timeline (dbg[64 + 2*kid] = min start, dbg[65 + 2*kid] = max end); kid: 0 begin,
 // 1..d layer kernels, 20 mask, 21 verify, 22 select kernel; kid + 32: CTA launch (before the
 // dependency wait)
 __device__ __forceinline__ void tl_start(const Params& P, int kid) {
-  if (P.dbg && threadIdx.x == 0) atomicMin(&P.dbg[64 + 2 * kid], gtime());
+  if (SMART_PROBES && P.dbg && threadIdx.x == 0) atomicMin(&P.dbg[64 + 2 * kid], gtime());
 }
 __device__ __forceinline__ void tl_end(const Params& P, int kid) {
-  if (P.dbg && threadIdx.x == 0) atomicMax(&P.dbg[65 + 2 * kid], gtime());
+  if (SMART_PROBES && P.dbg && threadIdx.x == 0) atomicMax(&P.dbg[65 + 2 * kid], gtime());
 }
 // globaltimer stamp of one thread into dbg[slot] (slots 16..31: CTA 0 timeline)
 __device__ __forceinline__ void gstamp(const Params& P, bool on, int slot) {
-  if (P.dbg && on) P.dbg[slot] = gtime();
+  if (SMART_PROBES && P.dbg && on) P.dbg[slot] = gtime();
 }
 // cycle stamps (clock64) of one thread into dbg[32 + slot]
 __device__ __forceinline__ void stamp(const Params& P, bool on, int slot) {
-  if (P.dbg && on) P.dbg[32 + slot] = clock64();
+  if (SMART_PROBES && P.dbg && on) P.dbg[32 + slot] = clock64();
 }
 
 // ---- cost model (fp64; Eqs.(4),(5),(15); clamp Q17) ----

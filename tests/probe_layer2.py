@@ -43,7 +43,11 @@ for rep in range(3):
             print(f"layer {layer}: R {rel(16)} staged {rel(17)} | CTA0 chunk0 data {rel(18)} softmax {rel(19)} topk {rel(20)}"
                   f" chunk1 {rel(21)} {rel(22)} {rel(23)} | slice arrive {rel(27)} | merge {rel(24)}->{rel(25)} atomic {rel(26)}"
                   f" | select {rel(28)} rows-in {rel(30)} done {rel(29)} end {rel(65 + 2 * layer)}")
-            print("   CTA0 chunk-loop end per warp", [rel(56 + w) for w in range(8)], "list sync", rel(31), "ranked", rel(96), "sync2", rel(97), "arrived", rel(98))
+            print("   list sync", rel(31), "ranked", rel(96), "sync2", rel(97), "arrived", rel(98))
+            print("   chunk0 cycles: bound", dd_(24, 31), "pend", dd_(31, 25), "append", dd_(25, 26), "compact", dd_(26, 27),
+                  "| chunk1: pend", dd_(28, 29), "append", dd_(29, 30))
             print("   merge cycles: Z", dd_(1, 2), "thresh+surv", dd_(2, 3), "rank+store", dd_(3, 4), "tail", dd_(4, 5), "arrive", dd_(5, 6))
             print("   select cycles: stage", dd_(9, 10), "elig+rank", dd_(10, 11), "sort", dd_(11, 12), "rule", dd_(12, 13),
                   "commit", dd_(13, 14), "tail", dd_(14, 22))
+            print("   A5 cycles: scan", dd_(12, 15), "bar", dd_(15, 16), "rule+div", dd_(16, 17), "argmax", dd_(17, 18),
+                  "bar", dd_(18, 19), "reduce", dd_(19, 20), "B5", dd_(20, 13))
