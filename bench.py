@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--cost", default="roofline", choices=["roofline", "measured"],
                     help="cost-model fixture: roofline-fitted (default) or measured on a B200 (NEXT #2)")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-hbm-regime", action="store_true", help="skip the cfg5 layer-1 HBM-regime measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -452,6 +453,12 @@ def main():
                          "C oracle, 1 thread, ~12 s bounded", "ms_per_step": 1e3 * el / n,
                "host_cpu": _cpu_model(), "host_nproc": os.cpu_count()}
 
+    # ---- the HBM-bound regime of the same kernel: cfg5's first layer (256 frontier rows x
+    # V = 152064 bf16 = 78 MB per launch), L2-cold rotating pools, CUDA events on the stream ----
+    hbm = None
+    if rank == 0 and world == 1 and not args.no_hbm_regime:
+        hbm = hbm_regime(S, dev, stream, peak, peak_src)
+
     if rank == 0:
         beta = st0["accepted_local"] / max(st0["nodes_local"], 1)
         line = {
@@ -469,6 +476,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline,
+            "roofline_hbm_regime": hbm,
             "cpu_baseline": cpu,
             "step_breakdown_ms": {"begin": beg_ms, "expand_per_layer": [float(x) for x in exp_ms],
                                   "select_per_layer": [float(x) for x in sel_ms], "mask": mask_ms,
@@ -487,6 +495,56 @@ def main():
         dist.destroy_process_group()
     ctx.close()
     return 0
+
+
+def hbm_regime(S, dev, stream, peak, peak_src, reps=30):
+    """Layer kernel (A1+A2) on cfg5's first layer: 256 frontier rows of V = 152064 bf16 logits in
+    FRONTIER row layout, synthetic rows shaped like inputs/synth.py (N(0, 2) background + 8 head
+    tokens), generated on the device; pools rotate over > 2x L2 so every launch reads from HBM."""
+    import torch
+    wl = WORKLOADS["cfg5_r1distill_b256"]
+    import make_cost_fixture as mcf
+    fx = mcf.load(wl["fixture"])
+    b, V = wl["b"], wl["V"]
+    cfg = S.Config(vocab=V, top_k=wl["k"], max_depth=wl["d"], max_frontier=wl["W"], batch_local=b,
+                   batch_global=b, budget_verify=wl["B_verify"], alpha=ALPHA, bonus=1, logits_dtype=S.BF16,
+                   row_mode=S.ROWS_FRONTIER)
+    ctx = S.Smart(cfg, S.Cost(lam=fx["lam"], beta=fx["beta"], gamma=fx["gamma"], delta=fx["delta"], rho=fx["rho"],
+                              eta=fx["eta"], c_T=fx["c_T"]), dev.index or 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    npool = max(3, -(-2 * l2 // (b * V * 2)) + 1)
+    pools = []
+    for _ in range(npool):
+        x = torch.randn(b, V, device=dev, generator=g) * SYNTH["sigma_bg"]
+        idx = torch.randint(0, V, (b, 8), device=dev, generator=g)
+        amp = (torch.rand(b, 1, device=dev, generator=g) * (SYNTH["a_hi"] - SYNTH["a_lo"]) + SYNTH["a_lo"]) * \
+            torch.arange(1, 9, device=dev).float().pow(-0.7)
+        x.scatter_add_(1, idx, amp)
+        pools.append(x.to(torch.bfloat16))
+    times = []
+    with torch.cuda.stream(stream):
+        for i in range(reps + 10):
+            ctx.begin_step(stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.expand_step(1, pools[i % npool], stream=stream)
+            e1.record(stream)
+            ctx.select(1, stream=stream)
+            if i >= 10:
+                times.append((e0, e1))
+    stream.synchronize()
+    ms = sorted(a.elapsed_time(c) for a, c in times)
+    med = ms[len(ms) // 2]
+    nbytes = b * V * 2
+    ctx.close()
+    gbs = nbytes / (med / 1e3) / 1e9
+    return {"bound": "hbm", "workload": "cfg5_r1distill_b256 layer 1: 256 rows x 152064 bf16 (78 MB/launch)",
+            "kernel": "layer_kernel (A1+A2), eager launch incl. launch latency", "achieved": gbs, "peak": peak,
+            "unit": "GB/s", "frac": gbs / peak, "per_launch_ms_median": med, "per_launch_ms_min": ms[0],
+            "launches": len(ms), "peak_source": peak_src,
+            "l2": f"{npool} rotating pools x {nbytes / 1e6:.0f} MB"}
 
 
 def _cpu_model():

@@ -14,8 +14,9 @@
 //    mbarrier tx count) into a 6-stage shared-memory ring; 8 consumer warps read 16-byte
 //    vectors from it.
 //  * softmax: each consumer warp reduces its 1024 (bf16) / 512 (fp32) elements of a chunk to
-//    (max, sum exp) with a fixed shuffle tree; the row merge combines the cpr x 8 partials in
-//    fixed order, so Z is bit-identical for any grid size or sharding.
+//    (max, sum exp) with a fixed shuffle tree; the CTA that streamed a chunk combines its 8 warp
+//    partials in warp order, and the row merge combines the cpr chunk partials in fixed order, so
+//    Z is bit-identical for any grid size, team layout or sharding.
 //  * top-k (exact, ties -> lower index): keys are 64-bit (orderable value | ~index), so one
 //    compare orders two candidates.  Per warp and segment (consecutive chunks of one row in one
 //    CTA) a running lower bound of the k-th best key is kept: at the segment's first chunk it is
@@ -120,17 +121,18 @@ struct __align__(16) ExpandShared {
 __host__ __device__ inline int list_stride(int k) { return (k + 1) & ~1; }
 
 struct TeamBuf {
-  float2* ms[2];
+  float4* ms[2];              // receive: per-chunk softmax partials (M_c, S_c, -, -) [cpr]
   unsigned long long* lists[2];
   unsigned long long* surv;  // merge scratch [kCluster * kp]
-  float2* msl;               // send staging: this CTA's partials [cpr][8]
+  float2* msl;               // this CTA's (chunk, warp) partials [cpr][8]
   unsigned long long* listl; // send staging: this CTA's top-k [kp]
+  float4* msc;               // send staging: this CTA's per-chunk partials [cpr]
 };
 
 __host__ __device__ inline size_t team_buf_bytes(int cpr, int k) {
   const size_t kp = (size_t)list_stride(k);
-  return 2 * ((size_t)cpr * kConsumerWarps * 8 + (size_t)kCluster * kp * 8) + (size_t)kCluster * kp * 8 +
-         (size_t)cpr * kConsumerWarps * 8 + kp * 8;
+  return 2 * ((size_t)cpr * 16 + (size_t)kCluster * kp * 8) + (size_t)kCluster * kp * 8 +
+         (size_t)cpr * kConsumerWarps * 8 + kp * 8 + (size_t)cpr * 16;
 }
 
 __device__ inline TeamBuf team_buf(char* base, int cpr, int k) {
@@ -138,8 +140,8 @@ __device__ inline TeamBuf team_buf(char* base, int cpr, int k) {
   TeamBuf t;
   char* p = base;
   for (int b = 0; b < 2; ++b) {
-    t.ms[b] = reinterpret_cast<float2*>(p);
-    p += (size_t)cpr * kConsumerWarps * 8;
+    t.ms[b] = reinterpret_cast<float4*>(p);
+    p += (size_t)cpr * 16;
     t.lists[b] = reinterpret_cast<unsigned long long*>(p);
     p += (size_t)kCluster * kp * 8;
   }
@@ -148,6 +150,8 @@ __device__ inline TeamBuf team_buf(char* base, int cpr, int k) {
   t.msl = reinterpret_cast<float2*>(p);
   p += (size_t)cpr * kConsumerWarps * 8;
   t.listl = reinterpret_cast<unsigned long long*>(p);
+  p += (size_t)kp * 8;
+  t.msc = reinterpret_cast<float4*>(p);
   return t;
 }
 
@@ -212,23 +216,25 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
 // row's k-th best key from below); the entries >= T are ranked among themselves and the top k
 // written with p (A1) and cum (A2, Eq.(3)).
 __device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int slot, int t,
-                               const float2* ms, const unsigned long long* lists, unsigned long long* surv,
+                               const float4* ms, const unsigned long long* lists, unsigned long long* surv,
                                bool pr) {
   const int lane = threadIdx.x & 31;
-  stamp(P, pr, 1);
   const int k = P.k, cpr = P.cpr;
-  const int npart = cpr * kConsumerWarps;  // <= 512
-  // (1) softmax normaliser
+  stamp(P, pr, 1);
+  // (1) softmax normaliser from the cpr per-chunk partials (each already combined over its 8
+  // warps in fixed order by the member that streamed the chunk): M = max, Z = sum S_c exp(M_c - M)
+  // in a fixed association (lane-strided, then the xor tree) -- a function of cpr only
   float m = -INFINITY;
-  for (int q = lane; q < npart; q += 32) m = fmaxf(m, ms[q].x);
+  for (int q = lane; q < cpr; q += 32) m = fmaxf(m, ms[q].x);
   const float M = warp_max_fast(m);
   const float ML = M * kLog2e;
   float z = 0.f;
-  for (int q = lane; q < npart; q += 32) {
-    const float2 v = ms[q];
+  for (int q = lane; q < cpr; q += 32) {
+    const float4 v = ms[q];
     if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
   }
   const float Z = warp_sum(z);
+  const float rZ = 1.0f / Z;
   stamp(P, pr, 2);
   // (2) threshold: best tail over the members' lists
   const int kp = list_stride(k);
@@ -250,25 +256,34 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
   __syncwarp();
   stamp(P, pr, 3);
   // (4) exact top-k among the survivors; A1 p and A2 cum
-  for (int s0 = lane; s0 < ns; s0 += 32) {
-    const unsigned long long key = surv[s0];
-    int r0 = 0, r1 = 0;
-    int q = 0;
-    for (; q + 1 < ns; q += 2) {
-      r0 += (surv[q] > key);
-      r1 += (surv[q + 1] > key);
-    }
-    if (q < ns) r0 += (surv[q] > key);
-    const int rank = r0 + r1;
-    if (rank < k) {
-      const float v = tk_val(key);
-      const float pj = ex2(fmaf(v, kLog2e, -ML)) / Z;  // p = exp(x - M) / Z   (tau = 1, Q10)
-      Cand cd;
-      cd.tok = tk_idx(key);
-      cd.p = pj;
-      cd.cum = pc * pj;  // Eq.(3)
-      cd.parent = fe.y;
-      P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
+  auto emit = [&](unsigned long long key, int rank) {
+    const float v = tk_val(key);
+    const float pj = ex2(fmaf(v, kLog2e, -ML)) * rZ;  // p = exp(x - M) / Z   (tau = 1, Q10)
+    Cand cd;
+    cd.tok = tk_idx(key);
+    cd.p = pj;
+    cd.cum = pc * pj;  // Eq.(3)
+    cd.parent = fe.y;
+    P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
+  };
+  if (ns <= 32) {
+    // one survivor per lane; rank by broadcast compares (no shared-memory loop)
+    const unsigned long long mine = lane < ns ? surv[lane] : 0ull;
+    int rank = 0;
+    for (int q = 0; q < ns; ++q) rank += (__shfl_sync(kFull, mine, q) > mine);
+    if (lane < ns && rank < k) emit(mine, rank);
+  } else {
+    for (int s0 = lane; s0 < ns; s0 += 32) {
+      const unsigned long long key = surv[s0];
+      int r0 = 0, r1 = 0;
+      int q = 0;
+      for (; q + 1 < ns; q += 2) {
+        r0 += (surv[q] > key);
+        r1 += (surv[q + 1] > key);
+      }
+      if (q < ns) r0 += (surv[q] > key);
+      const int rank = r0 + r1;
+      if (rank < k) emit(key, rank);
     }
   }
   stamp(P, pr, 4);
@@ -415,7 +430,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         const float pc = n < kStageRows ? sh.rcum[n] : __ldcg(&P.fr_cum[par][row]);
         const int slot = row - __ldcg(&P.fr_off[par][fe.x]);  // frontier slot within the request (loaded while waiting)
         if (lane == 0)  // this row's bytes: all chunk partials + t lists
-          mbar_expect_tx(&sh.ready[b], (uint32_t)(cpr * kConsumerWarps * 8 + t * list_stride(k) * 8));
+          mbar_expect_tx(&sh.ready[b], (uint32_t)(cpr * 16 + t * list_stride(k) * 8));
         mbar_wait_acq_cluster(&sh.ready[b], (uint32_t)(n >> 1) & 1u);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 24);
         merge_row_team(P, layer, par, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv,
@@ -642,6 +657,22 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
           if (rank < k) tb.listl[rank] = key;
         }
         if ((k & 1) && tid == 0) tb.listl[k] = kKeySentinel - 1000;  // even-k padding slot
+        // per-chunk softmax partials: the 8 warps' (M_w, s_w) of each of this CTA's chunks
+        // combined in warp order (fixed association: a function of the chunk alone)
+        for (int cc = kConsumers - 1 - tid; cc < mhi - mlo; cc += kConsumers) {
+          const float2* pw = tb.msl + cc * kConsumerWarps;
+          float Mc = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kConsumerWarps; ++w) Mc = fmaxf(Mc, pw[w].x);
+          const float MLc = Mc * kLog2e;
+          float Sc = 0.f;
+#pragma unroll
+          for (int w = 0; w < kConsumerWarps; ++w) {
+            const float2 v = pw[w];
+            if (v.y != 0.f || isnan(v.y)) Sc += v.y * ex2(fmaf(v.x, kLog2e, -MLc));
+          }
+          tb.msc[cc] = make_float4(Mc, Sc, 0.f, 0.f);
+        }
       }
       gstamp(P, t0 && n == 0, 96);
       consumer_sync();  // staging complete
@@ -651,8 +682,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         fence_proxy_async_smem();
         const uint32_t bar = mapa_rank(&sh.ready[b], lrank);
         const int kp = list_stride(k);
-        bulk_s2cluster(mapa_rank(tb.ms[b] + mlo * kConsumerWarps, lrank), tb.msl,
-                       (uint32_t)((mhi - mlo) * kConsumerWarps * 8), bar);
+        bulk_s2cluster(mapa_rank(tb.ms[b] + mlo, lrank), tb.msc, (uint32_t)((mhi - mlo) * 16), bar);
         bulk_s2cluster(mapa_rank(tb.lists[b] + member * kp, lrank), tb.listl, (uint32_t)(kp * 8), bar);
         bulk_commit();
         gstamp(P, t0 && n == 0, 98);
