@@ -25,7 +25,7 @@ PREFIX, FROZEN = 0, 1
 NODE_SUM, PATH_MEAN = 0, 1
 DERIVATIVE, DIFFERENCE = 0, 1
 BF16, FP32 = 0, 1
-ROWS_NODE, ROWS_FRONTIER, ROWS_KARY = 0, 1, 2
+ROWS_NODE, ROWS_FRONTIER, ROWS_KARY, ROWS_POSITION = 0, 1, 2, 3
 TRACE_F = 14
 SUM_F = 9
 TRACE_NAMES = ["n_rows", "n_cand", "n_elig", "n_admit", "N0", "E0", "S0", "S_after",
@@ -257,7 +257,7 @@ def step(cfg: Config, cost: Cost, draft: np.ndarray, target: np.ndarray | None =
 
     draft: uint16 (bf16 bits) or float32 array whose last axis is the (possibly padded) vocab;
            ROWS_NODE: shape [b, T, ld]; ROWS_FRONTIER: [d, rows_cap, ld] (layer_stride derived);
-           ROWS_KARY: [b, n_kary, ld].
+           ROWS_KARY: [b, n_kary, ld]; ROWS_POSITION (DFLASH, P:879): [b, >= d, ld].
     target: same dtype, [b, T, ld_t] or None.
     """
     b, T, d, k = cfg.b, cfg.tmax(), cfg.d, cfg.k
@@ -267,7 +267,7 @@ def step(cfg: Config, cost: Cost, draft: np.ndarray, target: np.ndarray | None =
     ld = draft.shape[-1]
     if cfg.row_mode == ROWS_FRONTIER:
         layer_stride = draft.shape[1] * ld
-    elif cfg.row_mode == ROWS_KARY:
+    elif cfg.row_mode in (ROWS_KARY, ROWS_POSITION):
         layer_stride = draft.shape[1]
     if target is not None:
         target = np.ascontiguousarray(target)
@@ -355,7 +355,10 @@ def baseline_step(cfg: Config, draft: np.ndarray, target: np.ndarray | None = No
     b, d = cfg.b, cfg.d
     T = baseline_T(cfg)
     draft = np.ascontiguousarray(draft)
-    assert draft.shape[0] == b and draft.shape[1] == T, (draft.shape, b, T)
+    if cfg.row_mode == ROWS_POSITION:  # DFLASH position rows [b, d, ld]
+        assert draft.shape[0] == b and draft.shape[1] == d, (draft.shape, b, d)
+    else:
+        assert draft.shape[0] == b and draft.shape[1] == T, (draft.shape, b, T)
     ld = draft.shape[-1]
     if target is not None:
         target = np.ascontiguousarray(target)

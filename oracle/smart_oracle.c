@@ -268,6 +268,8 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
           row = (const char*)draft + ((int64_t)r * T + u) * ld * esz;
         else if (cfg->row_mode == ORC_ROWS_KARY) /* path-keyed: full k-ary tree index */
           row = (const char*)draft + ((int64_t)r * layer_stride + kid[r * T + u]) * ld * esz;
+        else if (cfg->row_mode == ORC_ROWS_POSITION) /* DFLASH: position l's row for every node */
+          row = (const char*)draft + ((int64_t)r * layer_stride + (l - 1)) * ld * esz;
         else
           row = (const char*)draft + ((l - 1) * layer_stride + frow * ld) * esz;
         frow++;
@@ -646,7 +648,9 @@ int orc_baseline_step(const orc_config* cfg, const void* draft, int64_t ld, cons
       const int64_t l0 = na;
       for (int i = 0; i < nf; i++) {
         const int32_t u = efront[i];
-        const char* row = (const char*)draft + ((int64_t)r * T + u) * ld * esz;
+        const char* row = cfg->row_mode == ORC_ROWS_POSITION /* DFLASH position rows */
+                              ? (const char*)draft + ((int64_t)r * d + (l - 1)) * ld * esz
+                              : (const char*)draft + ((int64_t)r * T + u) * ld * esz;
         rc = orc_topk_softmax(row, cfg->dtype, V, k, topi, topp, NULL, NULL);
         if (rc) goto done;
         for (int j = 0; j < k; j++) {

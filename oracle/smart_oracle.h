@@ -31,7 +31,7 @@ enum { ORC_PREFIX = 0, ORC_FROZEN = 1 };       /* Q7  */
 enum { ORC_NODE_SUM = 0, ORC_PATH_MEAN = 1 };  /* Q11 */
 enum { ORC_DERIVATIVE = 0, ORC_DIFFERENCE = 1 };/* Q5  */
 enum { ORC_BF16 = 0, ORC_FP32 = 1 };
-enum { ORC_ROWS_NODE = 0, ORC_ROWS_FRONTIER = 1, ORC_ROWS_KARY = 2 };
+enum { ORC_ROWS_NODE = 0, ORC_ROWS_FRONTIER = 1, ORC_ROWS_KARY = 2, ORC_ROWS_POSITION = 3 };
 
 typedef struct {
   int32_t V, k, d, W;          /* vocab, top-k, depth, frontier cap (0 = unlimited) */
@@ -71,6 +71,13 @@ int orc_topk_softmax(const void* row, int dtype, int V, int k,
  *                            ROWS_KARY:     row of the node whose path of top-k ranks gives heap
  *                                           index f (root 0, child j of f: f*k+j+1) at
  *                                           draft + (r*layer_stride + f)*ld  (tests only)
+ *                            ROWS_POSITION: DFLASH -- one non-autoregressive forward gives
+ *                                           independent per-position distributions; every frontier
+ *                                           node of request r at layer l expands with position row
+ *                                           l: draft + (r*layer_stride + l-1)*ld, layer_stride =
+ *                                           position rows per request (>= d).  With selection
+ *                                           BASELINE and W >= g this is the paper's Cartesian
+ *                                           product pruned to the top-g by cumulative probability.
  * target: NODE layout [b][T][ld_t] or NULL (skip A8).
  * Output arrays are caller-allocated (sizes in oracle.py).  Returns 0 ok,
  * 1 invalid config, 2 invalid logits (NaN/+inf). */
