@@ -68,8 +68,15 @@ typedef enum { SMART_COST_GLOBAL = 0, SMART_COST_LOCAL = 1 } smart_cost_scope;/*
  *  FRONTIER: row i of d_logits belongs to frontier entry i (request-major, canonical order),
  *            i.e. what a real draft forward over the packed frontier produces.
  *  NODE:     row (r, u) lives at d_logits + (r*tree_capacity + u)*ld: one pool per step,
- *            each node's row read when that node is expanded (bench / test layout). */
-typedef enum { SMART_ROWS_FRONTIER = 0, SMART_ROWS_NODE = 1 } smart_row_mode;
+ *            each node's row read when that node is expanded (bench / test layout).
+ *  POSITION: DFLASH (NEXT #4): one non-autoregressive draft forward gives
+ *            max_depth independent position distributions per request; every frontier node of
+ *            local request r at layer l expands with row d_logits + (r*max_depth + l-1)*ld
+ *            (pool [batch_local, max_depth, ld], passed to every smart_expand_step).  With
+ *            selection BASELINE and max_frontier >= floor(budget_verify / batch) this is the
+ *            paper's Cartesian product of per-position top-k pruned to the top-g by cum; with
+ *            PREFIX / FROZEN it is DFLASH+SMART. */
+typedef enum { SMART_ROWS_FRONTIER = 0, SMART_ROWS_NODE = 1, SMART_ROWS_POSITION = 2 } smart_row_mode;
 
 /* Cost-model constants (milliseconds): Eq.(4) C_draft = lambda*N + beta;
  * Eq.(5) C_verify = gamma*(exp(delta*N^rho)-1) + eta; Eq.(1) c_T = per-step AR cost. */

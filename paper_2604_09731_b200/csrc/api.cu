@@ -130,7 +130,7 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
     return bad("BASELINE needs max_frontier >= 1 and a single rank");
   if (c->selection < 0 || c->selection > 2 || c->accept_model < 0 || c->accept_model > 1 || c->marginal < 0 ||
       c->marginal > 1 || c->cost_scope < 0 || c->cost_scope > 1 || c->logits_dtype < 0 || c->logits_dtype > 1 ||
-      c->row_mode < 0 || c->row_mode > 1)
+      c->row_mode < 0 || c->row_mode > 2)
     return bad("enum field out of range");
   int B = c->budget_verify / c->batch_global;
   if (B < 1) return bad("per-request budget floor(budget_verify / batch_global) < 1");
@@ -393,7 +393,17 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   if (getenv("SMART_VERBOSE"))
     fprintf(stderr, "[smart] grid_expand %d (layer smem %zu B) grid_verify %d select_smem %zu B fused %d\n",
             c->grid_expand, layer_smem_bytes(P.cpr, P.k), c->grid_verify, c->select_smem, (int)c->fused_select);
-  mask_set_smem();
+  // per-step kernels' shared memory is sized from the config at create; a tree capacity whose
+  // mask or rerank scratch exceeds the per-CTA limit is a capacity error here, not a launch error
+  if (mask_smem_bytes(P.T) > 227 * 1024 ||
+      (P.selection == SMART_BASELINE && rerank_smem_bytes(P) > 227 * 1024)) {
+    const int Tcap = P.T;
+    cudaFree(c->ws);
+    cudaFree(c->cost_dev);
+    delete c;
+    return fail(nullptr, SMART_ECAPACITY, "tree capacity T = %d needs more than 227 KiB of mask/rerank scratch", Tcap);
+  }
+  mask_set_smem(P.T);
   if (P.selection == SMART_BASELINE) rerank_set_smem(rerank_smem_bytes(P));
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {

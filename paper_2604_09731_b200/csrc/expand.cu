@@ -400,6 +400,10 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       const int2 fe = rowfe(n, row);
       return logits + ((long long)fe.x * P.T + fe.y) * ld_bytes;
     }
+    if (P.row_mode == SMART_ROWS_POSITION) {  // DFLASH: the request's position-l row
+      const int2 fe = rowfe(n, row);
+      return logits + ((long long)fe.x * P.d + (layer - 1)) * ld_bytes;
+    }
     return logits + (long long)row * ld_bytes;
   };
 

@@ -554,12 +554,15 @@ void launch_rerank(const Params& P, cudaStream_t s) {
 
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok, int32_t* tree_len,
                  cudaStream_t s) {
-  const size_t smem = (size_t)32 * 3 * P.T * sizeof(int);
+  const size_t smem = mask_smem_bytes(P.T);
   launch_k(mask_kernel, dim3(1), dim3(1024), smem, s, P, mask, pos, parent, tok, tree_len);
 }
 
-cudaError_t mask_set_smem() {
-  return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 3 * 1024 * 4);
+size_t mask_smem_bytes(int T) { return (size_t)32 * 3 * T * sizeof(int); }
+
+cudaError_t mask_set_smem(int T) {
+  return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(mask_smem_bytes(T), 48 * 1024));
 }
 
 size_t verify_smem_bytes(int T) {

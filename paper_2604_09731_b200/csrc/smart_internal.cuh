@@ -340,7 +340,8 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
                    bool sample = false, float inv_tau = 1.f, unsigned long long seed = 0ull);
 size_t verify_smem_bytes(int T);
 int verify_occupancy();
-cudaError_t mask_set_smem();
+cudaError_t mask_set_smem(int T);
+size_t mask_smem_bytes(int T);
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
                             cudaStream_t s);
 

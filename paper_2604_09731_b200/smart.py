@@ -24,7 +24,7 @@ PREFIX, FROZEN, BASELINE = 0, 1, 2  # BASELINE: two-stage likelihood-maximising 
 NODE_SUM, PATH_MEAN = 0, 1
 DERIVATIVE, DIFFERENCE = 0, 1
 COST_GLOBAL, COST_LOCAL = 0, 1
-ROWS_FRONTIER, ROWS_NODE = 0, 1
+ROWS_FRONTIER, ROWS_NODE, ROWS_POSITION = 0, 1, 2  # POSITION: DFLASH rows
 MAX_DEPTH = 16
 
 EXPORTED = ["smart_query_sizes", "smart_create", "smart_nccl_unique_id", "smart_attach_nccl",
