@@ -674,7 +674,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     // short lists: one entry per thread.  fp64 prefix = 32-wide up-scan inside each tile of 32
     // entries plus the preceding tiles' totals in order (a function of the entry index only, so
     // any block size and any sharding give the same bits); the cut is the first failing entry
-    // (ballots), and argmax_j S_j is reduced here as well (tile winners, then in tile order).
+    // (ballots, then a warp min).  The prefixes are kept in the sort scratch so that the trace's
+    // argmax_j S_j is computed after the next frontier is published (off the critical path).
     const int j = tid;
     const bool act = j < ne;
     const double bj = act ? (double)sel_key_b(L.keys[j]) : 0.0;
@@ -687,60 +688,25 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     double excl = __shfl_up_sync(kFull, incl, 1);
     if (lane == 0) excl = 0.0;
     if (lane == 31 && tid < kA5Par) ss.tile_d[warp] = incl;
-    stamp(P, tid == 0, 15);
     blk_sync<NT>();
-    stamp(P, tid == 0, 16);
-    int ff = ne;
-    double bestS = -1.0;
-    int bestj = ne + 1;
     if (tid < kA5Par) {
       double before = 0.0;
       for (int w = 0; w < warp; ++w) before += ss.tile_d[w];  // tiles in order
       before += excl;
-      if (act) {
-        if (!rule_ok(bj, before, j)) ff = j;
-        bestS = sp(E0 + before + bj, j + 1);
-        bestj = j + 1;
-      }
-      stamp(P, tid == 0, 17);
-      const unsigned bal = __ballot_sync(kFull, ff < ne);
-      ff = bal ? warp * 32 + __ffs(bal) - 1 : ne;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(kFull, bestS, o);
-        const int oj = __shfl_xor_sync(kFull, bestj, o);
-        if (os > bestS || (os == bestS && oj < bestj)) {
-          bestS = os;
-          bestj = oj;
-        }
-      }
-      if (lane == 0) {
-        ss.wred_i[warp] = ff;
-        ss.wred_d[warp] = bestS;
-        ss.tile_i[warp] = bestj;
-      }
+      if (act) reinterpret_cast<double*>(L.keys2)[j] = before;
+      const unsigned bal = __ballot_sync(kFull, act && !rule_ok(bj, before, j));
+      if (lane == 0) ss.wred_i[warp] = bal ? warp * 32 + __ffs(bal) - 1 : ne;
     }
-    stamp(P, tid == 0, 18);
     blk_sync<NT>();
-    stamp(P, tid == 0, 19);
-    if (tid == 0) {
-      int js0 = ne, bj0 = 0;
-      double bs = sp(E0, 0);
-      for (int w = 0; w < (ne + 31) / 32; ++w) {
-        js0 = min(js0, ss.wred_i[w]);
-        const double os = ss.wred_d[w];
-        const int oj = ss.tile_i[w];
-        if (oj <= ne && (os > bs || (os == bs && oj < bj0))) {
-          bs = os;
-          bj0 = oj;
-        }
+    if (warp == 0) {
+      const int js0 = (int)__reduce_min_sync(kFull, (unsigned)(lane < (ne + 31) / 32 ? ss.wred_i[lane] : ne));
+      if (lane == 0) {
+        ss.bcast_i[3] = js0;
+        ss.bcast_i[5] = ne;
+        ss.bcast_i[6] = -2;  // argmax_j from the kept prefixes, in the tail
+        ss.bcast_l[0] = N0;
       }
-      ss.bcast_i[3] = js0;
-      ss.bcast_i[5] = ne;
-      ss.bcast_i[6] = bj0;  // argmax_j (the tail only sums the admitted benefits)
-      ss.bcast_l[0] = N0;
     }
-    stamp(P, tid == 0, 20);
   } else if (warp == 0) {
     // lane-contiguous chunks: sequential fp64 prefix inside a lane, warp scan of lane totals
     const int per = (ne + 31) >> 5;
@@ -959,7 +925,52 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       *P.E_glob = Ea;
     }
   }
-  if (warp == 1) {
+  if (warp == 1 && ss.bcast_i[6] == -2) {
+    // short lists: S_j from the prefixes the parallel A5 kept (same association as the cut)
+    const int ne_r = ss.bcast_i[5];
+    const long long N0r = ss.bcast_l[0];
+    const double* scr = reinterpret_cast<const double*>(L.keys2);
+    double bestS = sp(E0, 0);
+    int bestj = 0;
+    for (int j = lane; j < ne_r; j += 32) {
+      const double Sa = sp(E0 + scr[j] + (double)sel_key_b(L.keys[j]), j + 1);
+      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+        bestS = Sa;
+        bestj = j + 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_xor_sync(kFull, bestS, o);
+      const int oj = __shfl_xor_sync(kFull, bestj, o);
+      if (os > bestS || (os == bestS && oj < bestj)) {
+        bestS = os;
+        bestj = oj;
+      }
+    }
+    if (lane == 0) {
+      const double ab = js < ne_r ? scr[js] : (ne_r > 0 ? scr[ne_r - 1] + (double)sel_key_b(L.keys[ne_r - 1]) : 0.0);
+      const int R_all = (mode == kSelGlobal) ? ss.bcast_i[4] : R;
+      tr.executed = R_all > 0 ? 1 : 0;
+      tr.n_rows = R;
+      tr.n_cand = nct;
+      tr.n_elig = ne_r;
+      tr.n_admit = js;
+      tr.argmax_j = bestj;
+      tr.N0 = (int)N0r;
+      tr.E0 = E0;
+      tr.S0 = sp(E0, 0) / bc;
+      tr.dc0 = dc0;
+      tr.saturated = (N0r + ne_r >= P.sat_from) ? 1 : 0;
+      if (tr.saturated) atomicOr(P.err, kErrSaturated);
+      if (mode != kSelFull) {
+        const double Ea = E0 + ab;
+        tr.S_after = sp(Ea, js) / bc;
+        *P.N_glob = (int)(N0r + js);
+        *P.E_glob = Ea;
+      }
+    }
+  } else if (warp == 1) {
     const int ne_r = ss.bcast_i[5];
     const int argmax_pre = ss.bcast_i[6];  // long lists: already reduced by the A5 groups
     const long long N0r = ss.bcast_l[0];
