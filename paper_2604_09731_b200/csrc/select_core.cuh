@@ -773,7 +773,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     for (int u = 0; u < kPre; ++u)
       if (qr[u] >= 0) ppr[u] = P.path_sum[(size_t)L.rreq[qr[u] / k] * P.T + cdr[u].parent];
   }
+  stamp(P, tid == 0, 15);
   blk_sync<NT>();  // B6
+  stamp(P, tid == 0, 16);
   auto bits_below = [&](int r, int c) {  // admitted candidates of r with index < c
     int n = 0;
     for (int w = 0; w < (c >> 5); ++w) n += __popc(L.bm[r * nbw + w]);
@@ -788,50 +790,77 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   auto finished_r = [&](int r, int a) {  // Alg.1 line 10
     return L.fin[r] || a == 0 || (!base && L.nd[r] + a >= P.B);
   };
-  for (int r = tid; r < bl && (!one_warp || warp == 0); r += NT) {
-    int a = 0;
-    for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
-    L.adm[r] = a;
-    const int nx = finished_r(r, a) ? 0 : a;
-    L.nxt[r] = nx;
-    L.base[r] = nx;
-    P.fr_cnt[npar][r] = nx;
-  }
   if (one_warp) {
+    // warp 0 alone: counts, offsets and the admitted candidates' frontier entries, then the
+    // flag (no block barrier on this path; the fence covers only warp 0's few stores)
     if (warp == 0) {
-      const int v = lane < bl ? L.base[lane] : 0;
-      int incl = v;
+      int nx = 0;
+      if (lane < bl) {
+        int a = 0;
+        for (int w = 0; w < nbw; ++w) a += __popc(L.bm[lane * nbw + w]);
+        L.adm[lane] = a;
+        nx = finished_r(lane, a) ? 0 : a;
+        L.nxt[lane] = nx;
+      }
+      int incl = nx;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(kFull, incl, o);
         if (lane >= o) incl += t;
       }
-      if (lane < bl) {
-        L.base[lane] = incl - v;
-        P.fr_off[npar][lane] = incl - v;
+      if (lane < bl) L.base[lane] = incl - nx;
+      __syncwarp();
+      stamp(P, tid == 0, 17);
+      for (int j = lane; j < js; j += 32) {
+        const unsigned long long key = L.keys[j];
+        const int r = sel_key_r(key) - P.b_off;
+        if (r < 0 || r >= bl || L.nxt[r] == 0) continue;
+        const int c = sel_key_c(key);
+        const int q = L.off[r] * k + c;
+        const int idx = bits_below(r, c);
+        P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+        P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
       }
+      if (lane < bl) P.fr_off[npar][lane] = incl - nx;
       if (lane == 31) *P.fr_total[npar] = incl;
+      __syncwarp();
+      stamp(P, tid == 0, 18);
+      if (lane == 0) publish_flag(&P.fr_ready[layer]);
+      stamp(P, tid == 0, 19);
     }
-    blk_sync<NT>();  // B7
+    blk_sync<NT>();  // B7: per-request counts and offsets for everyone
   } else {
+    for (int r = tid; r < bl; r += NT) {
+      int a = 0;
+      for (int w = 0; w < nbw; ++w) a += __popc(L.bm[r * nbw + w]);
+      L.adm[r] = a;
+      const int nx = finished_r(r, a) ? 0 : a;
+      L.nxt[r] = nx;
+      L.base[r] = nx;
+    }
     blk_sync<NT>();  // B7
     const int total = excl_scan_int<NT>(L.base, bl, ss);  // next-frontier offsets
     for (int r = tid; r < bl; r += NT) P.fr_off[npar][r] = L.base[r];
     if (tid == 0) *P.fr_total[npar] = total;
+    // (4) next frontier (own requests that continue), with the cum of each node for the row merge
+    for (int q = tid; q < nct; q += NT) {
+      const int r = L.rreq[q / k];
+      const int c = q - L.off[r] * k;
+      if (!((L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u) || L.nxt[r] == 0) continue;
+      const int idx = bits_below(r, c);
+      P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+      P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
+    }
+    blk_sync<NT>();  // B8: the next frontier is complete
+    if (tid == 0) publish_flag(&P.fr_ready[layer]);
   }
-  // (4) next frontier (own requests that continue), with the cum of each node for the row merge
+  // after the flag: state the next layer's streaming CTAs do not read
+  for (int r = tid; r < bl; r += NT) P.fr_cnt[npar][r] = L.nxt[r];
   for (int q = tid; q < nct; q += NT) {
     const int r = L.rreq[q / k];
     const int c = q - L.off[r] * k;
-    const int f = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
-    P.cand_adm[lbase + q] = f;
-    if (!f || L.nxt[r] == 0) continue;
-    const int idx = bits_below(r, c);
-    P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
-    P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
+    P.cand_adm[lbase + q] = (L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u;
   }
-  blk_sync<NT>();  // B8: the next frontier is complete
-  if (tid == 0) publish_flag(&P.fr_ready[layer]);
   stamp(P, tid == 0, 14);
   // (2) admitted candidates write their node (index among the request's admits in canonical
   // order = admit bits below) and stage cum / parent path sum for (3b)

@@ -230,7 +230,7 @@ __device__ __forceinline__ int warp_sum_i(int v) {
 // frontier-ready flag: one thread publishes after a CTA barrier (release, cumulative over the
 // barrier); pollers acquire.  A poll that never completes traps instead of hanging the device.
 __device__ __forceinline__ void publish_flag(int* f) {
-  asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.s32 [%0], 1;" ::"l"(f) : "memory");
+  asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(f) : "memory");
 }
 __device__ __forceinline__ void wait_flag(const int* f) {
   for (unsigned it = 0; ld_acquire_gpu(f) == 0; ++it) {

@@ -49,5 +49,5 @@ for rep in range(3):
             print("   merge cycles: Z", dd_(1, 2), "thresh+surv", dd_(2, 3), "rank+store", dd_(3, 4), "tail", dd_(4, 5), "arrive", dd_(5, 6))
             print("   select cycles: stage", dd_(9, 10), "elig+rank", dd_(10, 11), "sort", dd_(11, 12), "rule", dd_(12, 13),
                   "commit", dd_(13, 14), "tail", dd_(14, 22))
-            print("   A5 cycles: scan", dd_(12, 15), "bar", dd_(15, 16), "rule+div", dd_(16, 17), "argmax", dd_(17, 18),
-                  "bar", dd_(18, 19), "reduce", dd_(19, 20), "B5", dd_(20, 13))
+            print("   commit cycles: bitmaps", dd_(13, 15), "B6", dd_(15, 16), "counts+scan", dd_(16, 17),
+                  "frontier", dd_(17, 18), "fence+flag", dd_(18, 19), "B7", dd_(19, 14))
