@@ -26,8 +26,10 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
 }  // namespace
 
 __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32_t* root_pos) {
-  pdl_wait();
+  // trigger first: the layer-1 grid (264 clustered CTAs) starts launching while the previous
+  // step's tail drains; its griddepcontrol.wait still waits for this kernel's completion
   pdl_trigger();
+  pdl_wait();
   tl_start(P, 0);
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < P.b_loc) {
@@ -76,8 +78,8 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, MW = P.MW;
   tl_start(P, 52);
+  pdl_trigger();  // the verify grid may start launching during the last layer (it waits for us)
   pdl_wait();
-  pdl_trigger();
   tl_start(P, 20);
   // verify-row offsets: exclusive scan of n_nodes (rows of K4)
   {
@@ -561,6 +563,12 @@ void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent,
 size_t mask_smem_bytes(int T) { return (size_t)32 * 3 * T * sizeof(int); }
 
 cudaError_t mask_set_smem(int T) {
+  // every kernel of the step asks for the maximum shared-memory carveout, so consecutive kernels
+  // never wait for an SM's L1/shared split to be reconfigured
+  cudaFuncSetAttribute(mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(begin_step_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)std::max<size_t>(mask_smem_bytes(T), 48 * 1024));
 }
@@ -572,6 +580,8 @@ size_t verify_smem_bytes(int T) {
 template <bool BF16, bool TMA, bool SAMPLE>
 static void verify_attr(int sm) {
   cudaFuncSetAttribute(verify_kernel<BF16, TMA, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(verify_kernel<BF16, TMA, SAMPLE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
 }
 
 int verify_occupancy() {

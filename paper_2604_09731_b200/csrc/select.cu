@@ -43,6 +43,9 @@ size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nra
 size_t select_rec_bytes(int nc_cap) { return sel_rec_bytes(nc_cap); }
 
 cudaError_t select_set_smem(size_t bytes) {
+  cudaFuncSetAttribute(select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(export_frontier_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
