@@ -306,6 +306,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.vrow_off, (b + 1) * 4);
   add(&P.vrow_rn, vrows * 8);
   add(&P.req_done, b * 4);
+  add(&P.vbest, (long long)b * T * 8);
   size_t total = 0;
   for (auto& it : items) total += (it.bytes + 255) & ~size_t(255);
   e = cudaMalloc(&c->ws, total);
@@ -404,6 +405,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     return fail(nullptr, SMART_ECAPACITY, "tree capacity T = %d needs more than 227 KiB of mask/rerank scratch", Tcap);
   }
   mask_set_smem(P.T);
+  walk_set_smem(P.T);
   if (P.selection == SMART_BASELINE) rerank_set_smem(rerank_smem_bytes(P));
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {

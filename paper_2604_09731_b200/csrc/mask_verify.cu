@@ -17,6 +17,11 @@ __device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {  // pack
   asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+__device__ __forceinline__ uint32_t vkey_orderable(float f) {  // order-preserving float -> u32
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -350,107 +355,13 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
         bi = mi;
       }
     }
-    // ---- segment end: CTA best (warp 0, two reductions), one acq_rel arrival per CTA; warp 0
-    // alone then merges a completed row and walks a completed request while the other warps
-    // stream on (the per-warp bests are double-buffered by segment parity) ----
-    const int sb = seg & 1;
-    if (lane == 0) {
-      sh.wv[sb][warp] = bv;
-      sh.wi[sb][warp] = bi;
-    }
-    consumer_sync();
-    gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 0);
-    if (warp == 0) {
-      int last = 0;
-      {
-        const float v = lane < kConsumerWarps ? sh.wv[sb][lane] : -INFINITY;
-        const int ix = lane < kConsumerWarps ? sh.wi[sb][lane] : kIdxSentinel;
-        const float vb = warp_max_fast(v);
-        const int ib = (int)__reduce_min_sync(kFull, (unsigned)(v == vb ? ix : kIdxSentinel));
-        if (lane == 0) {
-          const size_t so = (size_t)row * cpr + c0;
-          P.vsegv[so] = vb;
-          P.vsegi[so] = ib;
-          P.vseglen[so] = nch;
-          const int old = atom_add_acq_rel_gpu(&P.row_done[row], nch);  // publish + acquire
-          last = (old + nch == cpr);
-        }
-        last = __shfl_sync(kFull, last, 0);
-      }
-      gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 1);
-      if (last) {
-      // row merge: one load wave over the row's segments, two warp reductions
-      float v = -INFINITY;
-      int ix = kIdxSentinel;
-      for (int c = lane; c < cpr; c += 32) {
-        const size_t so = (size_t)row * cpr + c;
-        const int sl = __ldcg(&P.vseglen[so]);
-        const float sv = __ldcg(&P.vsegv[so]);
-        const int si = __ldcg(&P.vsegi[so]);
-        if (sl > 0) {
-          if (better(sv, si, v, ix)) {
-            v = sv;
-            ix = si;
-          }
-          P.vseglen[so] = 0;
-        }
-      }
-      const float vb = warp_max_fast(v);
-      ix = (int)__reduce_min_sync(kFull, (unsigned)(v == vb ? ix : kIdxSentinel));
-      int rl = 0;
-      if (lane == 0) {
-        P.vrow_arg[(size_t)r * T + node] = ix;
-        P.row_done[row] = 0;
-        const int old = atom_add_acq_rel_gpu(&P.req_done[r], 1);
-        rl = (old + 1 == P.n_nodes[r]);
-      }
-      rl = __shfl_sync(kFull, rl, 0);
-      gstamp(P, blockIdx.x == 0 && lane == 0 && seg < 4, 110 + 4 * seg + 2);
-      if (rl) {
-        // greedy walk of request r: follow the child whose token is the target argmax.
-        // The request's tree (parent, token, row argmax) is staged in shared memory first.
-        const int n = P.n_nodes[r];
-        const int D = P.d > 0 ? P.d : 1;
-        int* s_par = sh.walk;
-        int* s_tok = sh.walk + T;
-        int* s_arg = sh.walk + 2 * T;
-        for (int j = lane; j < n; j += 32) {
-          s_par[j] = P.parent[(size_t)r * T + j];
-          s_tok[j] = P.tok[(size_t)r * T + j];
-          s_arg[j] = __ldcg(&P.vrow_arg[(size_t)r * T + j]);
-        }
-        __syncwarp();
-        int cur = 0, acc = 0, bon = -1;
-        for (;;) {
-          const int t = s_arg[cur];
-          int found = -1;
-          for (int j0 = cur + 1; j0 < n; j0 += 32) {
-            const int j = j0 + lane;
-            const bool f = j < n && s_par[j] == cur && s_tok[j] == t;
-            const unsigned bal = __ballot_sync(kFull, f);
-            if (bal) {
-              found = j0 + __ffs(bal) - 1;
-              break;
-            }
-          }
-          if (found < 0) {
-            bon = t;
-            break;
-          }
-          if (lane == 0 && accept_path && acc < D) accept_path[(size_t)r * D + acc] = found;
-          ++acc;
-          cur = found;
-        }
-        if (lane == 0) {
-          if (accept_len) accept_len[r] = acc;
-          if (bonus) bonus[r] = bon;
-          atomicAdd(P.sum_accept, (unsigned long long)acc);
-          P.req_done[r] = 0;
-        }
-        if (accept_path)
-          for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;
-      }
-      }
+    // ---- segment end: every warp posts its best (value desc, index asc) as one 64-bit key with
+    // a fire-and-forget red.max on the row's slot; the walk runs in verify_walk_kernel once the
+    // grid has completed (no arrivals, merges or barriers here) ----
+    if (lane == 0 && bi != kIdxSentinel) {
+      const unsigned long long key = ((unsigned long long)vkey_orderable(bv) << 32) | (0xffffffffu - (unsigned)bi);
+      asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(P.vbest + (size_t)r * T + node), "l"(key)
+                   : "memory");
     }
     gstamp(P, blockIdx.x == 0 && tid == 0 && seg < 4, 110 + 4 * seg + 3);
     q += nch;
@@ -460,6 +371,65 @@ verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int
   if (nanf) atomicOr(P.err, kErrTargetNaN);
   tl_end(P, 21);
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[256 + blockIdx.x] = gtime();  // per-CTA end (debug timeline)
+}
+
+// A8 walk: one warp per request.  The request's tree (parent, token) is staged in shared
+// memory before the dependency wait (the tree is final: the verify grid launched this kernel only
+// after its own wait on the mask kernel); after the verify grid completes, the row keys give the
+// target argmax of every node; the slots are cleared for the next step.
+__global__ void __launch_bounds__(1024) verify_walk_kernel(Params P, int32_t* accept_len, int32_t* accept_path,
+                                                           int32_t* bonus) {
+  extern __shared__ int s_walk[];  // [32 warps][3 * T]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + warp;
+  const int T = P.T;
+  int* s_par = s_walk + warp * 3 * T;
+  int* s_tok = s_par + T;
+  int* s_arg = s_tok + T;
+  const int n = r < P.b_loc ? P.n_nodes[r] : 0;
+  for (int j = lane; j < n; j += 32) {
+    s_par[j] = P.parent[(size_t)r * T + j];
+    s_tok[j] = P.tok[(size_t)r * T + j];
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (r >= P.b_loc) return;
+  for (int j = lane; j < n; j += 32) {
+    unsigned long long* slot = P.vbest + (size_t)r * T + j;
+    const unsigned long long key = __ldcg(slot);
+    s_arg[j] = (int)(0xffffffffu - (uint32_t)key);
+    *slot = 0ull;
+  }
+  __syncwarp();
+  const int D = P.d > 0 ? P.d : 1;
+  int cur = 0, acc = 0, bon = -1;
+  for (;;) {
+    const int t = s_arg[cur];
+    int found = -1;
+    for (int j0 = cur + 1; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const bool f = j < n && s_par[j] == cur && s_tok[j] == t;
+      const unsigned bal = __ballot_sync(kFull, f);
+      if (bal) {
+        found = j0 + __ffs(bal) - 1;
+        break;
+      }
+    }
+    if (found < 0) {
+      bon = t;
+      break;
+    }
+    if (lane == 0 && accept_path && acc < D) accept_path[(size_t)r * D + acc] = found;
+    ++acc;
+    cur = found;
+  }
+  if (lane == 0) {
+    if (accept_len) accept_len[r] = acc;
+    if (bonus) bonus[r] = bon;
+    atomicAdd(P.sum_accept, (unsigned long long)acc);
+  }
+  if (accept_path)
+    for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;
 }
 
 }  // namespace
@@ -621,6 +591,17 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
   const char* t = static_cast<const char*>(target);
   if (sample) launch_verify_t<true>(P, t, ld_bytes, tma, accept_len, accept_path, bonus, grid, s, inv_tau, seed);
   else launch_verify_t<false>(P, t, ld_bytes, tma, accept_len, accept_path, bonus, grid, s, inv_tau, seed);
+  launch_k(verify_walk_kernel, dim3((P.b_loc + 31) / 32), dim3(1024), walk_smem_bytes(P.T), s, P, accept_len,
+           accept_path, bonus);
+}
+
+size_t walk_smem_bytes(int T) { return (size_t)32 * 3 * T * sizeof(int); }
+
+cudaError_t walk_set_smem(int T) {
+  cudaFuncSetAttribute(verify_walk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  return cudaFuncSetAttribute(verify_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)std::max<size_t>(walk_smem_bytes(T), 48 * 1024));
 }
 
 }  // namespace smart

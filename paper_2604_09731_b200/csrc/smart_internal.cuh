@@ -120,6 +120,7 @@ struct Params {
   int* vrow_off;      // [b_loc+1]
   int2* vrow_rn;      // [b_loc*T] (request, node) of each verify row (written by the mask kernel)
   int* req_done;      // [b_loc]
+  unsigned long long* vbest;  // [b_loc*T] target argmax key of each tree row (red.max; cleared by the walk)
 
   // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----
   // per-rank record: keys[m_cap] u64 | E_r[b_loc] f64 | hdr[b_loc] n_r, hdr[b_loc] = count
@@ -339,6 +340,8 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
                    int32_t* accept_len, int32_t* accept_path, int32_t* bonus, int grid, cudaStream_t s,
                    bool sample = false, float inv_tau = 1.f, unsigned long long seed = 0ull);
 size_t verify_smem_bytes(int T);
+size_t walk_smem_bytes(int T);
+cudaError_t walk_set_smem(int T);
 int verify_occupancy();
 cudaError_t mask_set_smem(int T);
 size_t mask_smem_bytes(int T);
