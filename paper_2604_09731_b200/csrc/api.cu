@@ -396,7 +396,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
             c->grid_expand, layer_smem_bytes(P.cpr, P.k), c->grid_verify, c->select_smem, (int)c->fused_select);
   // per-step kernels' shared memory is sized from the config at create; a tree capacity whose
   // mask or rerank scratch exceeds the per-CTA limit is a capacity error here, not a launch error
-  if (mask_smem_bytes(P.T) > 227 * 1024 ||
+  if (mask_smem_bytes(P.T, P.b_loc) > 227 * 1024 ||
       (P.selection == SMART_BASELINE && rerank_smem_bytes(P) > 227 * 1024)) {
     const int Tcap = P.T;
     cudaFree(c->ws);
@@ -404,7 +404,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     delete c;
     return fail(nullptr, SMART_ECAPACITY, "tree capacity T = %d needs more than 227 KiB of mask/rerank scratch", Tcap);
   }
-  mask_set_smem(P.T);
+  mask_set_smem(P.T, P.b_loc);
   walk_set_smem(P.T);
   if (P.selection == SMART_BASELINE) rerank_set_smem(rerank_smem_bytes(P));
   e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));

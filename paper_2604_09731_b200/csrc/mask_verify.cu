@@ -78,15 +78,31 @@ namespace {
 // request's (parent, depth, token) arrays in shared memory, then walks ancestors on chip ----
 __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, int32_t* pos, int32_t* parent,
                                                     int32_t* tok, int32_t* tree_len) {
-  extern __shared__ int s_tree[];  // [32 warps][3 * T]
+  extern __shared__ int s_tree[];  // [32 warps][3 * T] staged trees, then [b_loc + 1] row offsets
   __shared__ int s_run[33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = P.T, MW = P.MW;
+  int* s_off = s_tree + 32 * 3 * T;
   tl_start(P, 52);
   pdl_trigger();  // the verify grid may start launching during the last layer (it waits for us)
   pdl_wait();
   tl_start(P, 20);
-  // verify-row offsets: exclusive scan of n_nodes (rows of K4)
+  int* sp = s_tree + (size_t)warp * 3 * T;
+  int* sd = sp + T;
+  int* st = sd + T;
+  // the warp's first request: its tree is staged while the row-offset scan runs
+  int n0 = 0, rp0 = 0;
+  if (warp < P.b_loc) {
+    const int r = warp;
+    n0 = P.n_nodes[r];
+    rp0 = P.root_pos[r];
+    for (int i = lane; i < n0; i += 32) {
+      sp[i] = P.parent[(size_t)r * T + i];
+      sd[i] = P.depth[(size_t)r * T + i];
+      st[i] = P.tok[(size_t)r * T + i];
+    }
+  }
+  // verify-row offsets: exclusive scan of n_nodes (rows of K4), kept in shared memory too
   {
     const int per = (P.b_loc + 1023) / 1024;
     const int b0 = tid * per, b1 = min(P.b_loc, b0 + per);
@@ -113,24 +129,29 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
     int run = s_run[warp] + incl - local;
     for (int r = b0; r < b1; ++r) {
       P.vrow_off[r] = run;
+      s_off[r] = run;
       run += P.n_nodes[r];
     }
     if (tid == 0) P.vrow_off[P.b_loc] = s_run[32];
     __syncthreads();
   }
-  int* sp = s_tree + (size_t)warp * 3 * T;
-  int* sd = sp + T;
-  int* st = sd + T;
   for (int r = warp; r < P.b_loc; r += 32) {
-    const int n = P.n_nodes[r];
-    const int rp = P.root_pos[r];
-    const int vo = P.vrow_off[r];
-    for (int i = lane; i < n; i += 32) {
-      sp[i] = P.parent[(size_t)r * T + i];
-      sd[i] = P.depth[(size_t)r * T + i];
-      st[i] = P.tok[(size_t)r * T + i];
-      P.vrow_rn[vo + i] = make_int2(r, i);  // verify row -> (request, node)
+    int n, rp;
+    if (r == warp) {  // staged above
+      n = n0;
+      rp = rp0;
+    } else {
+      __syncwarp();
+      n = P.n_nodes[r];
+      rp = P.root_pos[r];
+      for (int i = lane; i < n; i += 32) {
+        sp[i] = P.parent[(size_t)r * T + i];
+        sd[i] = P.depth[(size_t)r * T + i];
+        st[i] = P.tok[(size_t)r * T + i];
+      }
     }
+    const int vo = s_off[r];
+    for (int i = lane; i < n; i += 32) P.vrow_rn[vo + i] = make_int2(r, i);  // verify row -> (request, node)
     __syncwarp();
     for (int i = lane; i < T; i += 32) {
       const size_t o = (size_t)r * T + i;
@@ -155,7 +176,6 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
       }
     }
     if (lane == 0 && tree_len) tree_len[r] = n;
-    __syncwarp();
   }
   tl_end(P, 20);
 }
@@ -526,13 +546,13 @@ void launch_rerank(const Params& P, cudaStream_t s) {
 
 void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent, int32_t* tok, int32_t* tree_len,
                  cudaStream_t s) {
-  const size_t smem = mask_smem_bytes(P.T);
+  const size_t smem = mask_smem_bytes(P.T, P.b_loc);
   launch_k(mask_kernel, dim3(1), dim3(1024), smem, s, P, mask, pos, parent, tok, tree_len);
 }
 
-size_t mask_smem_bytes(int T) { return (size_t)32 * 3 * T * sizeof(int); }
+size_t mask_smem_bytes(int T, int b) { return ((size_t)32 * 3 * T + b + 1) * sizeof(int); }
 
-cudaError_t mask_set_smem(int T) {
+cudaError_t mask_set_smem(int T, int b) {
   // every kernel of the step asks for the maximum shared-memory carveout, so consecutive kernels
   // never wait for an SM's L1/shared split to be reconfigured
   cudaFuncSetAttribute(mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -540,7 +560,7 @@ cudaError_t mask_set_smem(int T) {
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(mask_smem_bytes(T), 48 * 1024));
+                              (int)std::max<size_t>(mask_smem_bytes(T, b), 48 * 1024));
 }
 
 size_t verify_smem_bytes(int T) {

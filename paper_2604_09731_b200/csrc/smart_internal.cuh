@@ -343,8 +343,8 @@ size_t verify_smem_bytes(int T);
 size_t walk_smem_bytes(int T);
 cudaError_t walk_set_smem(int T);
 int verify_occupancy();
-cudaError_t mask_set_smem(int T);
-size_t mask_smem_bytes(int T);
+cudaError_t mask_set_smem(int T, int b);
+size_t mask_smem_bytes(int T, int b);
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
                             cudaStream_t s);
 
