@@ -202,6 +202,8 @@ def main():
                     help="cost-model fixture: roofline-fitted (default) or measured on a B200 (NEXT #2)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-hbm-regime", action="store_true", help="skip the cfg5 layer-1 HBM-regime measurement")
+    ap.add_argument("--steps-only", action="store_true",
+                    help="profiling runs: skip the per-kernel breakdown, verify and T=1 extras after the timed steps")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -282,7 +284,8 @@ def main():
                 step(p, stream)
             graphs.append(g)
     torch.cuda.synchronize()
-    launches_per_step = 1 + wl["d"] + 2 + (2 * wl["d"] if world > 1 else 0)
+    # begin + d layer kernels + mask + verify stream + verify walk (+ 2 select kernels per layer when sharded)
+    launches_per_step = 1 + wl["d"] + 3 + (2 * wl["d"] if world > 1 else 0)
 
     def replay(i):
         if graphs:
@@ -322,7 +325,7 @@ def main():
 
     # ---- per-kernel timing (outside the timed region; events on the launching stream) ----
     kt = {"expand": [], "select": [], "mask": [], "verify": [], "begin": []}
-    reps = 20 if sharded is None else 0
+    reps = 20 if sharded is None and not args.steps_only else 0
     p = pools[0]
     for _ in range(reps):
         evs = []
@@ -351,6 +354,26 @@ def main():
         kt["select"].append(d_[2:2 + 2 * wl["d"]:2])
         kt["mask"].append(d_[-2])
         kt["verify"].append(d_[-1])
+    # A8 stream + walk back to back on the same tree (each walk clears its row slots, so repeated
+    # calls are valid): launch latency overlaps the previous call, so this approximates the
+    # kernels' own time (used for the verify roofline)
+    ver_rep = None
+    if reps:
+        o = p["out"]
+        nrep, ngraph = 10, 5
+        gv = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gv, stream=stream):
+            for _ in range(nrep):
+                ctx.verify_accept(p["target"], o["accept_len"], o["accept_path"], o["bonus"], stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            gv.replay()
+            e0.record(stream)
+            for _ in range(ngraph):
+                gv.replay()
+            e1.record(stream)
+        stream.synchronize()
+        ver_rep = e0.elapsed_time(e1) / (nrep * ngraph)
     # A8 at temperature 1 (NEXT #1) on the same tree, for the breakdown (not part of the step)
     ver_t1 = []
     for rep in range(reps):
@@ -399,6 +422,12 @@ def main():
                 "per_launch_bytes": dom["bytes"] / max(dom["launches"], 1),
                 "per_launch_ms": dom["ms_total"] / max(dom["launches"], 1), "peak_source": peak_src}
     step_alg_bytes = exp_bytes + ver_bytes
+    roof_verify = None
+    if ver_rep:
+        vg = ver_bytes / (ver_rep / 1e3) / 1e9
+        roof_verify = {"bound": "hbm", "kernel": "verify_kernel + verify_walk_kernel (A8), 10 back-to-back calls per CUDA graph, L2-warm (same 26 MB each call)",
+                       "achieved": vg, "peak": peak, "unit": "GB/s", "frac": vg / peak,
+                       "per_launch_bytes": ver_bytes, "per_launch_ms": ver_rep, "peak_source": peak_src}
 
     # ---- end-to-end through the public API with host buffers ----
     e2e = None
@@ -477,6 +506,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline,
             "roofline_hbm_regime": hbm,
+            "roofline_verify": roof_verify,
             "cpu_baseline": cpu,
             "step_breakdown_ms": {"begin": beg_ms, "expand_per_layer": [float(x) for x in exp_ms],
                                   "select_per_layer": [float(x) for x in sel_ms], "mask": mask_ms,
