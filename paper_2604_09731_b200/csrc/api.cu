@@ -252,9 +252,8 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   P.eta = cost->eta;
   P.c_T = cost->c_T;
 
-  const long long b = P.b_loc, T = P.T, cap = P.cap_rows, k = P.k, cpr = P.cpr, d = std::max(P.d, 1);
+  const long long b = P.b_loc, T = P.T, cap = P.cap_rows, k = P.k, d = std::max(P.d, 1);
   const long long vrows = b * T;
-  const long long rd = std::max(cap, vrows);
   // exchange sizing (used only with nranks > 1, allocated lazily in attach)
   // workspace carve
   struct Item {
@@ -282,10 +281,6 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     add(&P.fr_off[q], b * 4);
     add(&P.fr_total[q], 4);
   }
-  add(&P.ms, cap * cpr * kStreamWarps * 8);
-  add(&P.segkey, cap * cpr * k * 8);
-  add(&P.seglen, cap * cpr * 4);
-  add(&P.row_done, rd * 4);
   add(&P.layer_done, SMART_MAX_DEPTH * 4);
   add(&P.fr_ready, (SMART_MAX_DEPTH + 1) * 4);
   add(&P.rowstat, cap * 8);
@@ -299,13 +294,8 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.sum_accept, 8);
   add(&P.E_glob, 8);
   add(&P.N_glob, 4);
-  add(&P.vsegv, vrows * cpr * 4);
-  add(&P.vsegi, vrows * cpr * 4);
-  add(&P.vseglen, vrows * cpr * 4);
-  add(&P.vrow_arg, vrows * 4);
   add(&P.vrow_off, (b + 1) * 4);
   add(&P.vrow_rn, vrows * 8);
-  add(&P.req_done, b * 4);
   add(&P.vbest, (long long)b * T * 8);
   size_t total = 0;
   for (auto& it : items) total += (it.bytes + 255) & ~size_t(255);

@@ -182,9 +182,6 @@ __global__ void __launch_bounds__(1024) mask_kernel(Params P, uint32_t* mask, in
 
 struct VerifyShared {
   int2 rn[kStageRows];  // (request, node) of the CTA's first rows
-  float wv[2][kConsumerWarps];
-  int wi[2][kConsumerWarps];
-  int walk[1];  // [3 * T] staged (parent, token, argmax) of the walked request (dynamic tail)
 };
 
 
@@ -564,7 +561,8 @@ cudaError_t mask_set_smem(int T, int b) {
 }
 
 size_t verify_smem_bytes(int T) {
-  return (size_t)kVStages * kChunkBytes + sizeof(VPipe) + sizeof(VerifyShared) + (size_t)3 * T * 4;
+  (void)T;
+  return (size_t)kVStages * kChunkBytes + sizeof(VPipe) + sizeof(VerifyShared);
 }
 
 template <bool BF16, bool TMA, bool SAMPLE>

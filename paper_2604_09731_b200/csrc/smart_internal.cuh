@@ -79,10 +79,6 @@ struct Params {
   int* fr_total[2];   // [1]
 
   // ---- A1 streaming scratch ----
-  float2* ms;         // [cap_rows*cpr*8] per (chunk, warp) softmax partial (max, sum)
-  unsigned long long* segkey;  // [cap_rows*cpr*k] per-segment (at its first chunk) CTA top-k keys
-  int* seglen;        // [cap_rows*cpr] segment length in chunks (at its first chunk)
-  int* row_done;      // [max(cap_rows, b_loc*T)] arrival counters (self-resetting)
   int* layer_done;    // [SMART_MAX_DEPTH] rows merged per layer (self-resetting)
   int* fr_ready;      // [SMART_MAX_DEPTH + 1] frontier of layer l published (reset by begin_step)
   float2* rowstat;    // [cap_rows] (M, Z) of the last expanded layer
@@ -113,13 +109,8 @@ struct Params {
   int* N_glob;        // [1]
 
   // ---- verify scratch ----
-  float* vsegv;       // [b_loc*T*cpr]
-  int* vsegi;         // [b_loc*T*cpr]
-  int* vseglen;       // [b_loc*T*cpr]
-  int* vrow_arg;      // [b_loc*T]
   int* vrow_off;      // [b_loc+1]
   int2* vrow_rn;      // [b_loc*T] (request, node) of each verify row (written by the mask kernel)
-  int* req_done;      // [b_loc]
   unsigned long long* vbest;  // [b_loc*T] target argmax key of each tree row (red.max; cleared by the walk)
 
   // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----
