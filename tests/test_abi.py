@@ -71,7 +71,7 @@ def test_query_sizes_baseline(sm):
 
 @pytest.mark.parametrize("field,value", [("top_k", 0), ("top_k", 33), ("max_depth", 17), ("alpha", 0.0),
                                          ("alpha", 1.5), ("budget_verify", 0), ("vocab", 1),
-                                         ("selection", 3), ("bonus", 2)])
+                                         ("selection", 3), ("bonus", 2), ("row_mode", 3), ("row_mode", -1)])
 def test_validation_rejects(sm, field, value):
     cfg = sm.Config(vocab=1000, top_k=4, max_depth=4, batch_local=2, budget_verify=16)
     setattr(cfg, field, value)
@@ -107,3 +107,31 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(//|#).*", "", txt).lower() or f == "smart_internal.cuh", f
+
+
+def test_position_row_mode_accepted(sm):
+    """NEXT #4 DFLASH rows: SMART_ROWS_POSITION is a valid row mode for SMART and BASELINE."""
+    for sel in (sm.PREFIX, sm.BASELINE):
+        cfg = sm.Config(vocab=1000, top_k=4, max_depth=3, max_frontier=4, batch_local=2, budget_verify=16,
+                        selection=sel, row_mode=sm.ROWS_POSITION)
+        assert sm.query_sizes(cfg)["T"] >= 1
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference prints one JSON line with the contract's keys (the fp64 oracle on
+    the host cores; CPU only)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--workload", "cfg2_llama8b_b1"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
