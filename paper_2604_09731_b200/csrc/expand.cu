@@ -441,7 +441,8 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
                        blockIdx.x == 0 && lane == 0 && n == 0);
         stamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 5);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 25);
-        if (lane < t) mbar_arrive_cluster(mapa_rank(&sh.freeb[b], lrank + lane), 1);  // buffer b is free
+        // buffer b is free again (only awaited when the team streams another row into it)
+        if (lane < t && n + 2 < nrows) mbar_arrive_cluster(mapa_rank(&sh.freeb[b], lrank + lane), 1);
         if (lane == 0) {
           red_add_release_gpu(&P.layer_done[layer - 1], 1);  // row done (the select CTA polls)
           stamp(P, blockIdx.x == 0 && n == 0, 6);
