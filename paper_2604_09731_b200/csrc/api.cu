@@ -283,7 +283,6 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   }
   add(&P.layer_done, SMART_MAX_DEPTH * 4);
   add(&P.fr_ready, (SMART_MAX_DEPTH + 1) * 4);
-  add(&P.rowstat, cap * 8);
   add(&P.cand, d * cap * k * sizeof(Cand));
   add(&P.cand_b, d * cap * k * 4);
   add(&P.cand_adm, d * cap * k * 4);

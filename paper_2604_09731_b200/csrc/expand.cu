@@ -234,7 +234,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
     if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
   }
   const float Z = warp_sum(z);
-  const float rZ = 1.0f / Z;
+  const float rZ = __frcp_rn(Z);  // correctly rounded 1/Z (no division slow path)
   stamp(P, pr, 2);
   // (2) threshold: best tail over the members' lists
   const int kp = list_stride(k);
@@ -289,7 +289,6 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
   stamp(P, pr, 4);
   if (lane == 0) {
     P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, slot);
-    P.rowstat[row] = make_float2(M, Z);
     if (!(Z >= 1.0f) || isinf(Z) || isnan(M)) atomicOr(P.err, kErrDraftNaN);  // Q23
   }
   __syncwarp();

@@ -81,7 +81,6 @@ struct Params {
   // ---- A1 streaming scratch ----
   int* layer_done;    // [SMART_MAX_DEPTH] rows merged per layer (self-resetting)
   int* fr_ready;      // [SMART_MAX_DEPTH + 1] frontier of layer l published (reset by begin_step)
-  float2* rowstat;    // [cap_rows] (M, Z) of the last expanded layer
   Cand* cand;         // [d][cap_rows*k]
   float* cand_b;      // [d][cap_rows*k] benefit
   int* cand_adm;      // [d][cap_rows*k] admitted flag
