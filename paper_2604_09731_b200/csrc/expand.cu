@@ -224,15 +224,14 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
   // (1) softmax normaliser from the cpr per-chunk partials (each already combined over its 8
   // warps in fixed order by the member that streamed the chunk): M = max, Z = sum S_c exp(M_c - M)
   // in a fixed association (lane-strided, then the xor tree) -- a function of cpr only
-  float m = -INFINITY;
-  for (int q = lane; q < cpr; q += 32) m = fmaxf(m, ms[q].x);
-  const float M = warp_max_fast(m);
+  // (cpr <= 64: at most two partials per lane, loaded once; the sum stays lane-strided in order)
+  const float4 v0 = lane < cpr ? ms[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+  const float4 v1 = lane + 32 < cpr ? ms[lane + 32] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+  const float M = warp_max_fast(fmaxf(v0.x, v1.x));
   const float ML = M * kLog2e;
   float z = 0.f;
-  for (int q = lane; q < cpr; q += 32) {
-    const float4 v = ms[q];
-    if (v.y != 0.f || isnan(v.y)) z += v.y * ex2(fmaf(v.x, kLog2e, -ML));
-  }
+  z += (v0.y != 0.f || isnan(v0.y)) ? v0.y * ex2(fmaf(v0.x, kLog2e, -ML)) : 0.f;
+  z += (v1.y != 0.f || isnan(v1.y)) ? v1.y * ex2(fmaf(v1.x, kLog2e, -ML)) : 0.f;
   const float Z = warp_sum(z);
   const float rZ = __frcp_rn(Z);  // correctly rounded 1/Z (no division slow path)
   stamp(P, pr, 2);
@@ -270,6 +269,7 @@ __device__ void merge_row_team(const Params& P, int layer, int par, int row, int
     // one survivor per lane; rank by broadcast compares (no shared-memory loop)
     const unsigned long long mine = lane < ns ? surv[lane] : 0ull;
     int rank = 0;
+#pragma unroll 8
     for (int q = 0; q < ns; ++q) rank += (__shfl_sync(kFull, mine, q) > mine);
     if (lane < ns && rank < k) emit(mine, rank);
   } else {
