@@ -482,7 +482,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
       const float b = L.cb[q];
       int rank = 0;
-      for (int j = s0; j < s1 && rank < e_r; ++j) {
+#pragma unroll 4
+      for (int j = s0; j < s1; ++j) {  // no early exit: uniform trip counts, pipelined loads
         const float bj = L.cb[j];
         rank += (bj > b) || (bj == b && j < q);
       }
