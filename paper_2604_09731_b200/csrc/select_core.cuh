@@ -249,6 +249,13 @@ __host__ __device__ inline size_t sel_align(size_t x) { return (x + 15) & ~size_
 // staged candidate records (P.sel_rec): 16 B per candidate, after keys2
 __host__ __device__ inline size_t sel_rec_bytes(int nc_cap) { return (size_t)nc_cap * 16; }
 
+// bucket sort scratch for lists longer than 256 keys (2 x kSortBuckets ints, after the records)
+constexpr int kSortBucketBits = 12;
+constexpr int kSortBuckets = 1 << kSortBucketBits;
+__host__ __device__ inline size_t sel_bucket_bytes(int sort_cap) {
+  return sort_cap > 256 ? (size_t)2 * kSortBuckets * 4 : 0;
+}
+
 __host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks = 1,
                                                  int k = 1) {
   const int per_req = nc_cap / (b_loc > 0 ? b_loc : 1);  // wf * k
@@ -263,6 +270,7 @@ __host__ __device__ inline size_t sel_smem_bytes(int b_loc, int b_all, int sort_
   bytes += sel_align(((size_t)sort_cap + 2) * 16);
   bytes += sel_align((size_t)b_all * 8);
   bytes += (size_t)sort_cap * 16;
+  bytes += sel_bucket_bytes(sort_cap);  // (after the staged records, when those are present)
   (void)nranks;
   return bytes;
 }
@@ -386,6 +394,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       reinterpret_cast<char*>(L.E) + sel_align((size_t)b_all * 8));
   L.keys2 = L.keys + P.sort_cap;
   // optional staging of the layer's candidate records (when the scratch has room, P.sel_rec)
+  unsigned long long* const kbase = L.keys;  // keys | keys2 | staged records | sort buckets
   int4* const crec = P.sel_rec ? reinterpret_cast<int4*>(L.keys + 2 * (size_t)P.sort_cap) : nullptr;
   auto get_cand = [&](int q) {
     if (crec) {
@@ -497,7 +506,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   const int nsort = base ? 0 : (mode == kSelGlobal) ? P.nranks * P.m_cap : ne;
   if (base) {
     // the baseline admits every eligible candidate: no global order, no rule (Q32)
-  } else if (nsort <= 1024) {
+  } else if (nsort <= 256) {
     // rank sort (keys unique; padding ~0 keys sort to the end); two keys per shared load
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(L.keys);
     for (int i = tid; i < nsort; i += NT) {
@@ -518,12 +527,35 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     L.keys = L.keys2;
     L.keys2 = t;
   } else {
-    int P2 = 1;
-    while (P2 < nsort) P2 <<= 1;
-    for (int i = nsort + tid; i < P2; i += NT) L.keys[i] = ~0ull;
+    // long lists: bucket pass on the key's top 12 bits (benefit sign/exponent/3 mantissa bits,
+    // order-preserving), then each key's rank inside its bucket; keys are unique, so the result
+    // is exactly the sorted order (the bitonic network cost ~470 cycles per stage, 66 stages)
+    int* bcnt = reinterpret_cast<int*>(kbase + 2 * (size_t)P.sort_cap +
+                                       (P.sel_rec ? (size_t)P.cap_rows * P.k * 2 : 0));  // counts -> cursors
+    int* boff = bcnt + kSortBuckets;        // [kSortBuckets] exclusive offsets
+    for (int i = tid; i < kSortBuckets; i += NT) bcnt[i] = 0;
     blk_sync<NT>();
-    if (P2 <= 2 * NT) bitonic_sort_reg<NT>(L.keys, P2);
-    else bitonic_sort<NT>(L.keys, P2);
+    for (int i = tid; i < nsort; i += NT) atomicAdd(&bcnt[(int)(L.keys[i] >> (64 - kSortBucketBits))], 1);
+    blk_sync<NT>();
+    for (int i = tid; i < kSortBuckets; i += NT) boff[i] = bcnt[i];
+    blk_sync<NT>();
+    excl_scan_int<NT>(boff, kSortBuckets, ss);
+    for (int i = tid; i < kSortBuckets; i += NT) bcnt[i] = boff[i];
+    blk_sync<NT>();
+    for (int i = tid; i < nsort; i += NT) {
+      const unsigned long long key = L.keys[i];
+      L.keys2[atomicAdd(&bcnt[(int)(key >> (64 - kSortBucketBits))], 1)] = key;
+    }
+    blk_sync<NT>();
+    for (int p = tid; p < nsort; p += NT) {
+      const unsigned long long key = L.keys2[p];
+      const int bk = (int)(key >> (64 - kSortBucketBits));
+      const int b0 = boff[bk], b1 = bcnt[bk];  // the bucket's range in keys2
+      int rank = b0;
+      for (int q = b0; q < b1; ++q) rank += (L.keys2[q] < key);
+      L.keys[rank] = key;
+    }
+    blk_sync<NT>();
   }
   stamp(P, tid == 0, 12);
 
