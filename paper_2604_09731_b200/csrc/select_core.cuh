@@ -616,9 +616,9 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     N0 = ss.bcast_l[1];
     ne = ss.bcast_i[2];
   }
-  // long lists (>= 512 eligible): 8 warps, group-contiguous then lane-contiguous chunks; short
-  // lists: warp 0 alone.  Either way the fp64 association is a function of ne only.
-  const bool big = !base && ne >= 512;
+  // lists longer than kA5Par: the looped form of the short-list scan below (same association,
+  // a function of the entry index only)
+  const bool big = !base && ne > kA5Par;
   auto rule_ok = [&](double bj, double before, int j) {
     // Eq.(16), strict: alpha*c_T*b/dc > c_T*(omega*b + E)/cost, cross-multiplied (dc, cost > 0;
     // cost == 0 means S := 0, i.e. admit any positive benefit)
@@ -628,72 +628,63 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     return (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
   };
   if (big) {
-    constexpr int kA5 = 8;
-    const int gper = (ne + kA5 - 1) / kA5;
-    const int g0 = min(ne, warp * gper), g1 = min(ne, g0 + gper);
-    const int per = (gper + 31) >> 5;
-    const int j0 = min(g1, g0 + lane * per), j1 = min(g1, j0 + per);
-    double lt = 0.0, lex = 0.0;
-    if (warp < kA5) {
-      for (int j = j0; j < j1; ++j) lt += (double)sel_key_b(L.keys[j]);
-      lex = lt;
+    // long lists: fp64 prefix = 32-wide up-scan inside each tile of 32 entries plus the
+    // exclusive prefix of the tile totals (lane-contiguous groups of tiles, then a warp
+    // up-scan: a function of the list length only); the cut is the smallest failing index
+    // (ballot per tile, shared min)
+    double* scr = reinterpret_cast<double*>(L.keys2);
+    const int ntile = (ne + 31) / 32;  // <= 128 (tile_d holds 260)
+    if (tid == 0) ss.bcast_i[3] = ne;
+    for (int t = warp; t < ntile; t += NT / 32) {
+      const int j = t * 32 + lane;
+      const double bj = j < ne ? (double)sel_key_b(L.keys[j]) : 0.0;
+      double incl = bj;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(kFull, lex, o);
-        if (lane >= o) lex += u;
+        const double u = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += u;
       }
-      if (lane == 31) ss.tile_d[warp] = lex;  // group total
-      lex -= lt;
+      double excl = __shfl_up_sync(kFull, incl, 1);
+      if (lane == 0) excl = 0.0;
+      if (j < ne) scr[j] = excl;
+      if (lane == 31) ss.tile_d[t] = incl;
     }
     blk_sync<NT>();
-    if (warp < kA5) {
-      double before = lex;
-      for (int w = 0; w < warp; ++w) before += ss.tile_d[w];  // groups in order
-      int ff = ne;
-      double bestS = -1.0;
-      int bestj = ne + 1;
-      for (int j = j0; j < j1; ++j) {
-        const double bj = (double)sel_key_b(L.keys[j]);
-        if (ff == ne && !rule_ok(bj, before, j)) ff = j;
-        const double Sa = sp(E0 + before + bj, j + 1);
-        if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
-          bestS = Sa;
-          bestj = j + 1;
-        }
-        before += bj;
-      }
-      ff = __reduce_min_sync(kFull, ff);
+    if (warp == 0) {  // tile totals -> exclusive prefixes: lane-contiguous groups, warp up-scan
+      const int per = (ntile + 31) >> 5;
+      const int t0 = min(ntile, lane * per), t1 = min(ntile, t0 + per);
+      double loc = 0.0;
+      for (int t = t0; t < t1; ++t) loc += ss.tile_d[t];
+      double inc = loc;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(kFull, bestS, o);
-        const int oj = __shfl_xor_sync(kFull, bestj, o);
-        if (os > bestS || (os == bestS && oj < bestj)) {
-          bestS = os;
-          bestj = oj;
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += u;
       }
-      if (lane == 0) {
-        ss.wred_i[warp] = ff;
-        ss.wred_d[warp] = bestS;
-        ss.tile_i[warp] = bestj;
+      double run = __shfl_up_sync(kFull, inc, 1);
+      if (lane == 0) run = 0.0;
+      for (int t = t0; t < t1; ++t) {
+        const double v = ss.tile_d[t];
+        ss.tile_d[t] = run;
+        run += v;
       }
     }
     blk_sync<NT>();
-    if (warp == 0 && lane == 0) {
-      int js0 = ne, bj = 0;
-      double bs = sp(E0, 0);
-      for (int w = 0; w < kA5; ++w) {
-        js0 = min(js0, ss.wred_i[w]);
-        const double os = ss.wred_d[w];
-        const int oj = ss.tile_i[w];
-        if (oj <= ne && (os > bs || (os == bs && oj < bj))) {
-          bs = os;
-          bj = oj;
-        }
+    for (int t = warp; t < ntile; t += NT / 32) {
+      const int j = t * 32 + lane;
+      bool fail = false;
+      if (j < ne) {
+        const double before = ss.tile_d[t] + scr[j];
+        scr[j] = before;
+        fail = !rule_ok((double)sel_key_b(L.keys[j]), before, j);
       }
-      ss.bcast_i[3] = js0;
+      const unsigned bal = __ballot_sync(kFull, fail);
+      if (bal && lane == 0) atomicMin(&ss.bcast_i[3], t * 32 + __ffs(bal) - 1);
+    }
+    blk_sync<NT>();
+    if (tid == 0) {
       ss.bcast_i[5] = ne;
-      ss.bcast_i[6] = bj;  // argmax_j, reported by warp 1 in the tail
+      ss.bcast_i[6] = -2;  // argmax_j from the kept prefixes, in the tail
       ss.bcast_l[0] = N0;
     }
   } else if (base) {
@@ -987,14 +978,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       *P.E_glob = Ea;
     }
   }
-  if (warp == 1 && ss.bcast_i[6] == -2) {
-    // short lists: S_j from the prefixes the parallel A5 kept (same association as the cut)
+  const bool wide_argmax = ss.bcast_i[6] == -2 && ss.bcast_i[5] > kA5Par;
+  if (wide_argmax) {
+    // long lists: S_j over all threads (one fp64 division each), per-warp winners in smem
     const int ne_r = ss.bcast_i[5];
-    const long long N0r = ss.bcast_l[0];
     const double* scr = reinterpret_cast<const double*>(L.keys2);
-    double bestS = sp(E0, 0);
-    int bestj = 0;
-    for (int j = lane; j < ne_r; j += 32) {
+    double bestS = -1.0;
+    int bestj = ne_r + 1;
+    for (int j = tid; j < ne_r; j += NT) {
       const double Sa = sp(E0 + scr[j] + (double)sel_key_b(L.keys[j]), j + 1);
       if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
         bestS = Sa;
@@ -1008,6 +999,45 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       if (os > bestS || (os == bestS && oj < bestj)) {
         bestS = os;
         bestj = oj;
+      }
+    }
+    if (lane == 0) {
+      ss.wred_d[warp] = bestS;
+      ss.tile_i[warp] = bestj;
+    }
+    blk_sync<NT>();
+  }
+  if (warp == 1 && ss.bcast_i[6] == -2) {
+    // short lists: S_j from the prefixes the parallel A5 kept (same association as the cut)
+    const int ne_r = ss.bcast_i[5];
+    const long long N0r = ss.bcast_l[0];
+    const double* scr = reinterpret_cast<const double*>(L.keys2);
+    double bestS = sp(E0, 0);
+    int bestj = 0;
+    for (int j = wide_argmax ? ne_r : lane; j < ne_r; j += 32) {
+      const double Sa = sp(E0 + scr[j] + (double)sel_key_b(L.keys[j]), j + 1);
+      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+        bestS = Sa;
+        bestj = j + 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_xor_sync(kFull, bestS, o);
+      const int oj = __shfl_xor_sync(kFull, bestj, o);
+      if (os > bestS || (os == bestS && oj < bestj)) {
+        bestS = os;
+        bestj = oj;
+      }
+    }
+    if (wide_argmax && lane == 0) {
+      for (int w = 0; w < NT / 32; ++w) {  // warp winners in warp order
+        const double os = ss.wred_d[w];
+        const int oj = ss.tile_i[w];
+        if (oj <= ne_r && (os > bestS || (os == bestS && oj < bestj))) {
+          bestS = os;
+          bestj = oj;
+        }
       }
     }
     if (lane == 0) {
