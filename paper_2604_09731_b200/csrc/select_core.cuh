@@ -714,8 +714,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
     if (lane == 31 && tid < kA5Par) ss.tile_d[warp] = incl;
     blk_sync<NT>();
     if (tid < kA5Par) {
+      // preceding tiles' totals in order (the loads issued together, the adds predicated)
+      double tv[kA5Par / 32];
+#pragma unroll
+      for (int w = 0; w < kA5Par / 32; ++w) tv[w] = ss.tile_d[w];
       double before = 0.0;
-      for (int w = 0; w < warp; ++w) before += ss.tile_d[w];  // tiles in order
+#pragma unroll
+      for (int w = 0; w < kA5Par / 32; ++w)
+        if (w < warp) before += tv[w];
       before += excl;
       if (act) reinterpret_cast<double*>(L.keys2)[j] = before;
       const unsigned bal = __ballot_sync(kFull, act && !rule_ok(bj, before, j));
