@@ -137,7 +137,8 @@ typedef struct {
 typedef struct {
   int32_t layers_executed;
   int32_t error_flags;    /* bit0: NaN/+inf/all--inf draft row; bit1: NaN target row;
-                             bit2: cost saturation seen                                    */
+                             bit2: cost saturation seen; bit3: a device-side wait timed out
+                             (calls out of order / a broken launch sequence)               */
   int64_t nodes_local;    /* sum over local requests of drafted nodes                      */
   int64_t accepted_local; /* sum of accept lengths (after smart_verify_accept)              */
   double E_global, S_final;

@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with plain gcc -O2 (no intrinsics, no -ffast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "smart_oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O2", "-std=gnu99", "-fopenmp", "-Wall", "-fPIC", "-shared",
                                "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
@@ -50,7 +50,7 @@ class _Cfg(C.Structure):
                 ("b", C.c_int32), ("B_verify", C.c_int32), ("alpha", C.c_double),
                 ("omega", C.c_int32), ("selection", C.c_int32), ("accept_model", C.c_int32),
                 ("marginal", C.c_int32), ("dtype", C.c_int32), ("row_mode", C.c_int32),
-                ("T", C.c_int32), ("margin_eps", C.c_double)]
+                ("T", C.c_int32), ("margin_eps", C.c_double), ("b_budget", C.c_int32)]
 
 
 _lib = None
@@ -84,6 +84,8 @@ def lib():
         L.orc_hash.restype = C.c_uint64
         L.orc_uniform.argtypes = [C.c_uint64, i64, i64, i64]
         L.orc_uniform.restype = d
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_set_threads.restype = None
         _lib = L
     return _lib
 
@@ -119,11 +121,12 @@ class Config:
     dtype: int = BF16
     row_mode: int = ROWS_NODE
     T: int = 0                 # 0 -> derived: 1 + min(B, d*W)
-    margin_eps: float = 1e-4
+    margin_eps: float = 1e-5   # Q24: decisions closer than 1e-5 are tie-ambiguous
+    b_budget: int = 0          # requests sharing B_verify (0 = b); > b: LOCAL cost scope (Q34)
 
     @property
     def B(self) -> int:
-        return self.B_verify // self.b
+        return self.B_verify // (self.b_budget or self.b)
 
     def tmax(self) -> int:
         if self.T:
@@ -134,7 +137,7 @@ class Config:
     def c(self) -> _Cfg:
         return _Cfg(self.V, self.k, self.d, self.W, self.b, self.B_verify, self.alpha, self.omega,
                     self.selection, self.accept_model, self.marginal, self.dtype, self.row_mode,
-                    self.tmax(), self.margin_eps)
+                    self.tmax(), self.margin_eps, self.b_budget)
 
 
 def _ptr(a):
@@ -305,6 +308,11 @@ def step(cfg: Config, cost: Cost, draft: np.ndarray, target: np.ndarray | None =
         bonus=out["bonus"], trace=out["trace"].reshape(D, TRACE_F),
         cand_i=cand_i.reshape(D, capc, 5) if dump else None,
         cand_d=cand_d.reshape(D, capc, 3) if dump else None, summary=out["summary"], T=T)
+
+
+def set_threads(n: int) -> None:
+    """worker threads for the row-parallel parts (A1 rows, A8 requests); 1 = serial."""
+    lib().orc_set_threads(int(n))
 
 
 def uniform(seed: int, r: int, u: int, v: int) -> float:

@@ -24,6 +24,9 @@
 
 #define EXP_CLAMP 700.0 /* S:133, Q17 */
 
+static int g_threads = 1;
+void orc_set_threads(int n) { g_threads = n > 0 ? n : 1; }
+
 /* ------------------------------------------------------------------------ */
 /* Cost model                                                                */
 /* ------------------------------------------------------------------------ */
@@ -225,7 +228,9 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
   int rc = 0, sat_any = 0, first_amb = 0, layers_exec = 0;
 
   if (b < 1 || k < 1 || k > V || d < 0 || T < 1 || cfg->alpha <= 0.0 || cfg->alpha > 1.0) return 1;
-  B = cfg->B_verify / b; /* Alg.1 line 1, floor (Q2) */
+  /* Alg.1 line 1, floor (Q2); b_budget > b: this batch is one replica's share of the
+   * b_budget requests the budget is split over (cost_scope LOCAL, Q34) */
+  B = cfg->B_verify / (cfg->b_budget > 0 ? cfg->b_budget : b);
   if (B < 1) return 1;
 
   /* per-request state: S_0 = {root}, A_0 = {root} */
@@ -235,8 +240,10 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
   int32_t* nact = calloc(b, sizeof(int32_t));
   int32_t* nact_next = calloc(b, sizeof(int32_t));
   int32_t* act_next = malloc(sizeof(int32_t) * b * T);
-  int32_t* topi = malloc(sizeof(int32_t) * k);
-  double* topp = malloc(sizeof(double) * k);
+  int32_t* topi = malloc(sizeof(int32_t) * k * ((int64_t)b * T + 1)); /* per frontier row */
+  double* topp = malloc(sizeof(double) * k * ((int64_t)b * T + 1));
+  const char** rowp = malloc(sizeof(char*) * ((int64_t)b * T + 1));
+  int* rowrc = malloc(sizeof(int) * ((int64_t)b * T + 1));
   int64_t cap = (int64_t)b * T * k + 1;
   cand_t* cand = malloc(sizeof(cand_t) * cap);
   cand_t** ord = malloc(sizeof(cand_t*) * cap);
@@ -259,7 +266,8 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
     double* tr = trace + (l - 1) * ORC_TRACE_F;
     int64_t nc = 0, rows = 0, frow = 0;
     int sat = 0;
-    /* ---- A1/A2: U_l(A_{l-1}) — top-k candidates of every frontier node ---- */
+    /* ---- A1/A2: U_l(A_{l-1}) — top-k candidates of every frontier node ----
+     * (rows are independent: their softmax/top-k may run on several threads, orc_set_threads) */
     for (r = 0; r < b; r++) {
       for (i = 0; i < nact[r]; i++) {
         int32_t u = act[r * T + i];
@@ -272,19 +280,33 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
           row = (const char*)draft + ((int64_t)r * layer_stride + (l - 1)) * ld * esz;
         else
           row = (const char*)draft + ((l - 1) * layer_stride + frow * ld) * esz;
+        rowp[frow] = row;
         frow++;
-        rc = orc_topk_softmax(row, cfg->dtype, V, k, topi, topp, NULL, NULL);
-        if (rc) goto done;
+      }
+    }
+    {
+      int64_t q;
+#pragma omp parallel for num_threads(g_threads) schedule(dynamic, 1) if (g_threads > 1)
+      for (q = 0; q < frow; q++)
+        rowrc[q] = orc_topk_softmax(rowp[q], cfg->dtype, V, k, topi + q * k, topp + q * k, NULL, NULL);
+      for (q = 0; q < frow; q++)
+        if (rowrc[q]) { rc = rowrc[q]; goto done; }
+    }
+    frow = 0;
+    for (r = 0; r < b; r++) {
+      for (i = 0; i < nact[r]; i++) {
+        int32_t u = act[r * T + i];
         for (j = 0; j < k; j++) {
           cand_t* c = &cand[nc++];
           c->r = (int32_t)r;
           c->parent = u;
-          c->tok = topi[j];
+          c->tok = topi[frow * k + j];
           c->c = (int32_t)(i * k + j);
-          c->p = topp[j];
-          c->cum = cum[r * T + u] * topp[j]; /* Eq.(3): cum(parent) * p */
+          c->p = topp[frow * k + j];
+          c->cum = cum[r * T + u] * topp[frow * k + j]; /* Eq.(3): cum(parent) * p */
           c->admitted = 0;
         }
+        frow++;
         rows++;
       }
     }
@@ -463,12 +485,15 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
     }
   }
 
-  /* ---- A8: greedy (T=0) tree verification walk (Q16) ---- */
+  /* ---- A8: greedy (T=0) tree verification walk (Q16); requests are independent ---- */
   int64_t sum_a = 0, sum_n = 0;
+  int nan_seen = 0;
+  for (r = 0; r < b; r++) sum_n += n[r];
+#pragma omp parallel for num_threads(g_threads) schedule(dynamic, 1) reduction(+ : sum_a) reduction(| : nan_seen) if (g_threads > 1)
   for (r = 0; r < b; r++) {
-    sum_n += n[r];
+    int64_t jj;
     accept_len[r] = 0;
-    for (i = 0; i < d; i++) accept_path[r * d + i] = -1;
+    for (jj = 0; jj < d; jj++) accept_path[r * d + jj] = -1;
     bonus[r] = -1;
     if (!target) continue;
     int32_t cur = 0;
@@ -476,14 +501,16 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
       const char* row = (const char*)target + ((int64_t)r * T + cur) * ld_t * esz;
       int64_t best = -1;
       double bx = 0.0;
-      for (j = 0; j < V; j++) {
-        double x = logit_at(row, cfg->dtype, j);
-        if (isnan(x)) { rc = 2; goto done; }
-        if (best < 0 || better_xi(x, j, bx, best)) { best = j; bx = x; }
+      int bad = 0;
+      for (jj = 0; jj < V; jj++) {
+        double x = logit_at(row, cfg->dtype, jj);
+        if (isnan(x)) { bad = 1; break; }
+        if (best < 0 || better_xi(x, jj, bx, best)) { best = jj; bx = x; }
       }
+      if (bad) { nan_seen = 1; break; }
       int32_t next = -1;
-      for (j = cur + 1; j < n_nodes[r]; j++)
-        if (parent[r * T + j] == cur && tok[r * T + j] == best) { next = (int32_t)j; break; }
+      for (jj = cur + 1; jj < n_nodes[r]; jj++)
+        if (parent[r * T + jj] == cur && tok[r * T + jj] == best) { next = (int32_t)jj; break; }
       if (next < 0) { bonus[r] = (int32_t)best; break; }
       accept_path[r * d + accept_len[r]] = next;
       accept_len[r]++;
@@ -491,6 +518,7 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
     }
     sum_a += accept_len[r];
   }
+  if (nan_seen) { rc = 2; goto done; }
 
   {
     double Ea = 0.0;
@@ -516,7 +544,7 @@ int orc_step(const orc_config* cfg, const orc_cost* cost,
 
 done:
   free(n); free(E); free(act); free(nact); free(nact_next); free(act_next);
-  free(topi); free(topp); free(cand); free(ord); free(elig); free(kid);
+  free(topi); free(topp); free(rowp); free(rowrc); free(cand); free(ord); free(elig); free(kid);
   return rc;
 }
 

@@ -42,7 +42,15 @@ typedef struct {
   int32_t selection, accept_model, marginal, dtype, row_mode;
   int32_t T;                   /* per-request node capacity incl. root (pool rows)  */
   double margin_eps;           /* relative margin below which a decision is flagged (Q24) */
+  int32_t b_budget;            /* requests sharing B_verify (the global batch, Q2): B =
+                                  floor(B_verify / b_budget); 0 = b.  With b_budget > b the
+                                  b requests are one replica's share, costed as their own
+                                  batch (cost_scope LOCAL, Q13 / DESIGN.md Q34)              */
 } orc_config;
+
+/* worker threads of the row-parallel parts (A1 softmax/top-k rows, A8 target argmax rows);
+ * 1 = serial (default).  Only the bench's all-cores baseline raises it. */
+void orc_set_threads(int n);
 
 /* ---- closed-form pieces (each pinned separately) ------------------------- */
 double orc_cost_draft(const orc_cost* c, double x);             /* Eq.(4) */

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -35,6 +36,7 @@ struct smart_ctx {
   size_t select_smem = 0;
   bool fused_select = true;  // selection runs in the layer kernel's last CTA
   bool no_early = false;     // SMART_NO_EARLY=1: every layer kernel waits for the previous grid
+  bool in_run_step = false;  // inside smart_run_step: the layer kernels are back to back (early start ok)
   double* cost_dev = nullptr;
   Params P{};
   void* ws = nullptr;      // single device allocation
@@ -142,6 +144,13 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
   }
   long long T = derive_T(c, B);
   if (T < 1 || T > 1024) return bad("tree capacity T must be in [1, 1024]");
+  if (c->selection != SMART_BASELINE && c->tree_capacity > 0) {
+    // every layer may admit up to min(B - n_r, W) nodes per request, so a tree can hold
+    // 1 + min(B, d * W) nodes; a smaller capacity would overflow the per-request arrays
+    const long long Wq = c->max_frontier > 0 ? c->max_frontier : (1ll << 30);
+    if (T < 1 + std::min<long long>(B, (long long)c->max_depth * Wq))
+      return bad("tree_capacity must be >= 1 + min(B, max_depth * max_frontier)");
+  }
   long long wf = frontier_width(c, B, T);
   if (c->selection == SMART_BASELINE && T < 1 + std::max<long long>(B, (long long)std::max(c->max_depth, 1) * c->max_frontier))
     return bad("BASELINE tree capacity must hold 1 + max(B, d * W) nodes");
@@ -165,6 +174,30 @@ smart_status validate(const smart_config* c, const smart_cost* k, smart_sizes* s
     s->chunk_elems = ce;
   }
   return SMART_OK;
+}
+
+// dynamic shared-memory attributes are per kernel function (process-wide), so every context
+// raises them to the largest size any live or earlier context needed; never lowers them
+std::mutex g_attr_mu;
+size_t g_attr_max[4] = {0, 0, 0, 0};  // mask, walk, rerank, select
+cudaError_t raise_attr(int which, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (bytes > g_attr_max[which]) g_attr_max[which] = bytes;
+  const size_t v = g_attr_max[which];
+  switch (which) {
+    case 0: return mask_set_smem_bytes(v);
+    case 1: return walk_set_smem_bytes(v);
+    case 2: return rerank_set_smem(v);
+    default: return select_set_smem(v);
+  }
+}
+
+// step calls may come from a thread whose current device differs from the context's
+inline cudaError_t use_device(const smart_ctx* c) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e == cudaSuccess && cur != c->device) e = cudaSetDevice(c->device);
+  return e;
 }
 
 int next_pow2(long long n) {
@@ -197,6 +230,19 @@ smart_status smart_query_sizes(const smart_config* cfg, smart_sizes* out) {
   smart_status st = validate(cfg, nullptr, out, why);
   if (st) return fail(nullptr, st, "%s", why.c_str());
   return SMART_OK;
+}
+
+// frees everything smart_create may have allocated (used by every failure path after the first
+// allocation and by smart_destroy)
+static void release_ctx(smart_ctx* c) {
+  if (!c) return;
+  if (c->ws) cudaFree(c->ws);
+  if (c->cost_dev) cudaFree(c->cost_dev);
+  if (c->P.dbg) cudaFree(c->P.dbg);
+  c->ws = nullptr;
+  c->cost_dev = nullptr;
+  c->P.dbg = nullptr;
+  delete c;
 }
 
 smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int device, smart_ctx** out) {
@@ -300,7 +346,8 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   for (auto& it : items) total += (it.bytes + 255) & ~size_t(255);
   e = cudaMalloc(&c->ws, total);
   if (e != cudaSuccess) {
-    delete c;
+    c->ws = nullptr;
+    release_ctx(c);
     return fail(nullptr, SMART_ECUDA, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
   }
   cudaMemset(c->ws, 0, total);
@@ -339,8 +386,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     e = cudaMalloc(&c->cost_dev, tab.size() * sizeof(double));
     if (e == cudaSuccess) e = cudaMemcpy(c->cost_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
-      cudaFree(c->ws);
-      delete c;
+      release_ctx(c);
       return fail(nullptr, SMART_ECUDA, "cost table: %s", cudaGetErrorString(e));
     }
     P.cost_tab = c->cost_dev;
@@ -375,9 +421,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   }
   c->fused_select = c->select_smem <= (size_t)kStages * kChunkBytes && c->grid_expand >= 16 && !getenv("SMART_NO_FUSE");
   if (c->select_smem > 220 * 1024) {
-    cudaFree(c->ws);
-    cudaFree(c->cost_dev);
-    delete c;
+    release_ctx(c);
     return fail(nullptr, SMART_ECAPACITY, "selection needs more than 220 KiB of shared memory");
   }
   if (getenv("SMART_VERBOSE"))
@@ -388,24 +432,20 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   if (mask_smem_bytes(P.T, P.b_loc) > 227 * 1024 ||
       (P.selection == SMART_BASELINE && rerank_smem_bytes(P) > 227 * 1024)) {
     const int Tcap = P.T;
-    cudaFree(c->ws);
-    cudaFree(c->cost_dev);
-    delete c;
+    release_ctx(c);
     return fail(nullptr, SMART_ECAPACITY, "tree capacity T = %d needs more than 227 KiB of mask/rerank scratch", Tcap);
   }
-  mask_set_smem(P.T, P.b_loc);
-  walk_set_smem(P.T);
-  if (P.selection == SMART_BASELINE) rerank_set_smem(rerank_smem_bytes(P));
-  e = select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024));
+  e = raise_attr(0, mask_smem_bytes(P.T, P.b_loc));
+  if (e == cudaSuccess) e = raise_attr(1, walk_smem_bytes(P.T));
+  if (e == cudaSuccess && P.selection == SMART_BASELINE) e = raise_attr(2, rerank_smem_bytes(P));
+  if (e == cudaSuccess) e = raise_attr(3, std::max<size_t>(c->select_smem, 48 * 1024));
   if (e != cudaSuccess) {
-    cudaFree(c->ws);
-    delete c;
-    return fail(nullptr, SMART_ECUDA, "select smem attribute: %s", cudaGetErrorString(e));
+    release_ctx(c);
+    return fail(nullptr, SMART_ECUDA, "shared-memory attributes: %s", cudaGetErrorString(e));
   }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
-    cudaFree(c->ws);
-    delete c;
+    release_ctx(c);
     return fail(nullptr, SMART_ECUDA, "init: %s", cudaGetErrorString(e));
   }
   *out = c;
@@ -460,7 +500,7 @@ static smart_status setup_exchange(smart_ctx* c, int rank, int nranks, void* sen
   if (need > 220 * 1024) return fail(c, SMART_ECAPACITY, "global selection needs %zu B shared memory", need);
   c->select_smem = std::max(c->select_smem, need);
   c->fused_select = false;
-  CUDA_TRY(c, select_set_smem(std::max<size_t>(c->select_smem, 48 * 1024)));
+  CUDA_TRY(c, raise_attr(3, std::max<size_t>(c->select_smem, 48 * 1024)));
   return SMART_OK;
 }
 
@@ -521,14 +561,13 @@ smart_status smart_destroy(smart_ctx* c) {
     cudaFree(c->P.xs);
     cudaFree(c->P.xr);
   }
-  if (c->ws) cudaFree(c->ws);
-  if (c->cost_dev) cudaFree(c->cost_dev);
-  delete c;
+  release_ctx(c);
   return SMART_OK;
 }
 
 smart_status smart_begin_step(smart_ctx* c, const int32_t* d_root_tok, const int32_t* d_root_pos, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int thr = 256, grid = (c->P.b_loc + thr - 1) / thr;
   launch_k(begin_step_kernel, dim3(grid), dim3(thr), 0, s, c->P, d_root_tok, d_root_pos);
@@ -542,6 +581,7 @@ smart_status smart_begin_step(smart_ctx* c, const int32_t* d_root_tok, const int
 
 smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits, int64_t ld, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (!d_logits) return fail(c, SMART_EINVAL, "null logits");
   if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld (%lld) < vocab (%d)", (long long)ld, c->cfg.vocab);
   if (c->next_layer == 0) return fail(c, SMART_ESTATE, "expand before begin_step");
@@ -553,7 +593,9 @@ smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits
   const bool tma = ((reinterpret_cast<uintptr_t>(d_logits) & 15) == 0) && (ld_bytes % 16 == 0) &&
                    (((long long)c->P.V * c->P.esz) % 16 == 0);
   // early start: the previous layer's fused selection publishes its frontier before its kernel ends
-  const bool early = layer >= 2 && c->fused_select && c->P.nranks <= 1 && !c->no_early;
+  // (only inside smart_run_step: between separate calls the caller may run its own kernels, e.g.
+  // a draft forward writing these logits, which the flag does not order against)
+  const bool early = layer >= 2 && c->in_run_step && c->fused_select && c->P.nranks <= 1 && !c->no_early;
   launch_expand(c->P, layer, d_logits, ld_bytes, tma, c->fused_select, early, c->grid_expand, s);
   CUDA_TRY(c, cudaGetLastError());
   c->phase = 1;
@@ -563,6 +605,7 @@ smart_status smart_expand_step(smart_ctx* c, int32_t layer, const void* d_logits
 
 smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int32_t* d_frontier_count, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (layer != c->next_layer || c->phase != 1)
     return fail(c, SMART_ESTATE, "select layer %d out of order (expected %d after expand)", layer, c->next_layer);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -595,6 +638,7 @@ smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int3
 smart_status smart_select_finish(smart_ctx* c, int32_t layer, int32_t* d_frontier, int32_t* d_frontier_count,
                                  void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (layer != c->next_layer || c->phase != 2)
     return fail(c, SMART_ESTATE, "select_finish layer %d out of order", layer);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -611,6 +655,7 @@ smart_status smart_select_finish(smart_ctx* c, int32_t layer, int32_t* d_frontie
 smart_status smart_build_mask(smart_ctx* c, uint32_t* d_mask, int32_t* d_pos, int32_t* d_parent, int32_t* d_tok,
                               int32_t* d_tree_len, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (c->next_layer == 0 || c->phase != 0) return fail(c, SMART_ESTATE, "build_mask needs a begun step between layers");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (c->P.selection == SMART_BASELINE) launch_rerank(c->P, s);  // stage 2 of the baseline (Q32)
@@ -624,6 +669,7 @@ smart_status smart_build_mask(smart_ctx* c, uint32_t* d_mask, int32_t* d_pos, in
 smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld, int32_t* d_accept_len,
                                  int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (!d_target) return fail(c, SMART_EINVAL, "null target logits");
   if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld < vocab");
   if (!c->masked) return fail(c, SMART_ESTATE, "verify_accept must follow build_mask");
@@ -640,6 +686,7 @@ smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld,
 smart_status smart_verify_sample(smart_ctx* c, const void* d_target, int64_t ld, double temperature, uint64_t seed,
                                  int32_t* d_accept_len, int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  CUDA_TRY(c, use_device(c));
   if (!d_target) return fail(c, SMART_EINVAL, "null target logits");
   if (ld < c->cfg.vocab) return fail(c, SMART_EINVAL, "ld < vocab");
   if (!(temperature > 0.0) || !(1.0 / temperature < 3.0e38)) return fail(c, SMART_EINVAL, "temperature must be > 0");
@@ -663,10 +710,12 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
   if (c->cfg.row_mode != SMART_ROWS_NODE) return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE");
   if (c->byo_exchange) return fail(c, SMART_ESTATE, "smart_run_step cannot drive a caller-provided exchange");
   smart_status st = smart_begin_step(c, d_root_tok, d_root_pos, stream);
+  c->in_run_step = true;
   for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
     st = smart_expand_step(c, l, d_draft, ld, stream);
     if (!st) st = smart_select(c, l, nullptr, nullptr, stream);
   }
+  c->in_run_step = false;
   if (!st) st = smart_build_mask(c, d_mask, d_pos, d_parent, d_tok, d_tree_len, stream);
   if (!st && d_target) st = smart_verify_accept(c, d_target, ld_t, d_accept_len, d_accept_path, d_bonus, stream);
   return st;
@@ -735,6 +784,7 @@ smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {
     out->S_final = C > 0 ? c->cost.c_T * (c->P.omega * bc) / (bc * C) : 0.0;
   }
   if (err & (kErrDraftNaN | kErrTargetNaN)) return fail(c, SMART_EDEVICE, "invalid logits (NaN/+inf) seen (flags %d)", err);
+  if (err & kErrTimeout) return fail(c, SMART_EDEVICE, "a device-side wait timed out (flags %d)", err);
   return SMART_OK;
 }
 

@@ -335,7 +335,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   if (!early || sel_cta0) pdl_wait();
   pdl_trigger();
   if (early && !sel_cta0) {
-    if (tid == 0) wait_flag(&P.fr_ready[layer - 1]);
+    if (tid == 0) wait_flag(&P.fr_ready[layer - 1], P.err);
     __syncthreads();
   }
   tl_start(P, layer);

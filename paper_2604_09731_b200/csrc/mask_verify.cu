@@ -549,7 +549,7 @@ void launch_mask(const Params& P, uint32_t* mask, int32_t* pos, int32_t* parent,
 
 size_t mask_smem_bytes(int T, int b) { return ((size_t)32 * 3 * T + b + 1) * sizeof(int); }
 
-cudaError_t mask_set_smem(int T, int b) {
+cudaError_t mask_set_smem_bytes(size_t bytes) {
   // every kernel of the step asks for the maximum shared-memory carveout, so consecutive kernels
   // never wait for an SM's L1/shared split to be reconfigured
   cudaFuncSetAttribute(mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -557,7 +557,7 @@ cudaError_t mask_set_smem(int T, int b) {
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(mask_smem_bytes(T, b), 48 * 1024));
+                              (int)std::max<size_t>(bytes, 48 * 1024));
 }
 
 size_t verify_smem_bytes(int T) {
@@ -615,11 +615,11 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
 
 size_t walk_smem_bytes(int T) { return (size_t)32 * 3 * T * sizeof(int); }
 
-cudaError_t walk_set_smem(int T) {
+cudaError_t walk_set_smem_bytes(size_t bytes) {
   cudaFuncSetAttribute(verify_walk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(verify_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)std::max<size_t>(walk_smem_bytes(T), 48 * 1024));
+                              (int)std::max<size_t>(bytes, 48 * 1024));
 }
 
 }  // namespace smart

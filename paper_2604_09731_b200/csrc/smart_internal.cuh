@@ -30,6 +30,7 @@ constexpr int kStageRows = 64;  // row descriptors a streaming CTA stages in sha
 constexpr int kErrDraftNaN = 1;
 constexpr int kErrTargetNaN = 2;
 constexpr int kErrSaturated = 4;
+constexpr int kErrTimeout = 8;   // a device-side wait gave up (broken launch sequence); sticky
 
 // one candidate produced by A1/A2 for (frontier row, rank j)
 struct Cand {
@@ -219,15 +220,21 @@ __device__ __forceinline__ int warp_sum_i(int v) {
 }
 
 // frontier-ready flag: one thread publishes after a CTA barrier (release, cumulative over the
-// barrier); pollers acquire.  A poll that never completes traps instead of hanging the device.
+// barrier); pollers acquire.  A poll that has not completed after ~2^31 tries (minutes: far beyond
+// any time slicing or preemption) gives up and sets the sticky kErrTimeout flag, which
+// smart_get_stats reports as SMART_EDEVICE; the context is not killed (no trap).
 __device__ __forceinline__ void publish_flag(int* f) {
   asm volatile("st.release.gpu.global.s32 [%0], 1;" ::"l"(f) : "memory");
 }
-__device__ __forceinline__ void wait_flag(const int* f) {
+__device__ __forceinline__ bool wait_flag(const int* f, int* err) {
   for (unsigned it = 0; ld_acquire_gpu(f) == 0; ++it) {
-    if (it > (1u << 24)) __trap();  // ~seconds: a broken launch sequence, never a valid wait
-    __nanosleep(32);
+    if (it > (1u << 31)) {
+      atomicOr(err, kErrTimeout);
+      return false;
+    }
+    __nanosleep(64);
   }
+  return true;
 }
 
 // Programmatic dependent launch: every kernel of the step is launched with programmatic stream
@@ -331,9 +338,9 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
                    bool sample = false, float inv_tau = 1.f, unsigned long long seed = 0ull);
 size_t verify_smem_bytes(int T);
 size_t walk_smem_bytes(int T);
-cudaError_t walk_set_smem(int T);
+cudaError_t walk_set_smem_bytes(size_t bytes);
 int verify_occupancy();
-cudaError_t mask_set_smem(int T, int b);
+cudaError_t mask_set_smem_bytes(size_t bytes);
 size_t mask_smem_bytes(int T, int b);
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
                             cudaStream_t s);

@@ -135,3 +135,15 @@ def test_bench_reference_arm_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_tree_capacity_below_reachable_size_is_rejected(sm):
+    """A SMART tree can reach 1 + min(B, d * W) nodes; a smaller user-set tree_capacity would let
+    the commit write past the request's arrays, so validation rejects it (EINVAL)."""
+    base = dict(vocab=5000, top_k=4, max_depth=3, max_frontier=3, batch_local=2, budget_verify=20)
+    assert sm.query_sizes(sm.Config(**base))["T"] == 1 + min(10, 9)
+    with pytest.raises(sm.SmartError) as e:
+        sm.query_sizes(sm.Config(**base, tree_capacity=4))
+    assert e.value.status == sm.EINVAL
+    assert sm.query_sizes(sm.Config(**base, tree_capacity=10))["T"] == 10
+    assert sm.query_sizes(sm.Config(**base, tree_capacity=64))["T"] == 64

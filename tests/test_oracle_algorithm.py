@@ -429,3 +429,53 @@ def test_permutation_equivariance(orc):
         for i, r in enumerate(perm):
             assert a.n_nodes[r] == bb.n_nodes[i]
             assert (a.tok[r] == bb.tok[i]).all()
+
+
+def test_local_scope_single_request_is_per_sequence_algorithm1(orc):
+    """cost_scope LOCAL (Q13, Q34): a replica holding ONE request of a b_glob batch builds that
+    request's tree exactly as Algorithm 1 run on the sequence alone with the per-sequence budget
+    B = floor(B_verify / b_glob) (P:246-250 splits the budget per sequence; P:177 costs a single
+    tree): b_budget only fixes B, the cost sees the replica's own tree."""
+    rng = np.random.default_rng(41)
+    for it in range(12):
+        cfg, cost, _ = _random_instance(orc, rng)
+        b_glob = int(rng.integers(2, 6))
+        B = int(rng.integers(2, 9))
+        loc = orc.Config(**{**cfg.__dict__, "b": 1, "B_verify": B * b_glob + int(rng.integers(0, b_glob)),
+                            "b_budget": b_glob})
+        alone = orc.Config(**{**cfg.__dict__, "b": 1, "B_verify": B, "b_budget": 0})
+        assert loc.B == alone.B == B and loc.tmax() == alone.tmax()
+        pool = synth.draft_pool(it, 1, loc.tmax(), cfg.V, dtype="fp32", a_lo=2, a_hi=8, sigma_bg=1.0)
+        a, s = orc.step(loc, cost, pool), orc.step(alone, cost, pool)
+        assert a.n_nodes[0] == s.n_nodes[0] and (a.tok == s.tok).all() and (a.parent == s.parent).all()
+        np.testing.assert_array_equal(a.trace, s.trace)
+        assert a.S == s.S
+
+
+def test_local_scope_budget_default_is_global(orc):
+    """b_budget = b (or 0) is the plain batch-global step: same trees, traces and S."""
+    rng = np.random.default_rng(43)
+    for it in range(8):
+        cfg, cost, pool = _random_instance(orc, rng)
+        a = orc.step(cfg, cost, pool)
+        b2 = orc.step(orc.Config(**{**cfg.__dict__, "b_budget": cfg.b}), cost, pool)
+        np.testing.assert_array_equal(a.tok, b2.tok)
+        np.testing.assert_array_equal(a.trace, b2.trace)
+
+
+def test_threads_do_not_change_results(orc):
+    """The row-parallel A1 / A8 loops (orc_set_threads, the bench's all-cores baseline) compute
+    each row independently: any thread count gives bit-identical outputs."""
+    rng = np.random.default_rng(47)
+    try:
+        for it in range(6):
+            cfg, cost, pool = _random_instance(orc, rng)
+            tgt = synth.target_pool(pool, it + 5, 0.7)
+            orc.set_threads(1)
+            a = orc.step(cfg, cost, pool, tgt)
+            orc.set_threads(4)
+            b2 = orc.step(cfg, cost, pool, tgt)
+            for f in ("tok", "parent", "cum", "mask", "accept_len", "accept_path", "bonus", "trace"):
+                np.testing.assert_array_equal(getattr(a, f), getattr(b2, f))
+    finally:
+        orc.set_threads(1)
