@@ -124,7 +124,7 @@ def test_local_cost_scope_replica():
     from paper_2604_09731_b200 import smart as S
     import torch
     V, k, d, W, b_glob, Bv = 20000, 5, 4, 5, 8, 96
-    cost = (0.004, 0.0, 0.03, 0.01, 1.2, 1.5, 1.0)
+    cost = (0.002, 0.0, 0.03, 0.01, 1.2, 1.5, 1.0)
     for off, b_loc in ((0, 3), (3, 5)):
         case = Case(V=V, k=k, d=d, W=W, b=b_loc, B_verify=Bv, seed=77, cost=cost, a_lo=5.0, a_hi=12.0)
         ocfg = O.Config(V=V, k=k, d=d, W=W, b=b_loc, B_verify=Bv, alpha=case.alpha, omega=1, b_budget=b_glob)
