@@ -37,6 +37,10 @@ struct smart_ctx {
   bool fused_select = true;  // selection runs in the layer kernel's last CTA
   bool no_early = false;     // SMART_NO_EARLY=1: every layer kernel waits for the previous grid
   bool in_run_step = false;  // inside smart_run_step: the layer kernels are back to back (early start ok)
+  // persistent whole-step kernel (step.cu) for smart_run_step: 0 = not usable for this config
+  int step_grid = 0;
+  size_t step_smem = 0, step_sel_bytes = 0;
+  void* step_ws = nullptr;
   double* cost_dev = nullptr;
   Params P{};
   void* ws = nullptr;      // single device allocation
@@ -239,6 +243,8 @@ static void release_ctx(smart_ctx* c) {
   if (c->ws) cudaFree(c->ws);
   if (c->cost_dev) cudaFree(c->cost_dev);
   if (c->P.dbg) cudaFree(c->P.dbg);
+  if (c->step_ws) cudaFree(c->step_ws);
+  c->step_ws = nullptr;
   c->ws = nullptr;
   c->cost_dev = nullptr;
   c->P.dbg = nullptr;
@@ -399,7 +405,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   P.debug_mode = getenv("SMART_DEBUG_MODE") ? atoi(getenv("SMART_DEBUG_MODE")) : 0;
   c->no_early = getenv("SMART_NO_EARLY") != nullptr;
   if (getenv("SMART_TIMING")) {
-    e = cudaMalloc(&P.dbg, 1024 * sizeof(unsigned long long));
+    e = cudaMalloc(&P.dbg, 4096 * sizeof(unsigned long long));
     if (e != cudaSuccess) P.dbg = nullptr;
   }
   // launch geometry: persistent streaming grids sized to the SM count
@@ -443,6 +449,36 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     release_ctx(c);
     return fail(nullptr, SMART_ECUDA, "shared-memory attributes: %s", cudaGetErrorString(e));
   }
+  // persistent whole-step kernel: single rank, SMART selections (PREFIX / FROZEN), node or
+  // position pools; its selection CTA always stages the candidate records
+  if (P.nranks == 1 && cfg->selection != SMART_BASELINE && cfg->row_mode != SMART_ROWS_FRONTIER &&
+      !getenv("SMART_NO_STEP")) {
+    c->step_sel_bytes = select_smem_bytes((int)b, (int)b, sort_cap, (int)(cap * k), 1, (int)k) +
+                        select_rec_bytes((int)(cap * k));
+    c->step_grid = step_grid(P, c->step_sel_bytes, &c->step_smem);
+    if (c->step_grid >= 2) {
+      const long long S = c->step_grid - 1;
+      const long long lists = std::max<long long>(S, std::max<long long>(cap, b));
+      const size_t kb = (size_t)lists * ((k + 1) & ~1ll) * 8, mb = (size_t)std::max<long long>(cap, b) * ((P.cpr + 1) & ~1) * 8;
+      e = cudaMalloc(&c->step_ws, ((kb + 255) & ~size_t(255)) + ((mb + 255) & ~size_t(255)) + sizeof(StepCtl));
+      if (e != cudaSuccess) {
+        release_ctx(c);
+        return fail(nullptr, SMART_ECUDA, "step workspace: %s", cudaGetErrorString(e));
+      }
+      char* sb = static_cast<char*>(c->step_ws);
+      P.seg_keys = reinterpret_cast<unsigned long long*>(sb);
+      sb += (kb + 255) & ~size_t(255);
+      P.seg_ms = reinterpret_cast<float2*>(sb);
+      sb += (mb + 255) & ~size_t(255);
+      P.ctl = reinterpret_cast<StepCtl*>(sb);
+      cudaMemset(P.ctl, 0, sizeof(StepCtl));
+    } else {
+      c->step_grid = 0;
+    }
+  }
+  if (getenv("SMART_VERBOSE"))
+    fprintf(stderr, "[smart] step kernel grid %d smem %zu B (selection scratch %zu B)\n", c->step_grid, c->step_smem,
+            c->step_sel_bytes);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     release_ctx(c);
@@ -707,8 +743,31 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
                             int32_t* d_parent, int32_t* d_tok, int32_t* d_tree_len, int32_t* d_accept_len,
                             int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
-  if (c->cfg.row_mode != SMART_ROWS_NODE) return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE");
+  if (c->cfg.row_mode == SMART_ROWS_FRONTIER)
+    return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE or POSITION (pre-filled pools)");
   if (c->byo_exchange) return fail(c, SMART_ESTATE, "smart_run_step cannot drive a caller-provided exchange");
+  if (!d_draft) return fail(c, SMART_EINVAL, "null draft logits");
+  if (ld < c->cfg.vocab || (d_target && ld_t < c->cfg.vocab)) return fail(c, SMART_EINVAL, "ld < vocab");
+  if (c->step_grid > 0 && c->P.nranks <= 1) {
+    // one persistent launch for the whole step (step.cu) when both pools are TMA-addressable
+    const long long ldb = (long long)ld * c->P.esz, ldtb = (long long)ld_t * c->P.esz;
+    const bool rb = (((long long)c->P.V * c->P.esz) % 16) == 0;
+    const bool tma = rb && ((reinterpret_cast<uintptr_t>(d_draft) & 15) == 0) && (ldb % 16 == 0) &&
+                     (!d_target || (((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ldtb % 16 == 0)));
+    if (tma) {
+      CUDA_TRY(c, use_device(c));
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      StepOut o{d_mask, d_pos, d_parent, d_tok, d_tree_len, d_accept_len, d_accept_path, d_bonus};
+      launch_step(c->P, c->step_grid, c->step_smem, c->step_sel_bytes, d_draft, ldb, d_target, ldtb, d_root_tok,
+                  d_root_pos, o, s);
+      CUDA_TRY(c, cudaGetLastError());
+      c->next_layer = c->cfg.max_depth + 1;
+      c->phase = 0;
+      c->masked = true;
+      c->last_stream = s;
+      return SMART_OK;
+    }
+  }
   smart_status st = smart_begin_step(c, d_root_tok, d_root_pos, stream);
   c->in_run_step = true;
   for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
@@ -724,10 +783,11 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
 extern "C" int smart_debug_probes(smart_ctx* c, unsigned long long* host16, int reset) {
   if (!c || !c->P.dbg) return -1;
   cudaStreamSynchronize(c->last_stream);
-  if (host16) cudaMemcpy(host16, c->P.dbg, 1024 * 8, cudaMemcpyDeviceToHost);
+  if (host16) cudaMemcpy(host16, c->P.dbg, 4096 * 8, cudaMemcpyDeviceToHost);
   if (reset) {
-    static unsigned long long init[1024];
-    for (int i = 0; i < 1024; ++i) init[i] = (i == 0 || i == 8 || (i >= 64 && !(i & 1))) ? ~0ull : 0ull;
+    static unsigned long long init[4096];
+    for (int i = 0; i < 4096; ++i)  // reset 2: all zero (step-kernel probes use max / ~min slots)
+      init[i] = (reset != 2 && (i == 0 || i == 8 || (i >= 64 && !(i & 1)))) ? ~0ull : 0ull;
     cudaMemcpy(c->P.dbg, init, sizeof init, cudaMemcpyHostToDevice);
   }
   return 0;

@@ -27,90 +27,23 @@
 //  * the leader's merge warp computes Z (association fixed by the chunk count), the exact top-k
 //    of the members' lists (threshold + rank), p and cum; the CTA whose merge warp completes the
 //    layer's last row (one acq_rel arrival per row) runs the selection (select_core.cuh).
+#include "expand_core.cuh"
 #include "select_core.cuh"
-#include "stream.cuh"
 
 namespace smart {
 
 namespace {
-
-template <bool BF16>
-struct Traits {
-  static constexpr int EPV = BF16 ? 8 : 4;         // elements per 16 B vector
-  static constexpr int EPT = kVecPerThread * EPV;  // elements per consumer thread per chunk
-};
-
-// element n (= j*EPV + e) of consumer thread `tid` in a chunk -> row element index
-template <bool BF16>
-__device__ __forceinline__ int elem_index(int chunk_base, int tid, int n) {
-  constexpr int EPV = Traits<BF16>::EPV;
-  return chunk_base + ((n / EPV) * kConsumers + tid) * EPV + (n % EPV);
-}
-
-template <bool BF16>
-__device__ __forceinline__ void unpack(const uint4 (&raw)[kVecPerThread], float (&x)[Traits<BF16>::EPT]) {
-#pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (BF16) {
-        x[j * 8 + 2 * q] = __uint_as_float(w[q] << 16);
-        x[j * 8 + 2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
-      } else {
-        x[j * 4 + q] = __uint_as_float(w[q]);
-      }
-    }
-  }
-}
-
-// direct (non-TMA) load of this thread's vectors of a chunk, scalar loads, -inf past the row end;
-// used only when rows are not 16-byte aligned (bulk copies need 16 B alignment and sizes)
-template <bool BF16>
-__device__ __forceinline__ void load_direct(const char* row, int chunk_base, int V, int tid,
-                                            uint4 (&raw)[kVecPerThread]) {
-  constexpr int EPV = Traits<BF16>::EPV;
-#pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    const int e0 = chunk_base + (j * kConsumers + tid) * EPV;
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w[q] = BF16 ? 0xff80ff80u : 0xff800000u;  // -inf
-#pragma unroll
-    for (int e = 0; e < EPV; ++e) {
-      if (e0 + e < V) {
-        if (BF16) {
-          const uint32_t h = *reinterpret_cast<const unsigned short*>(row + (size_t)(e0 + e) * 2);
-          const int q = e >> 1;
-          w[q] = (e & 1) ? ((w[q] & 0x0000ffffu) | (h << 16)) : ((w[q] & 0xffff0000u) | h);
-        } else {
-          w[e] = *reinterpret_cast<const uint32_t*>(row + (size_t)(e0 + e) * 4);
-        }
-      }
-    }
-    raw[j] = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-
-// per-warp top-k state in shared memory (64-bit keys)
-struct WarpTopk {
-  unsigned long long buf[kSegBuf];  // candidates of the current row slice (appended; compacted)
-  unsigned long long list[kMaxK];   // compacted top-k, sorted best first
-};
 
 constexpr int kCluster = 8;                          // CTAs per cluster (portable maximum)
 constexpr int kMergeWarp = kConsumerWarps + 1;       // warp 9: row merges in team leaders
 constexpr int kLayerThreadsT = kLayerThreads + 32;   // 320 threads: consumers, producer, merger
 
 struct __align__(16) ExpandShared {
-  unsigned long long tau;                         // slice-wide bound: max over warps of their k-th best
+  ConsShared cs;                                  // consumer state (expand_core.cuh)
   int2 rfe[kStageRows];                           // frontier entries of the team's rows
   float rcum[kStageRows];                         // their path scores (cum of the parent node)
-  __align__(16) unsigned pub[2][kConsumerWarps * kMaxK];        // slice start: top-k lane maxima per warp
-  __align__(16) unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k
   uint64_t ready[2];  // leader: all members' partials of the team's n-th row are in (parity n & 1)
   uint64_t freeb[2];  // every CTA: the leader has consumed buffer parity p (remote arrive)
-  WarpTopk w[kConsumerWarps];
 };
 
 // team buffers, carved after ExpandShared.  Receive side (the team leader's copy, double-
@@ -118,7 +51,6 @@ struct __align__(16) ExpandShared {
 // (every CTA): its slice's partials and top-k list, staged locally and moved to the leader with
 // one shared::cluster bulk copy each (completion counted on the leader's mbarrier).
 // kp = k rounded up to even, so every bulk copy is a multiple of 16 bytes.
-__host__ __device__ inline int list_stride(int k) { return (k + 1) & ~1; }
 
 struct TeamBuf {
   float4* ms[2];              // receive: per-chunk softmax partials (M_c, S_c, -, -) [cpr]
@@ -193,103 +125,27 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Warp-level compaction: list <- top-k of buf[0..n) by rank counting (keys distinct); ranks >= n
-// are sentinels.  The buffer then restarts from the list (caller sets its count to min(n, k)).
-__device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane) {
-  if (lane < k) w.list[lane] = kKeySentinel;
-  __syncwarp();
-  for (int e = lane; e < n; e += 32) {
-    const unsigned long long key = w.buf[e];
-    int rank = 0;
-#pragma unroll 8
-    for (int f = 0; f < n; ++f) rank += (w.buf[f] > key);
-    if (rank < k) w.list[rank] = key;
-  }
-  __syncwarp();
-  if (lane < k) w.buf[lane] = w.list[lane];
-  __syncwarp();
-}
-
-// ---- row merge by the team leader's merge warp, from its own shared memory ----
-// M = max, Z = sum s*exp(m - M) over the row's cpr x 8 partials (association fixed by cpr);
-// T = the best k-th entry over the members' lists (each list is its slice's top-k, so T bounds the
-// row's k-th best key from below); the entries >= T are ranked among themselves and the top k
-// written with p (A1) and cum (A2, Eq.(3)).
-__device__ void merge_row_team(const Params& P, int layer, int par, int row, int2 fe, float pc, int slot, int t,
-                               const float4* ms, const unsigned long long* lists, unsigned long long* surv,
-                               bool pr) {
+// ---- row merge by the team leader's merge warp, from its own shared memory (merge_row in
+// expand_core.cuh): Z from the cpr per-chunk partials, T = best tail over the t member lists, the
+// survivors ranked; A1 p and A2 cum (Eq.(3)) written as the row's k candidate records ----
+__device__ void merge_row_team(const Params& P, int layer, int row, int2 fe, float pc, int slot, int t,
+                               const float4* ms, const unsigned long long* lists, unsigned long long* surv) {
   const int lane = threadIdx.x & 31;
-  const int k = P.k, cpr = P.cpr;
-  stamp(P, pr, 1);
-  // (1) softmax normaliser from the cpr per-chunk partials (each already combined over its 8
-  // warps in fixed order by the member that streamed the chunk): M = max, Z = sum S_c exp(M_c - M)
-  // in a fixed association (lane-strided, then the xor tree) -- a function of cpr only
-  // (cpr <= 64: at most two partials per lane, loaded once; the sum stays lane-strided in order)
-  const float4 v0 = lane < cpr ? ms[lane] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
-  const float4 v1 = lane + 32 < cpr ? ms[lane + 32] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
-  const float M = warp_max_fast(fmaxf(v0.x, v1.x));
-  const float ML = M * kLog2e;
-  float z = 0.f;
-  z += (v0.y != 0.f || isnan(v0.y)) ? v0.y * ex2(fmaf(v0.x, kLog2e, -ML)) : 0.f;
-  z += (v1.y != 0.f || isnan(v1.y)) ? v1.y * ex2(fmaf(v1.x, kLog2e, -ML)) : 0.f;
-  const float Z = warp_sum(z);
-  const float rZ = __frcp_rn(Z);  // correctly rounded 1/Z (no division slow path)
-  stamp(P, pr, 2);
-  // (2) threshold: best tail over the members' lists
-  const int kp = list_stride(k);
-  const unsigned long long tail = lane < t ? lists[lane * kp + k - 1] : 0ull;
-  const unsigned th = __reduce_max_sync(kFull, (unsigned)(tail >> 32));
-  const unsigned tl = __reduce_max_sync(kFull, (unsigned)(tail >> 32) == th ? (unsigned)tail : 0u);
-  const unsigned long long T = ((unsigned long long)th << 32) | tl;
-  // (3) survivors, compacted by ballot
-  const int nkey = t * kp;  // the padding slot of an odd k holds a key below every real one
-  int ns = 0;
-  for (int e0 = 0; e0 < nkey; e0 += 32) {
-    const int e = e0 + lane;
-    const unsigned long long key = e < nkey ? lists[e] : 0ull;
-    const bool sv = e < nkey && key >= T;
-    const unsigned bal = __ballot_sync(kFull, sv);
-    if (sv) surv[ns + __popc(bal & ((1u << lane) - 1u))] = key;
-    ns += __popc(bal);
-  }
-  __syncwarp();
-  stamp(P, pr, 3);
-  // (4) exact top-k among the survivors; A1 p and A2 cum
-  auto emit = [&](unsigned long long key, int rank) {
-    const float v = tk_val(key);
-    const float pj = ex2(fmaf(v, kLog2e, -ML)) * rZ;  // p = exp(x - M) / Z   (tau = 1, Q10)
-    Cand cd;
-    cd.tok = tk_idx(key);
-    cd.p = pj;
-    cd.cum = pc * pj;  // Eq.(3)
-    cd.parent = fe.y;
-    P.cand[((size_t)(layer - 1) * P.cap_rows + row) * k + rank] = cd;
-  };
-  if (ns <= 32) {
-    // one survivor per lane; rank by broadcast compares (no shared-memory loop)
-    const unsigned long long mine = lane < ns ? surv[lane] : 0ull;
-    int rank = 0;
-#pragma unroll 8
-    for (int q = 0; q < ns; ++q) rank += (__shfl_sync(kFull, mine, q) > mine);
-    if (lane < ns && rank < k) emit(mine, rank);
-  } else {
-    for (int s0 = lane; s0 < ns; s0 += 32) {
-      const unsigned long long key = surv[s0];
-      int r0 = 0, r1 = 0;
-      int q = 0;
-      for (; q + 1 < ns; q += 2) {
-        r0 += (surv[q] > key);
-        r1 += (surv[q + 1] > key);
-      }
-      if (q < ns) r0 += (surv[q] > key);
-      const int rank = r0 + r1;
-      if (rank < k) emit(key, rank);
-    }
-  }
-  stamp(P, pr, 4);
+  const int k = P.k;
+  Cand* out = P.cand + ((size_t)(layer - 1) * P.cap_rows + row) * k;
+  const bool ok = merge_row(
+      k, P.cpr, t, pc, [&](int c) { return ms[c]; }, [&](int e) { return lists[e]; }, surv,
+      [&](int rank, int tok, float p, float cum) {
+        Cand cd;
+        cd.tok = tok;
+        cd.p = p;
+        cd.cum = cum;
+        cd.parent = fe.y;
+        out[rank] = cd;
+      });
   if (lane == 0) {
     P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, slot);
-    if (!(Z >= 1.0f) || isinf(Z) || isnan(M)) atomicOr(P.err, kErrDraftNaN);  // Q23
+    if (!ok) atomicOr(P.err, kErrDraftNaN);  // Q23
   }
   __syncwarp();
 }
@@ -304,8 +160,6 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   // per-request state the previous selection writes after the frontier)
   const int fuse_select = flags & 1;
   const bool early = (flags & 2) != 0;
-  constexpr int EPT = Traits<BF16>::EPT;
-  constexpr int EPV = Traits<BF16>::EPV;
   extern __shared__ __align__(128) char dsm[];
   char* ring = dsm;
   StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
@@ -324,7 +178,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     mbar_init(&sh.freeb[0], 1);
     mbar_init(&sh.freeb[1], 1);
     mbar_fence_init();
-    sh.tau = 0ull;
+    sh.cs.tau = 0ull;
   }
   cluster_sync_all();  // barriers initialised cluster-wide before any remote arrive
   tl_start(P, 32 + layer);
@@ -436,8 +290,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
           mbar_expect_tx(&sh.ready[b], (uint32_t)(cpr * 16 + t * list_stride(k) * 8));
         mbar_wait_acq_cluster(&sh.ready[b], (uint32_t)(n >> 1) & 1u);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 24);
-        merge_row_team(P, layer, par, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv,
-                       blockIdx.x == 0 && lane == 0 && n == 0);
+        merge_row_team(P, layer, row, fe, pc, slot, t, tb.ms[b], tb.lists[b], tb.surv);
         stamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 5);
         gstamp(P, blockIdx.x == 0 && lane == 0 && n == 0, 25);
         // buffer b is free again (only awaited when the team streams another row into it)
@@ -451,9 +304,8 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       }
     }
   } else {
-    // ---- consumer warps ----
-    WarpTopk& W = sh.w[warp];
-    int wcnt = 0;  // entries in W.buf (warp-uniform)
+    // ---- consumer warps (expand_core.cuh) ----
+    int wcnt = 0;  // entries in the warp's buffer (warp-uniform)
     int i = 0;
     for (int n = 0; n < nrows; ++n) {
       const int row = team + n * nteams;
@@ -467,217 +319,28 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       for (int c = mlo; c < mhi; ++c, ++i) {
         uint4 raw[kVecPerThread];
         const int s = i % kStages;
+        const char* stage = ring + (size_t)s * kChunkBytes;
         if (TMA) {
           mbar_wait(&pipe.full[s], ((uint32_t)(i / kStages)) & 1u);
           gstamp(P, t0 && i < 2, 18 + 3 * i);
-          const uint4* st = reinterpret_cast<const uint4*>(ring + (size_t)s * kChunkBytes);
+          const uint4* st = reinterpret_cast<const uint4*>(stage);
 #pragma unroll
           for (int j = 0; j < kVecPerThread; ++j) raw[j] = st[j * kConsumers + tid];
         } else {
           load_direct<BF16>(rowp(n, row), c * CE, V, tid, raw);
         }
-        if (P.debug_mode == 1) {  // timing experiment: stream only
-          __syncwarp();
-          if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);
-          continue;
-        }
-        float x[EPT];
-        unpack<BF16>(raw, x);
-        const int cbase = c * CE;
-        if (c == cpr - 1) {  // ragged last chunk: elements past the row end -> -inf
-#pragma unroll
-          for (int e = 0; e < EPT; ++e)
-            if (elem_index<BF16>(cbase, tid, e) >= V) x[e] = -INFINITY;
-        }
-        // ---- softmax partial of this (chunk, warp): max tree, 4 independent sum chains ----
-        float vm[kVecPerThread];
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-          float a0 = fmaxf(x[j * EPV], x[j * EPV + 1]);
-          float a1 = fmaxf(x[j * EPV + 2], x[j * EPV + 3]);
-          if (EPV == 8) {
-            a0 = fmaxf(a0, fmaxf(x[j * EPV + 4 % EPV], x[j * EPV + 5 % EPV]));
-            a1 = fmaxf(a1, fmaxf(x[j * EPV + 6 % EPV], x[j * EPV + 7 % EPV]));
-          }
-          vm[j] = fmaxf(a0, a1);
-        }
-        const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
-        const float Mw = warp_max_fast(m);
-        // exp2(x*log2e - M*log2e) on element pairs: FFMA2 + 2 MUFU + FADD2 (two pair accumulators)
-        unsigned long long acc2[2] = {0ull, 0ull};
-        if (Mw != -INFINITY && P.debug_mode != 4) {  // (debug_mode 4: timing experiment, no exps)
-          const float ML = Mw * kLog2e;
-          const unsigned long long l2e2 = f2pk(kLog2e, kLog2e), nml2 = f2pk(-ML, -ML);
-#pragma unroll
-          for (int e = 0; e < EPT; e += 2) {
-            const unsigned long long y = ffma2(f2pk(x[e], x[e + 1]), l2e2, nml2);
-            acc2[(e >> 1) & 1] = fadd2(acc2[(e >> 1) & 1], f2pk(ex2(f2lo(y)), ex2(f2hi(y))));
-          }
-        }
-        const float sacc = warp_sum((f2lo(acc2[0]) + f2hi(acc2[0])) + (f2lo(acc2[1]) + f2hi(acc2[1])));
-        gstamp(P, t0 && i < 2, 19 + 3 * i);
-        if (lane == 0) tb.msl[(c - mlo) * kConsumerWarps + warp] = make_float2(Mw, sacc);
-        if (P.debug_mode == 3) {  // timing experiment only: softmax without the top-k filter
-          __syncwarp();
-          if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);
-          continue;
-        }
-
-        const bool pq = t0 && i < 2;  // probe: CTA 0, warp 0 lane 0, first two chunks
-        stamp(P, pq, 24 + 4 * i);
-        // ---- top-k candidates of this warp-chunk ----
-        // CTA-wide bound at the slice's first chunk: every warp publishes its top-j lane maxima
-        // (j = ceil(k/8), one lane per round, so ties keep their multiplicity); these 8j values
-        // are distinct elements of the row, so their k-th largest v_k bounds the row's k-th best
-        // value from below and key(v_k, INT_MAX) bounds the slice's k-th best key.  Later chunks
-        // run barrier-free on the warp's own bound (tightened by compaction).
-        if (c == mlo) {
-          // every warp publishes its top-j lane maxima (j >= 2 rounds of a warp max; ties keep
-          // their multiplicity); v_k, the k-th largest of these 8j values, bounds the slice's
-          // k-th best value from below
-          const int jr = max((k + kConsumerWarps - 1) / kConsumerWarps, 2);
-          unsigned* pub = sh.pub[i & 1];
-          unsigned rem = (m == m) ? float_orderable(m) : 0u;
-          for (int r = 0; r < jr; ++r) {
-            const unsigned cur = __reduce_max_sync(kFull, rem);
-            const unsigned bal = __ballot_sync(kFull, rem == cur);
-            if (lane == __ffs(bal) - 1) rem = 0u;
-            if (lane == 0) pub[warp * jr + r] = cur;
-          }
-          consumer_sync();
-          const int np = kConsumerWarps * jr;  // multiple of 8
-          unsigned vc = 0xffffffffu;
-          for (int e = lane; e < np; e += 32) {
-            const unsigned u = pub[e];
-            int gt = 0;
-            for (int o = 0; o < np; o += 4) {
-              const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
-              gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
-            }
-            if (gt < k && u < vc) vc = u;
-          }
-          const unsigned vk = __reduce_min_sync(kFull, vc);
-          if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)
-            const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
-            if (b0 > bound) bound = b0;
-          }
-        }
-        // elements whose value reaches the bound are appended to the warp buffer at positions from
-        // a warp prefix sum (no shared atomics); when the buffer would overflow it is compacted to
-        // its top-k, the bound tightened and the remaining elements re-filtered
-        stamp(P, pq && i == 0, 31);
-        {
-          // barrier-free CTA bound: every warp posts its k-th best after each compaction (a lower
-          // bound of the slice's k-th best) with a shared atomic max; all warps adopt the maximum
-          const unsigned long long tt = *reinterpret_cast<volatile unsigned long long*>(&sh.tau);
-          if (tt > bound) bound = tt;
-        }
-        float bv = bound ? tk_val(bound) : -INFINITY;
-        if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
-          // vectors whose max reaches the bound are expanded cooperatively: each group of EPV
-          // lanes takes one such vector (its elements re-read from the still-held ring stage),
-          // compares them with the bound and appends the survivors at ballot-prefix positions
-          constexpr int G = 32 / EPV;  // vectors per pass
-          stamp(P, pq, 25 + 4 * i);
-#pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j) {
-            unsigned bal = __ballot_sync(kFull, vm[j] >= bv);
-            while (bal) {
-              if (wcnt > kSegBuf - 32) {  // keep room for a full pass: compact, tighten, re-filter
-                __syncwarp();
-                warp_compact(W, wcnt, k, lane);
-                wcnt = k;
-                if (W.list[k - 1] > bound) bound = W.list[k - 1];
-                if (lane == 0) atomicMax(&sh.tau, W.list[k - 1]);
-                bv = tk_val(bound);
-                bal &= __ballot_sync(kFull, vm[j] >= bv);
-                if (!bal) break;
-              }
-              unsigned bb = bal;
-              for (int g = 0; g < lane / EPV; ++g) bb &= bb - 1u;
-              const int L = bb ? __ffs(bb) - 1 : -1;  // owner lane of this group's vector
-#pragma unroll
-              for (int g = 0; g < G; ++g) bal &= bal - 1u;
-              bool q = false;
-              float v = -INFINITY;
-              int idx = 0;
-              if (L >= 0) {
-                const int tl = warp * 32 + L;  // the owner's consumer thread id
-                const int e = j * EPV + lane % EPV;
-                idx = elem_index<BF16>(cbase, tl, e);
-                if (idx < V) {  // past the row end: stale stage bytes, never a candidate
-                  const char* sp = TMA ? ring + (size_t)s * kChunkBytes +
-                                             ((size_t)(j * kConsumers + tl) * EPV + (e % EPV)) * (BF16 ? 2 : 4)
-                                       : rowp(n, row) + (size_t)idx * (BF16 ? 2 : 4);
-                  v = BF16 ? __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(sp)) << 16)
-                           : *reinterpret_cast<const float*>(sp);
-                }
-                q = v >= bv;  // NaN never qualifies (the row merge flags it)
-              }
-              const unsigned qb = __ballot_sync(kFull, q);
-              if (q) W.buf[wcnt + __popc(qb & ((1u << lane) - 1u))] = tk_key(v, idx);
-              wcnt += __popc(qb);
-            }
-          }
-        }
-        stamp(P, pq, 26 + 4 * i);
-        if (wcnt >= 2 * k && c + 1 < mhi) {  // keep the warp's buffer short
-          __syncwarp();
-          warp_compact(W, wcnt, k, lane);
-          wcnt = k;
-          if (W.list[k - 1] > bound) bound = W.list[k - 1];
-          if (lane == 0) atomicMax(&sh.tau, W.list[k - 1]);
-        }
+        consume_chunk<BF16, TMA>(P, sh.cs, tb.msl, raw, stage, TMA ? nullptr : rowp(n, row), c, mlo, mhi, i, wcnt,
+                                 bound);
         __syncwarp();
-        stamp(P, pq && i == 0, 27);
         if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
         gstamp(P, t0 && i < 2, 20 + 3 * i);
       }
-      // ---- slice end: warp buffers (top-k only if longer) -> CTA list (rank merge) -> leader ----
-      if (wcnt > k) {
-        warp_compact(W, wcnt, k, lane);
-        wcnt = k;
-      }
-      // padding keys are distinct and below every real key (value -inf, index > INT_MAX)
-      if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
-      wcnt = 0;
-      consumer_sync();
+      // ---- slice end: warp buffers -> CTA list (rank merge) -> leader ----
+      slice_end_post(sh.cs, k, wcnt);
       gstamp(P, t0 && n == 0, 31);
-      {
-        // rank of each of the nl = 8k entries against the whole list (broadcast 16-byte reads:
-        // one shared-memory wavefront per load)
-        const int nl = kConsumerWarps * k;  // even
-        if (tid < nl) {
-          const unsigned long long key = sh.cl[tid];
-          const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
-          int r0 = 0, r1 = 0;
-#pragma unroll 4
-          for (int f = 0; f < nl / 2; ++f) {
-            const ulonglong2 v = c2[f];
-            r0 += (v.x > key);
-            r1 += (v.y > key);
-          }
-          const int rank = r0 + r1;
-          if (rank < k) tb.listl[rank] = key;
-        }
-        if ((k & 1) && tid == 0) tb.listl[k] = kKeySentinel - 1000;  // even-k padding slot
-        // per-chunk softmax partials: the 8 warps' (M_w, s_w) of each of this CTA's chunks
-        // combined in warp order (fixed association: a function of the chunk alone)
-        for (int cc = kConsumers - 1 - tid; cc < mhi - mlo; cc += kConsumers) {
-          const float2* pw = tb.msl + cc * kConsumerWarps;
-          float Mc = -INFINITY;
-#pragma unroll
-          for (int w = 0; w < kConsumerWarps; ++w) Mc = fmaxf(Mc, pw[w].x);
-          const float MLc = Mc * kLog2e;
-          float Sc = 0.f;
-#pragma unroll
-          for (int w = 0; w < kConsumerWarps; ++w) {
-            const float2 v = pw[w];
-            if (v.y != 0.f || isnan(v.y)) Sc += v.y * ex2(fmaf(v.x, kLog2e, -MLc));
-          }
-          tb.msc[cc] = make_float4(Mc, Sc, 0.f, 0.f);
-        }
-      }
+      slice_end_merge(
+          sh.cs, tb.msl, k, mhi - mlo, [&](int rank, unsigned long long key) { tb.listl[rank] = key; },
+          [&](int cc, float Mc, float Sc) { tb.msc[cc] = make_float4(Mc, Sc, 0.f, 0.f); });
       gstamp(P, t0 && n == 0, 96);
       consumer_sync();  // staging complete
       gstamp(P, t0 && n == 0, 97);
@@ -690,7 +353,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
         bulk_s2cluster(mapa_rank(tb.lists[b] + member * kp, lrank), tb.listl, (uint32_t)(kp * 8), bar);
         bulk_commit();
         gstamp(P, t0 && n == 0, 98);
-        sh.tau = 0ull;  // next slice (other warps read it only after the next slice's first barrier)
+        sh.cs.tau = 0ull;  // next slice (other warps read it only after the next slice's first barrier)
       }
       gstamp(P, t0 && n == 0, 27);
     }
@@ -700,7 +363,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
     gstamp(P, tid == 0, 28);
     const int* done = &P.layer_done[layer - 1];
     int pass = 0;
-    auto wait_rows = [&]() {
+    auto wait_rows = [&](SelLayout&, int4*) {
       if (tid == 0 && pass == 0) {
         while (ld_acquire_gpu(done) < R) {
         }
@@ -708,12 +371,13 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
       }
       consumer_sync();
       gstamp(P, tid == 0, 30);
+      return false;
     };
     // (P.debug_mode == 2: timing experiment only, a second pass through the same code)
     const int npass = P.debug_mode == 2 ? 2 : 1;
     for (; pass < npass; ++pass) {
       if (pass) consumer_sync();
-      select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows);
+      select_layer<kConsumers>(P, layer, kSelFull, ring, wait_rows, PubReady{&P.fr_ready[layer]});
     }
     gstamp(P, tid == 0, 29);
   }

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int
     if (threadIdx.x == 0) *P.fr_total[layer & 1] = 0;
     return;
   }
-  select_layer<kSelectThreads>(P, layer, mode, smem);
+  select_layer<kSelectThreads>(P, layer, mode, smem, NoWait{}, PubReady{&P.fr_ready[layer]});
 }
 
 __global__ void export_frontier_kernel(Params P, int parity, int32_t* out, int32_t* count) {

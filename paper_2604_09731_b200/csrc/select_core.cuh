@@ -351,8 +351,17 @@ __device__ __forceinline__ double warp_det_sum(const double* a, int n, int lane)
 // bookkeeping and the A5 scan (lane-contiguous chunks, so the fp64 prefix is a function of the
 // list length only); 7 block barriers in total.
 // ---------------------------------------------------------------------------------------------
+// wait_rows(L, crec): runs after the prefetch; returns true if it has itself staged the layer's
+// candidate records in crec[] and each row's request in L.rreq[] (the persistent step kernel's
+// row merge), false if the records are to be read from P.cand / P.cand_rs
 struct NoWait {
-  __device__ void operator()() const {}
+  __device__ bool operator()(SelLayout&, int4*) const { return false; }
+};
+// pub(R_next): one thread publishes the next frontier (written and fenced by the caller's barrier
+// or __syncwarp); the per-layer kernels release P.fr_ready[layer]
+struct PubReady {
+  int* flag;
+  __device__ void operator()(int) const { publish_flag(flag); }
 };
 
 __device__ __forceinline__ Cand load_cand(const Cand* p) {  // L2 (written by other CTAs)
@@ -376,8 +385,8 @@ __device__ __forceinline__ Cand load_cand(const Cand* p) {  // L2 (written by ot
 // threads; warp 0 runs the A5 scan (lane-contiguous chunks: the fp64 prefix is a function of
 // the list length only, so any sharding reproduces it bit for bit).
 // ---------------------------------------------------------------------------------------------
-template <int NT, class Wait = NoWait>
-__device__ void select_layer(const Params& P, int layer, int mode, char* smem, Wait wait_rows = Wait()) {
+template <int NT, class Wait, class Pub>
+__device__ void select_layer(const Params& P, int layer, int mode, char* smem, Wait wait_rows, Pub pub) {
   __shared__ SelScratch ss;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (layer - 1) & 1, npar = layer & 1;
@@ -467,17 +476,26 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   }
 
   // ---- the layer's candidates (after the row merges): benefits b = cum / D_r (Eq.(13)) ----
-  wait_rows();
-  for (int q = tid; q < nct; q += NT) {
-    const int r = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
-    const int4 rec = __ldcg(reinterpret_cast<const int4*>(&P.cand[lbase + q]));  // whole record
-    const float cum = __int_as_float(rec.z);
-    if (crec) crec[q] = rec;  // staged for the commit (no second L2 round trip)
-    const float D = L.D[r];
-    const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
-    L.cb[q] = b;
-    P.cand_b[lbase + q] = b;
-    if (q % k == 0) L.rreq[q / k] = r;
+  if (wait_rows(L, crec)) {  // records and row requests already staged (crec, L.rreq)
+    for (int q = tid; q < nct; q += NT) {
+      const float cum = __int_as_float(crec[q].z);
+      const float D = L.D[L.rreq[q / k]];
+      const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
+      L.cb[q] = b;
+      P.cand_b[lbase + q] = b;
+    }
+  } else {
+    for (int q = tid; q < nct; q += NT) {
+      const int r = __ldcg(&P.cand_rs[(size_t)(layer - 1) * P.cap_rows + q / k]).x;
+      const int4 rec = __ldcg(reinterpret_cast<const int4*>(&P.cand[lbase + q]));  // whole record
+      const float cum = __int_as_float(rec.z);
+      if (crec) crec[q] = rec;  // staged for the commit (no second L2 round trip)
+      const float D = L.D[r];
+      const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
+      L.cb[q] = b;
+      P.cand_b[lbase + q] = b;
+      if (q % k == 0) L.rreq[q / k] = r;
+    }
   }
   blk_sync<NT>();  // B2
   stamp(P, tid == 0, 10);
@@ -853,9 +871,10 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       }
       if (lane < bl) P.fr_off[npar][lane] = incl - nx;
       if (lane == 31) *P.fr_total[npar] = incl;
+      const int tot = __shfl_sync(kFull, incl, 31);
       __syncwarp();
       stamp(P, tid == 0, 18);
-      if (lane == 0) publish_flag(&P.fr_ready[layer]);
+      if (lane == 0) pub(tot);
       stamp(P, tid == 0, 19);
     }
     blk_sync<NT>();  // B7: per-request counts and offsets for everyone
@@ -882,7 +901,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
     }
     blk_sync<NT>();  // B8: the next frontier is complete
-    if (tid == 0) publish_flag(&P.fr_ready[layer]);
+    if (tid == 0) pub(total);
   }
   // after the flag: state the next layer's streaming CTAs do not read
   for (int r = tid; r < bl; r += NT) P.fr_cnt[npar][r] = L.nxt[r];

@@ -40,6 +40,18 @@ struct Cand {
   int32_t parent;  // node index of the expanded frontier node
 };
 
+// control block of the persistent whole-step kernel (step.cu), in the workspace (zeroed at
+// create).  Flags carry (tag << 32 | value) with tag = epoch + 1 of the launch, so a step never
+// sees a previous step's flags and nothing needs resetting between steps; the last CTA to exit
+// advances the epoch.
+constexpr int kVerifySlot = SMART_MAX_DEPTH + 1;
+struct StepCtl {
+  unsigned long long flag[SMART_MAX_DEPTH + 2];  // [l]: layer-l frontier rows published; [kVerifySlot]: verify rows
+  int arrive[SMART_MAX_DEPTH + 2];               // slices of layer l streamed (reset by the select CTA)
+  int exit_cnt;
+  unsigned epoch;
+};
+
 // device copy of one layer's trace (same fields as smart_layer_trace)
 struct DevTrace {
   int32_t executed, n_rows, n_cand, n_elig, n_admit, argmax_j, N0, saturated;
@@ -112,6 +124,12 @@ struct Params {
   int* vrow_off;      // [b_loc+1]
   int2* vrow_rn;      // [b_loc*T] (request, node) of each verify row (written by the mask kernel)
   unsigned long long* vbest;  // [b_loc*T] target argmax key of each tree row (red.max; cleared by the walk)
+
+  // ---- persistent whole-step kernel (step.cu) ----
+  unsigned long long* seg_keys;  // slice top-k lists of the current layer, dense [row * t + member][kp]
+  float2* seg_ms;                // per-chunk softmax partials (M_c, S_c) of the current layer [row][cpr]
+  StepCtl* ctl;
+  int step_S;                    // streaming CTAs (the grid's last CTA runs the selection)
 
   // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----
   // per-rank record: keys[m_cap] u64 | E_r[b_loc] f64 | hdr[b_loc] n_r, hdr[b_loc] = count
@@ -342,6 +360,17 @@ cudaError_t walk_set_smem_bytes(size_t bytes);
 int verify_occupancy();
 cudaError_t mask_set_smem_bytes(size_t bytes);
 size_t mask_smem_bytes(int T, int b);
+struct StepOut {
+  uint32_t* mask;
+  int32_t *pos, *parent, *tok, *tree_len, *accept_len, *accept_path, *bonus;
+};
+// persistent whole-step kernel (step.cu); sel_bytes = select_layer scratch incl. staged records
+int step_grid(const Params& P, size_t sel_bytes, size_t* smem_out);  // 0: the config does not fit
+size_t step_stream_smem_bytes();
+size_t step_select_smem_bytes(const Params& P, int S, size_t sel_bytes);
+void launch_step(const Params& P, int grid, size_t smem, size_t sel_bytes, const void* draft, long long ld_d,
+                 const void* target, long long ld_t, const int32_t* root_tok, const int32_t* root_pos,
+                 const StepOut& out, cudaStream_t s);
 void launch_export_frontier(const Params& P, int parity, int32_t* d_frontier, int32_t* d_count,
                             cudaStream_t s);
 

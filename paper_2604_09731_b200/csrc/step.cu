@@ -1,0 +1,725 @@
+// step.cu — the persistent whole-step kernel behind smart_run_step: one launch runs a whole decode
+// step of the SMART controller (Algorithm 1) for a batch — d layers of A1+A2 (top-k +
+// softmax of every frontier row; cum = cum(parent) * p, Eq.(3)) and A3-A6
+// (select_core.cuh), then A7 (mask, position ids, parents) and A8 (the greedy
+// longest-accepted-path walk on the target logits, P:453 / S:383).
+//
+// Layout: gridDim.x - 1 streaming CTAs and one selection CTA, all co-resident
+// (grid = SMs x occupancy).  Layers are separated by flags in global memory, not by kernel
+// boundaries:
+//  * streaming CTA s, layer l with R frontier rows: team size t = min(cpr, S / R, 32) (t = 1 when
+//    R > S); CTA s is member s % t of team s / t, which streams rows team, team + S/t, ...; the
+//    member's slice of a row is chunks [m cpr / t, (m+1) cpr / t).  A producer lane bulk-copies the
+//    chunks into the TMA ring (cp.async.bulk + mbarrier), 8 consumer warps reduce them
+//    (expand_core.cuh) and write the slice's top-k list and per-chunk softmax partials to global
+//    memory, then one red.release.gpu arrival per slice.  Layer 1's rows are the roots (r, 0): no
+//    wait.  For layer l >= 2 the producer lane polls flag[l] (ld.acquire.gpu) and reads its rows'
+//    frontier entries; consumers learn the row count from it through a shared-memory mbarrier.
+//  * the selection CTA keeps the per-request state, waits for the R * t arrivals of a layer, stages
+//    all slice lists and partials in shared memory with one round of L2 loads, merges every row
+//    (one warp per row: Z, threshold, survivors, rank; expand_core.cuh merge_row) straight into the
+//    selection's staged candidate records, runs A3-A6 (select_layer) and publishes the next
+//    frontier as flag[l+1] = (tag << 32 | R').  After the last layer it writes the verify-row table
+//    and publishes flag[kVerifySlot]; the streaming CTAs stream every tree row of the target logits
+//    (exact argmax, red.max on the row's slot) while it writes the mask outputs; then it walks.
+// There is no leader merge and no cluster: the only cross-SM hops per layer are the slice arrivals
+// and the frontier flag.
+#include "expand_core.cuh"
+#include "select_core.cuh"
+#include "verify_core.cuh"
+
+namespace smart {
+
+namespace {
+
+constexpr int kStepThreads = kLayerThreads;  // 8 consumer warps + 1 producer warp
+constexpr int kProducerWarp = kConsumerWarps;
+constexpr int kTeamMax = 32;                  // slices per row (one list per lane in the merge)
+
+struct __align__(16) StepShared {
+  ConsShared cs;
+  float2 msl[kMaxCpr * kConsumerWarps];  // (chunk, warp) softmax partials of the current slice
+  // producer -> consumers: the value of event e (the row count of layer e + 2, or the verify rows)
+  // is rv[e], valid once ev > e (a monotonic counter: no phase aliasing however far ahead the
+  // producer runs)
+  int rv[SMART_MAX_DEPTH + 2];
+  unsigned ev;
+};
+
+__device__ __forceinline__ void post_event(StepShared& sh, int e, int v) {
+  sh.rv[e] = v;
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&sh.ev)), "r"((unsigned)(e + 1)) : "memory");
+}
+__device__ __forceinline__ int wait_event(StepShared& sh, int e) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&sh.ev)) : "memory");
+      if (v > (unsigned)e) break;
+      __nanosleep(32);
+    }
+  }
+  __syncwarp();
+  return *reinterpret_cast<volatile int*>(&sh.rv[e]);
+}
+
+// row stride of the per-chunk partials (even: a layer's partials are whole 16-byte units)
+__host__ __device__ inline int ms_stride(int cpr) { return (cpr + 1) & ~1; }
+
+__host__ __device__ inline int team_size(int R, int S, int cpr) {
+  if (R <= 0 || R >= S) return 1;
+  int t = S / R;
+  if (t > cpr) t = cpr;
+  if (t > kTeamMax) t = kTeamMax;
+  return t;
+}
+
+// balanced contiguous unit ranges over g = min(gmax, ceil(total / min_units)) CTAs
+__host__ __device__ inline int range_ctas(int total, int gmax, int min_units) {
+  const int g = (total + min_units - 1) / min_units;
+  return g < gmax ? g : gmax;
+}
+__device__ __forceinline__ RowRange range_of(int total, int gmax, int min_units, int b) {
+  const int g = range_ctas(total, gmax, min_units);
+  RowRange r;
+  if (b >= g) {
+    r.lo = r.hi = 0;
+    return r;
+  }
+  const int base = total / g, rem = total - base * g;
+  r.lo = b * base + min(b, rem);
+  r.hi = r.lo + base + (b < rem ? 1 : 0);
+  return r;
+}
+
+// Polls use relaxed loads and one acquire fence once the value is seen (relaxed load + fence =
+// acquire pattern): an ld.acquire per poll compiles to LDG + CCTL.IVALL, and a stream of L1
+// invalidations from a spinning lane slows every warp sharing the SM.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Polls are bounded (~2^24 tries, seconds): a broken protocol sets the sticky kErrTimeout
+// flag (SMART_EDEVICE from smart_get_stats) and lets the step run out instead of hanging the GPU.
+constexpr unsigned kPollLimit = 1u << 24;
+
+// poll a (tag << 32 | value) flag of this launch; returns the value (0 on timeout)
+__device__ __forceinline__ int wait_tag(const unsigned long long* f, unsigned tag, int* err) {
+  for (unsigned it = 0;; ++it) {
+    const unsigned long long v = ld_relaxed_u64(f);
+    if ((unsigned)(v >> 32) == tag) {
+      fence_acq_rel_gpu();
+      return (int)(unsigned)v;
+    }
+    if (it > kPollLimit) {
+      atomicOr(err, kErrTimeout);
+      return 0;
+    }
+    __nanosleep(20);
+  }
+}
+// poll an arrival counter until it reaches `want`
+__device__ __forceinline__ void wait_count(const int* c, int want, int* err) {
+  for (unsigned it = 0; ld_relaxed_s32(c) < want; ++it) {
+    if (it > kPollLimit) {
+      atomicOr(err, kErrTimeout);
+      return;
+    }
+    __nanosleep(20);
+  }
+  fence_acq_rel_gpu();
+}
+
+// timeline probes (SMART_PROBES=1 builds only): dbg[256 + 16 * layer + slot], globaltimer ns;
+// "max" slots keep the latest time, "min" slots the complement of the earliest (atomicMax of ~t)
+enum { kPbArrived = 0, kPbMerged = 1, kPbPublished = 2, kPbFlagMin = 3, kPbFlagMax = 4, kPbSliceMax = 5,
+       kPbChunkMin = 6, kPbChunkMax = 7, kPbSelDone = 8, kPbSync1 = 9, kPbStaged = 10, kPbConsumed1 = 11,
+       kPbPosted = 12 };
+__device__ __forceinline__ unsigned smid_reg() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void pb_max(const Params& P, int layer, int slot) {
+  if (SMART_PROBES && P.dbg) atomicMax(&P.dbg[256 + 16 * layer + slot], gtime());
+}
+__device__ __forceinline__ void pb_min(const Params& P, int layer, int slot) {
+  if (SMART_PROBES && P.dbg) atomicMax(&P.dbg[256 + 16 * layer + slot], ~gtime());
+}
+
+// ---------------------------------------------------------------------------------------------
+// streaming CTA
+// ---------------------------------------------------------------------------------------------
+template <bool BF16>
+__device__ void stream_role(const Params& P, char* dsm, const char* __restrict__ draft, long long ld_d,
+                            const char* __restrict__ target, long long ld_t, unsigned tag) {
+  char* ring = dsm;
+  StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
+  StepShared& sh = *reinterpret_cast<StepShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = P.step_S, s = (int)blockIdx.x;
+  const int k = P.k, cpr = P.cpr, kp = list_stride(k), T = P.T;
+  const long long row_bytes = (long long)P.V * (BF16 ? 2 : 4);
+  int R = P.d > 0 ? P.b_loc : 0;
+  int layer = 1;
+
+  if (warp == kProducerWarp) {
+    if (lane != 0) return;
+    int i = 0;  // the CTA's running chunk counter (ring stage and phase), same sequence as the consumers
+    int ev = 0;
+    auto issue = [&](const char* base, int c) {
+      const int st = i % kStages;
+      mbar_wait(&pipe.empty[st], ((uint32_t)(i / kStages) & 1u) ^ 1u);
+      const long long off = (long long)c * kChunkBytes;
+      const uint32_t bytes = (uint32_t)min((long long)kChunkBytes, row_bytes - off);
+      mbar_expect_tx(&pipe.full[st], bytes);
+      bulk_g2s(ring + (size_t)st * kChunkBytes, base + off, bytes, &pipe.full[st]);
+      ++i;
+    };
+    while (R > 0 && layer <= P.d) {
+      const int t = team_size(R, S, cpr);
+      const int nteams = S / t, team = s / t, member = s - team * t;
+      const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;
+      const int par = (layer - 1) & 1;
+      if (team < nteams) {
+        for (int row = team; row < R; row += nteams) {
+          int r = row, node = 0;  // layer 1: the roots
+          if (layer > 1) {
+            const int2 fe = __ldcg(&P.fr[par][row]);
+            r = fe.x;
+            node = fe.y;
+          }
+          const char* base = P.row_mode == SMART_ROWS_POSITION ? draft + ((long long)r * P.d + (layer - 1)) * ld_d
+                                                                : draft + ((long long)r * T + node) * ld_d;
+          for (int c = mlo; c < mhi; ++c) issue(base, c);
+        }
+      }
+      const int Rn = layer < P.d ? wait_tag(&P.ctl->flag[layer + 1], tag, P.err) : 0;
+      if (layer < P.d) {
+        pb_min(P, layer + 1, kPbFlagMin);
+        pb_max(P, layer + 1, kPbFlagMax);
+      }
+      post_event(sh, ev++, Rn);
+      R = Rn;
+      ++layer;
+    }
+    const int NR = wait_tag(&P.ctl->flag[kVerifySlot], tag, P.err);
+    pb_min(P, kVerifySlot, kPbFlagMin);
+    pb_max(P, kVerifySlot, kPbFlagMax);
+    post_event(sh, ev++, NR);
+    if (NR > 0) {
+      const RowRange rr = range_of(NR * cpr, S, P.min_units, s);
+      int row = rr.lo / cpr, c = rr.lo - row * cpr;
+      const char* base = nullptr;
+      for (int q = rr.lo; q < rr.hi; ++q) {
+        if (q == rr.lo || c == 0) {
+          const int2 e = __ldcg(&P.vrow_rn[row]);
+          base = target + ((long long)e.x * T + e.y) * ld_t;
+        }
+        issue(base, c);
+        if (++c == cpr) {
+          c = 0;
+          ++row;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps ----
+  int i = 0, ev = 0, wcnt = 0;
+  while (R > 0 && layer <= P.d) {
+    const int t = team_size(R, S, cpr);
+    const int nteams = S / t, team = s / t, member = s - team * t;
+    const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;
+    if (team < nteams) {
+      for (int row = team; row < R; row += nteams) {
+        unsigned long long bound = 0ull;  // lower bound of the slice's k-th best key
+        for (int c = mlo; c < mhi; ++c, ++i) {
+          const int st = i % kStages;
+          const char* stage = ring + (size_t)st * kChunkBytes;
+          mbar_wait(&pipe.full[st], ((uint32_t)(i / kStages)) & 1u);
+          if (tid == 0 && c == mlo) {
+            pb_min(P, layer, kPbChunkMin);
+            pb_max(P, layer, kPbChunkMax);
+            if (SMART_PROBES && P.dbg && layer == 2) P.dbg[1024 + 4 * s] = gtime();
+          }
+          uint4 raw[kVecPerThread];
+          const uint4* sv = reinterpret_cast<const uint4*>(stage);
+#pragma unroll
+          for (int j = 0; j < kVecPerThread; ++j) raw[j] = sv[j * kConsumers + tid];
+          consume_chunk<BF16, true>(P, sh.cs, sh.msl, raw, stage, nullptr, c, mlo, mhi, i, wcnt, bound);
+          __syncwarp();
+          if (tid == 0 && c == mlo) pb_max(P, layer, kPbConsumed1);
+          if (SMART_PROBES && P.dbg && layer == 2 && tid == 0 && c == mlo) P.dbg[1024 + 4 * s + 1] = gtime();
+          if (lane == 0) mbar_arrive(&pipe.empty[st]);  // release the stage
+        }
+        // slice end: the CTA's top-k and per-chunk partials straight to global memory
+        slice_end_post(sh.cs, k, wcnt);
+        if (tid == 0) pb_max(P, layer, kPbPosted);
+        if (SMART_PROBES && P.dbg && layer == 2 && tid == 0) {
+          P.dbg[1024 + 4 * s + 2] = gtime();
+          P.dbg[1024 + 4 * s + 3] = (unsigned long long)(mhi - mlo) | ((unsigned long long)row << 8) | ((unsigned long long)smid_reg() << 16);
+        }
+        unsigned long long* gk = P.seg_keys + (size_t)(row * t + member) * kp;
+        float2* gm = P.seg_ms + (size_t)row * ms_stride(cpr) + mlo;
+        slice_end_merge(
+            sh.cs, sh.msl, k, mhi - mlo, [&](int rank, unsigned long long key) { gk[rank] = key; },
+            [&](int cc, float Mc, float Sc) { gm[cc] = make_float2(Mc, Sc); });
+        consumer_sync();  // the slice's records are written (cumulative release below)
+        if (tid == 0) {
+          pb_max(P, layer, kPbSliceMax);
+          red_add_release_gpu(&P.ctl->arrive[layer], 1);
+          sh.cs.tau = 0ull;  // next slice (read only after the next slice's first barrier)
+        }
+      }
+    }
+    R = wait_event(sh, ev++);
+    ++layer;
+  }
+  // ---- A8 stream: every tree row of the target logits, exact argmax per row segment ----
+  const int NR = wait_event(sh, ev++);
+  if (NR <= 0) return;
+  const RowRange rr = range_of(NR * cpr, S, P.min_units, s);
+  if (rr.lo >= rr.hi) return;
+  int nanf = 0;
+  int q = rr.lo, row = rr.lo / cpr, c0 = rr.lo - row * cpr;
+  while (q < rr.hi) {
+    const int nch = min(cpr - c0, rr.hi - q);
+    const int2 rn = __ldcg(&P.vrow_rn[row]);
+    float bv = -INFINITY;
+    int bi = kIdxSentinel;
+    for (int c = c0; c < c0 + nch; ++c, ++i) {
+      const int st = i % kStages;
+      mbar_wait(&pipe.full[st], ((uint32_t)(i / kStages)) & 1u);
+      uint4 raw[kVecPerThread];
+      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunkBytes);
+#pragma unroll
+      for (int j = 0; j < kVecPerThread; ++j) raw[j] = sv[j * kConsumers + tid];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pipe.empty[st]);
+      verify_chunk<BF16, false>(raw, c * P.chunk_elems, P.V, tid, 0u, 1.f, bv, bi, nanf);
+    }
+    if (lane == 0 && bi != kIdxSentinel) {
+      const unsigned long long key = ((unsigned long long)vkey_orderable(bv) << 32) | (0xffffffffu - (unsigned)bi);
+      asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(P.vbest + (size_t)rn.x * T + rn.y), "l"(key)
+                   : "memory");
+    }
+    q += nch;
+    ++row;
+    c0 = 0;
+  }
+  if (nanf) atomicOr(P.err, kErrTargetNaN);
+  consumer_sync();
+  if (tid == 0) {
+    pb_max(P, kVerifySlot, kPbSliceMax);
+    red_add_release_gpu(&P.ctl->arrive[kVerifySlot], 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// selection CTA
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+struct MergeLayout {
+  int2* fe;                 // [rows] frontier entry (request, node)
+  float* pc;                // [rows] parent cum
+  int* slot;                // [rows] frontier slot within the request
+  unsigned long long* keys; // staged slice lists [R * t * kp]
+  float2* ms;               // staged per-chunk partials [R * cpr]
+};
+
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline size_t merge_bytes(int rows_cap, int key_cap, int cpr, int k) {
+  return a16((size_t)rows_cap * 8) + a16((size_t)rows_cap * 4) + a16((size_t)rows_cap * 4) +
+         a16((size_t)key_cap * list_stride(k) * 8) + a16((size_t)rows_cap * ms_stride(cpr) * 8);
+}
+
+__device__ inline MergeLayout merge_layout(char* p, int rows_cap, int key_cap, int cpr, int k) {
+  MergeLayout M;
+  M.fe = reinterpret_cast<int2*>(p);
+  p += a16((size_t)rows_cap * 8);
+  M.pc = reinterpret_cast<float*>(p);
+  p += a16((size_t)rows_cap * 4);
+  M.slot = reinterpret_cast<int*>(p);
+  p += a16((size_t)rows_cap * 4);
+  M.keys = reinterpret_cast<unsigned long long*>(p);
+  p += a16((size_t)key_cap * list_stride(k) * 8);
+  M.ms = reinterpret_cast<float2*>(p);
+  return M;
+}
+
+template <bool BF16>
+__device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const int32_t* root_tok,
+                            const int32_t* root_pos, const StepOut& out, bool verify, unsigned tag) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp >= kConsumerWarps) return;
+  const int S = P.step_S, k = P.k, cpr = P.cpr, kp = list_stride(k), T = P.T, bl = P.b_loc;
+  const int rows_cap = P.cap_rows > bl ? P.cap_rows : bl;
+  const int key_cap = S > rows_cap ? S : rows_cap;
+  MergeLayout M = merge_layout(dsm + a16(sel_bytes), rows_cap, key_cap, cpr, k);
+
+  // ---- begin step: S_0 = A_0 = {root} for every request ----
+  for (int r = tid; r < bl; r += kConsumers) {
+    const size_t o = (size_t)r * T;
+    P.n_nodes[r] = 1;
+    P.tok[o] = root_tok ? root_tok[r] : -1;
+    P.parent[o] = -1;
+    P.depth[o] = 0;
+    P.p[o] = 1.f;  // root: p = cum = 1
+    P.cum[o] = 1.f;
+    P.path_sum[o] = 0.0;
+    P.E_r[r] = 0.0;
+    P.leaf_cnt[r] = 1;
+    P.leaf_sum[r] = 0.0;
+    P.finished[r] = 0;
+    P.root_pos[r] = root_pos ? root_pos[r] : 0;
+    P.fr[0][r] = make_int2(r, 0);
+    P.fr_cum[0][r] = 1.f;
+    P.fr_cnt[0][r] = 1;
+    P.fr_off[0][r] = r;
+  }
+  if (tid < SMART_MAX_DEPTH) {
+    DevTrace t0{};
+    P.trace[tid] = t0;
+  }
+  if (tid == 0) {
+    *P.fr_total[0] = bl;
+    *P.err = 0;
+    *P.sum_accept = 0ull;
+    *P.N_glob = 0;
+    *P.E_glob = 0.0;
+  }
+  consumer_sync();
+
+  for (int layer = 1; layer <= P.d; ++layer) {
+    const int par = (layer - 1) & 1;
+    const int R = *P.fr_total[par];
+    if (R == 0) break;
+    const int t = team_size(R, S, cpr);
+    const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+    auto wait_merge = [&](SelLayout& L, int4* crec) -> bool {
+      // row descriptors (this CTA's own writes) while the rows stream
+      for (int row = tid; row < R; row += kConsumers) {
+        const int2 fe = P.fr[par][row];
+        M.fe[row] = fe;
+        M.pc[row] = P.fr_cum[par][row];
+        M.slot[row] = row - P.fr_off[par][fe.x];
+      }
+      if (tid == 0) {
+        const int want = R * t;
+        wait_count(&P.ctl->arrive[layer], want, P.err);
+        P.ctl->arrive[layer] = 0;  // no further arrivals this step
+        pb_max(P, layer, kPbArrived);
+      }
+      consumer_sync();
+      if (tid == 0) pb_max(P, layer, kPbSync1);
+      // one round of L2 loads (cp.async, 16-byte units): every slice list and chunk partial
+      {
+        const int nk2 = R * t * kp / 2;  // kp even
+        const int nm2 = R * ms_stride(cpr) / 2;
+        const int4* gk = reinterpret_cast<const int4*>(P.seg_keys);
+        const int4* gm = reinterpret_cast<const int4*>(P.seg_ms);
+        int4* sk = reinterpret_cast<int4*>(M.keys);
+        int4* smv = reinterpret_cast<int4*>(M.ms);
+        for (int e = tid; e < nk2; e += kConsumers) cp_async16(sk + e, gk + e);
+        for (int e = tid; e < nm2; e += kConsumers) cp_async16(smv + e, gm + e);
+        cp_async_wait_all();
+      }
+      consumer_sync();
+      if (tid == 0) pb_max(P, layer, kPbStaged);
+      // row merges (k-round tournaments over the t sorted slice lists), one warp per row,
+      // straight into the selection's staged records
+      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[900 + layer * 8] = clock64();
+      const int mss = ms_stride(cpr);
+      for (int row = warp; row < R; row += kConsumerWarps) {
+        const int2 fe = M.fe[row];
+        const unsigned long long* keys = M.keys + (size_t)row * t * kp;
+        const float2* ms = M.ms + (size_t)row * mss;
+        Cand* gout = P.cand + lbase + (size_t)row * k;
+        int4* sout = crec + row * k;
+        const bool ok = merge_row_tournament(
+            k, cpr, t, M.pc[row],
+            [&](int c) {
+              const float2 v = ms[c];
+              return make_float4(v.x, v.y, 0.f, 0.f);
+            },
+            [&](int m, int j) { return keys[m * kp + j]; },
+            [&](int rank, int tok, float p, float cum) {
+              sout[rank] = make_int4(tok, __float_as_int(p), __float_as_int(cum), fe.y);
+              Cand cd;
+              cd.tok = tok;
+              cd.p = p;
+              cd.cum = cum;
+              cd.parent = fe.y;
+              gout[rank] = cd;
+            });
+        if (SMART_PROBES && P.dbg && tid == 0 && row == 0) P.dbg[901 + layer * 8] = clock64();
+        if (lane == 0) {
+          L.rreq[row] = fe.x;
+          P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, M.slot[row]);
+          if (!ok) atomicOr(P.err, kErrDraftNaN);  // Q23
+        }
+      }
+      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[902 + layer * 8] = clock64();
+      consumer_sync();
+      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[903 + layer * 8] = clock64();
+      if (tid == 0) pb_max(P, layer, kPbMerged);
+      return true;
+    };
+    auto pub = [&](int tot) {
+      if (layer < P.d) st_release_u64(&P.ctl->flag[layer + 1], ((unsigned long long)tag << 32) | (unsigned)tot);
+      pb_max(P, layer, kPbPublished);
+    };
+    select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, pub);
+    consumer_sync();
+    if (tid == 0) pb_max(P, layer, kPbSelDone);
+    if (SMART_PROBES && P.dbg && tid == 0)  // the selection's clock64 phase stamps of this layer
+      for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
+  }
+
+  // ---- the final trees, staged in shared memory with one round of loads (this CTA's writes) ----
+  int* s_n = reinterpret_cast<int*>(dsm);                // [bl + 1] node counts, [bl + 1] scan scratch
+  int* s_par = s_n + a16((size_t)(2 * bl + 2) * 4) / 4;  // [bl * T] parent, depth, token, target argmax
+  int* s_dep = s_par + (size_t)bl * T;
+  int* s_tok = s_dep + (size_t)bl * T;
+  int* s_arg = s_tok + (size_t)bl * T;
+  for (int r = tid; r < bl; r += kConsumers) s_n[r] = P.n_nodes[r];
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    s_par[e] = P.parent[e];
+    s_dep[e] = P.depth[e];
+    s_tok[e] = P.tok[e];
+  }
+  consumer_sync();
+  // verify rows: (request, node) of every tree row, request-major (A8 reads all of them)
+  int NR = 0;
+  if (warp == 0) {
+    int* s_off = s_n + bl + 1;  // scratch copy for the scan (the counts stay in s_n)
+    for (int r = lane; r < bl; r += 32) s_off[r] = s_n[r];
+    __syncwarp();
+    NR = warp_excl_scan_smem(s_off, bl, lane);
+    for (int r = 0; r < bl; ++r) {
+      const int o = s_off[r], n = s_n[r];
+      for (int j = lane; j < n; j += 32) P.vrow_rn[o + j] = make_int2(r, j);
+      if (lane == 0) P.vrow_off[r] = o;
+    }
+    if (lane == 0) P.vrow_off[bl] = NR;
+    __syncwarp();
+    if (lane == 0) {
+      st_release_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
+      pb_max(P, kVerifySlot, kPbPublished);
+    }
+  }
+  // ---- A7 while the target rows stream: ancestor-or-self bit rows, positions, parents, tokens ----
+  const int MW = P.MW;
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    const int r = e / T, j = e - r * T;
+    const int n = s_n[r];
+    const int* sp = s_par + (size_t)r * T;
+    if (j < n) {
+      if (out.mask) {
+        for (int w = 0; w < MW; ++w) {
+          uint32_t word = 0;
+          for (int a = j; a >= 0; a = sp[a])  // ancestor-or-self chain (depth <= 16)
+            if ((a >> 5) == w) word |= 1u << (a & 31);
+          out.mask[(size_t)e * MW + w] = word;
+        }
+      }
+      if (out.pos) out.pos[e] = P.root_pos[r] + s_dep[e];
+      if (out.parent) out.parent[e] = sp[j];
+      if (out.tok) out.tok[e] = s_tok[e];
+    } else {
+      if (out.mask)
+        for (int w = 0; w < MW; ++w) out.mask[(size_t)e * MW + w] = 0u;
+      if (out.pos) out.pos[e] = 0;
+      if (out.parent) out.parent[e] = -1;
+      if (out.tok) out.tok[e] = -1;
+    }
+  }
+  for (int r = tid; r < bl && out.tree_len; r += kConsumers) out.tree_len[r] = s_n[r];
+  if (tid == 0) pb_max(P, kVerifySlot, kPbMerged);  // mask outputs written
+  NR = __shfl_sync(kFull, NR, 0);
+  if (warp == 0 && lane == 0) s_n[bl] = NR;
+  consumer_sync();
+  NR = s_n[bl];
+  if (!verify || NR == 0) return;
+
+  // ---- A8 walk once every verify slice has posted its row maxima ----
+  if (tid == 0) {
+    const int want = range_ctas(NR * cpr, S, P.min_units);
+    wait_count(&P.ctl->arrive[kVerifySlot], want, P.err);
+    P.ctl->arrive[kVerifySlot] = 0;
+    pb_max(P, kVerifySlot, kPbArrived);
+  }
+  consumer_sync();
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    const int r = e / T;
+    if (e - r * T < s_n[r]) {
+      unsigned long long* slot = P.vbest + e;
+      s_arg[e] = (int)(0xffffffffu - (uint32_t)__ldcg(slot));
+      *slot = 0ull;  // cleared for the next step
+    }
+  }
+  consumer_sync();
+  const int D = P.d > 0 ? P.d : 1;
+  for (int r = warp; r < bl; r += kConsumerWarps) {
+    const int n = s_n[r];
+    const int* sp = s_par + (size_t)r * T;
+    const int* st = s_tok + (size_t)r * T;
+    const int* sa = s_arg + (size_t)r * T;
+    int cur = 0, acc = 0, bon = -1;
+    for (;;) {
+      const int tgt = sa[cur];
+      int found = -1;
+      for (int j0 = cur + 1; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const bool f = j < n && sp[j] == cur && st[j] == tgt;
+        const unsigned bal = __ballot_sync(kFull, f);
+        if (bal) {
+          found = j0 + __ffs(bal) - 1;
+          break;
+        }
+      }
+      if (found < 0) {
+        bon = tgt;
+        break;
+      }
+      if (lane == 0 && out.accept_path && acc < D) out.accept_path[(size_t)r * D + acc] = found;
+      ++acc;
+      cur = found;
+    }
+    if (lane == 0) {
+      if (out.accept_len) out.accept_len[r] = acc;
+      if (out.bonus) out.bonus[r] = bon;
+      atomicAdd(P.sum_accept, (unsigned long long)acc);
+    }
+    if (out.accept_path)
+      for (int j = acc + lane; j < D; j += 32) out.accept_path[(size_t)r * D + j] = -1;
+  }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kStepThreads, 2)
+step_kernel(Params P, size_t sel_bytes, const char* __restrict__ draft, long long ld_d, const char* __restrict__ target,
+            long long ld_t, const int32_t* root_tok, const int32_t* root_pos, StepOut out) {
+  extern __shared__ __align__(128) char dsm[];
+  __shared__ unsigned s_tag;
+  const bool sel = (int)blockIdx.x == (int)gridDim.x - 1;
+  if (!sel && threadIdx.x == 0) {
+    StreamPipe& pipe = *reinterpret_cast<StreamPipe*>(dsm + kStages * kChunkBytes);
+    StepShared& sh = *reinterpret_cast<StepShared*>(dsm + kStages * kChunkBytes + sizeof(StreamPipe));
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&pipe.full[s], 1);
+      mbar_init(&pipe.empty[s], kConsumerWarps);
+    }
+    sh.ev = 0u;
+    mbar_fence_init();
+    sh.cs.tau = 0ull;
+  }
+  pdl_wait();  // the previous kernel of the stream (e.g. the previous step) has completed
+  if (threadIdx.x == 0) s_tag = __ldcg(&P.ctl->epoch) + 1u;
+  if (threadIdx.x == 0) pb_min(P, 0, kPbFlagMin);  // kernel start (earliest CTA)
+  __syncthreads();
+  const unsigned tag = s_tag;
+  if (sel) select_role<BF16>(P, dsm, sel_bytes, root_tok, root_pos, out, target != nullptr, tag);
+  else stream_role<BF16>(P, dsm, draft, ld_d, target, ld_t, tag);
+  __syncthreads();
+  if (threadIdx.x == 0) pb_max(P, 0, kPbSelDone);  // kernel end (latest CTA)
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&P.ctl->exit_cnt, 1) == (int)gridDim.x - 1) {  // the last CTA: next launch's epoch
+      P.ctl->exit_cnt = 0;
+      P.ctl->epoch = tag;
+    }
+  }
+}
+
+}  // namespace
+
+size_t step_stream_smem_bytes() { return (size_t)kStages * kChunkBytes + sizeof(StreamPipe) + sizeof(StepShared); }
+
+size_t step_select_smem_bytes(const Params& P, int S, size_t sel_bytes) {
+  const int rows_cap = P.cap_rows > P.b_loc ? P.cap_rows : P.b_loc;
+  const int key_cap = S > rows_cap ? S : rows_cap;
+  const size_t sel = a16(sel_bytes) + merge_bytes(rows_cap, key_cap, P.cpr, P.k);
+  const size_t fin = a16((size_t)(2 * P.b_loc + 2) * 4) + (size_t)4 * P.b_loc * P.T * 4;
+  return sel > fin ? sel : fin;
+}
+
+// grid of the step kernel (all CTAs co-resident: grid = SMs x occupancy) and its dynamic shared
+// memory (the larger of the streaming CTA's ring and the selection CTA's scratch); 0 if the
+// selection scratch does not fit one CTA
+int step_grid(const Params& P, size_t sel_bytes, size_t* smem_out) {
+  int dev = 0, nsm = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, step_kernel<true>);
+  const int lim = optin - (int)fa.sharedSizeBytes;  // dynamic + static <= the opt-in maximum
+  for (int b = 0; b < 2; ++b) {
+    cudaFuncSetAttribute(b ? step_kernel<true> : step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(b ? step_kernel<true> : step_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+  }
+  size_t smem = step_stream_smem_bytes();
+  int grid = 0;
+  for (int it = 0; it < 3; ++it) {
+    int occ = 0;
+    if (smem > (size_t)lim ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_kernel<true>, kStepThreads, smem) != cudaSuccess ||
+        occ < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+    grid = nsm * occ;
+    const size_t need = std::max(step_stream_smem_bytes(), step_select_smem_bytes(P, grid - 1, sel_bytes));
+    if (need <= smem) break;
+    smem = need;  // fewer CTAs per SM: recompute the grid (the scratch shrinks with S)
+  }
+  *smem_out = smem;
+  return grid;
+}
+
+void launch_step(const Params& P, int grid, size_t smem, size_t sel_bytes, const void* draft, long long ld_d,
+                 const void* target, long long ld_t, const int32_t* root_tok, const int32_t* root_pos,
+                 const StepOut& out, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  Params Q = P;
+  Q.step_S = grid - 1;
+  Q.sel_rec = 1;  // the row merge stages the candidate records in the selection's scratch
+  const char* d = static_cast<const char*>(draft);
+  const char* t = static_cast<const char*>(target);
+  if (P.dtype == SMART_BF16)
+    cudaLaunchKernelEx(&cfg, step_kernel<true>, Q, sel_bytes, d, ld_d, t, ld_t, root_tok, root_pos, out);
+  else
+    cudaLaunchKernelEx(&cfg, step_kernel<false>, Q, sel_bytes, d, ld_d, t, ld_t, root_tok, root_pos, out);
+}
+
+}  // namespace smart

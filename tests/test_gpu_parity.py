@@ -30,11 +30,18 @@ def _T(case):
 
 
 def _run(case, **kw):
+    """The oracle against BOTH CUDA paths on the same inputs: the per-layer C-ABI calls (the
+    layer kernels a real draft model interleaves with) and smart_run_step (the persistent
+    whole-step kernel, step.cu)."""
     T = _T(case)
     draft, target, rt, rp = make_inputs(case, T)
     orc = run_oracle(case, draft, target, rt, rp)
     gpu = run_gpu(case, draft, target, rt, rp, **kw)
-    return orc, gpu, compare(case, orc, gpu)
+    layers = compare(case, orc, gpu)
+    if not kw:
+        step = run_gpu(case, draft, target, rt, rp, use_run_step=True)
+        assert compare(case, orc, step) == layers
+    return orc, gpu, layers
 
 
 # ---- the toy worked example (cfg1) ----------------------------------------------------------
