@@ -20,6 +20,17 @@
 
 namespace smart {
 
+#ifndef CONSUME_STAMPS
+#define CONSUME_STAMPS 0  // tools/ubench/consume.cu only: clock64 stamps of CTA 0, warp 0
+#endif
+#if CONSUME_STAMPS
+__device__ unsigned long long g_cstamp[64];
+#define CSTAMP(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_cstamp[i] = clock64()
+#else
+#define CSTAMP(i)
+#endif
+
 template <bool BF16>
 struct Traits {
   static constexpr int EPV = BF16 ? 8 : 4;         // elements per 16 B vector
@@ -123,6 +134,14 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = P.k, V = P.V, cpr = P.cpr;
   WarpTopk& W = sh.w[warp];
+#ifndef CONSUME_EXPERIMENT
+#define CONSUME_EXPERIMENT 0  // tools/ubench/consume.cu only: 1 stream only, 2 softmax only, 3 top-k only
+#endif
+  if (CONSUME_EXPERIMENT == 1) {
+    if (lane == 0) msl[(c - mlo) * kConsumerWarps + warp] = make_float2(__uint_as_float(raw[0].x), 0.f);
+    return;
+  }
+  CSTAMP(0 + 8 * (c - mlo));
   float x[EPT];
   unpack<BF16>(raw, x);
   const int cbase = c * P.chunk_elems;
@@ -145,9 +164,10 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   }
   const float m = fmaxf(fmaxf(vm[0], vm[1]), fmaxf(vm[2], vm[3]));
   const float Mw = warp_max_fast(m);
+  CSTAMP(1 + 8 * (c - mlo));
   // exp2(x*log2e - M*log2e) on element pairs: FFMA2 + 2 MUFU + FADD2 (two pair accumulators)
   unsigned long long acc2[2] = {0ull, 0ull};
-  if (Mw != -INFINITY) {
+  if (Mw != -INFINITY && CONSUME_EXPERIMENT != 3) {
     const float ML = Mw * kLog2e;
     const unsigned long long l2e2 = f2pk(kLog2e, kLog2e), nml2 = f2pk(-ML, -ML);
 #pragma unroll
@@ -158,6 +178,8 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   }
   const float sacc = warp_sum((f2lo(acc2[0]) + f2hi(acc2[0])) + (f2lo(acc2[1]) + f2hi(acc2[1])));
   if (lane == 0) msl[(c - mlo) * kConsumerWarps + warp] = make_float2(Mw, sacc);
+  CSTAMP(2 + 8 * (c - mlo));
+  if (CONSUME_EXPERIMENT == 2) return;
 
   // ---- top-k candidates of this warp-chunk ----
   // CTA-wide bound at the slice's first chunk: every warp publishes its top-j lane maxima
@@ -175,7 +197,9 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
       if (lane == __ffs(bal) - 1) rem = 0u;
       if (lane == 0) pub[warp * jr + r] = cur;
     }
+    CSTAMP(3 + 8 * (c - mlo));
     consumer_sync();
+    CSTAMP(4 + 8 * (c - mlo));
     const int np = kConsumerWarps * jr;  // multiple of 8
     unsigned vc = 0xffffffffu;
     for (int e = lane; e < np; e += 32) {
@@ -200,6 +224,7 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
     if (tt > bound) bound = tt;
   }
   float bv = bound ? tk_val(bound) : -INFINITY;
+  CSTAMP(5 + 8 * (c - mlo));
   if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
     // vectors whose max reaches the bound are expanded cooperatively: each group of EPV lanes
     // takes one such vector (its elements re-read from the still-held ring stage), compares them
@@ -245,6 +270,7 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
       }
     }
   }
+  CSTAMP(6 + 8 * (c - mlo));
   if (wcnt >= 2 * k && c + 1 < mhi) {  // keep the warp's buffer short
     __syncwarp();
     warp_compact(W, wcnt, k, lane);
@@ -252,6 +278,7 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
     if (W.list[k - 1] > bound) bound = W.list[k - 1];
     if (lane == 0) atomicMax(&sh.tau, W.list[k - 1]);
   }
+  CSTAMP(7 + 8 * (c - mlo));
 }
 
 // Slice end, part 1 (every consumer warp): the warp's padded top-k into sh.cl, then a consumer
@@ -263,9 +290,11 @@ __device__ __forceinline__ void slice_end_post(ConsShared& sh, int k, int& wcnt)
     warp_compact(W, wcnt, k, lane);
     wcnt = k;
   }
+  CSTAMP(40);
   if (lane < k) sh.cl[warp * k + lane] = lane < wcnt ? W.buf[lane] : kKeySentinel - 1 - (warp * k + lane);
   wcnt = 0;
   consumer_sync();
+  CSTAMP(41);
 }
 
 // Slice end, part 2 (after slice_end_post): the CTA's top-k of the slice by a rank merge of the
@@ -377,19 +406,21 @@ __device__ __forceinline__ bool merge_row(int k, int cpr, int t, float pc, MsAt 
 }
 
 // Row merge by a k-round tournament (A1 finish + A2), for t <= 32 slice lists each sorted best
-// first: lane m holds the head of list m (and the next entry, so a repeated winner does not wait
-// on a load); every round the warp's maximum key (two REDUX: value word, then index word among the
-// value's holders) is the row's next best and its lane advances.  Same outputs as merge_row.
-// key_at(m, j) reads entry j of list m.
-template <class MsAt, class KeyAt, class Emit>
-__device__ __forceinline__ bool merge_row_tournament(int k, int cpr, int t, float pc, MsAt ms, KeyAt key_at,
-                                                     Emit emit) {
+// first and held in shared memory at keys + m * kp: lane m holds the head of list m and the next
+// entry; every round the warp's maximum key (two REDUX: value word, then index word among the
+// value's holders) is the row's next best, and its lane advances branch-free (every lane reloads
+// its next entry from a precomputed 32-bit shared address).  Same outputs as merge_row.
+template <class MsAt, class Emit>
+__device__ __forceinline__ bool merge_row_tournament(int k, int cpr, int t, float pc, MsAt ms,
+                                                     const unsigned long long* keys, Emit emit) {
   const int lane = threadIdx.x & 31;
+  const int kp = list_stride(k);
   const float4 v0 = lane < cpr ? ms(lane) : make_float4(-INFINITY, 0.f, 0.f, 0.f);
   const float4 v1 = lane + 32 < cpr ? ms(lane + 32) : make_float4(-INFINITY, 0.f, 0.f, 0.f);
   const bool own = lane < t;
-  unsigned long long cur = own ? key_at(lane, 0) : 0ull;
-  unsigned long long nxt = own && k > 1 ? key_at(lane, 1) : 0ull;
+  const uint32_t base = smem_u32(keys + (own ? lane : 0) * kp);
+  unsigned long long cur = own ? keys[lane * kp] : 0ull;
+  unsigned long long nxt = own && k > 1 ? keys[lane * kp + 1] : 0ull;
   int h = 1;  // index of nxt in the lane's list
   const float M = warp_max_fast(fmaxf(v0.x, v1.x));
   const float ML = M * kLog2e;
@@ -403,17 +434,86 @@ __device__ __forceinline__ bool merge_row_tournament(int k, int cpr, int t, floa
     const unsigned hi = __reduce_max_sync(kFull, (unsigned)(cur >> 32));
     const unsigned lo = __reduce_max_sync(kFull, (unsigned)(cur >> 32) == hi ? (unsigned)cur : 0u);
     const unsigned long long win = ((unsigned long long)hi << 32) | lo;
-    if (lane == r) mine = win;
-    if (own && cur == win) {  // keys are distinct: exactly one lane advances
-      cur = nxt;
-      ++h;
-      nxt = h < k ? key_at(lane, h) : 0ull;
-    }
+    mine = lane == r ? win : mine;
+    const bool adv = own && cur == win;  // keys are distinct: exactly one lane advances
+    cur = adv ? nxt : cur;
+    h += adv ? 1 : 0;
+    unsigned long long ld;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ld) : "r"(base + 8u * (uint32_t)min(h, k - 1)));
+    nxt = adv ? (h < k ? ld : 0ull) : nxt;
   }
   if (lane < k) {
     const float v = tk_val(mine);
     const float pj = ex2(fmaf(v, kLog2e, -ML)) * rZ;  // p = exp(x - M) / Z   (tau = 1, Q10)
     emit(lane, tk_idx(mine), pj, pc * pj);            // Eq.(3)
+  }
+  __syncwarp();
+  return (Z >= 1.0f) && !isinf(Z) && !isnan(M);
+}
+
+// Row merge by threshold + rank (A1 finish + A2) for t <= 32 slice lists, each the top-k of its
+// slice sorted best first, in shared memory at keys + m * kp (kp = list_stride(k)).  No sequential
+// rounds: T = max(best k-th entry over the lists, k-th best list head) is a lower bound of the
+// row's k-th best key (each bounds it: a list's k-th entry is the k-th best of a subset; the k
+// largest heads are k distinct elements); the survivors (entries >= T, typically ~k) are compacted
+// and ranked by counting with broadcast loads.  Z from the cpr per-chunk partials as merge_row.
+// `surv` is a per-warp scratch of >= t * k keys.  Same outputs as merge_row.
+template <class MsAt, class Emit>
+__device__ __forceinline__ bool merge_row_rank(int k, int cpr, int t, float pc, MsAt ms,
+                                               const unsigned long long* keys, unsigned long long* surv, Emit emit) {
+  const int lane = threadIdx.x & 31;
+  const int kp = list_stride(k);
+  const bool own = lane < t;
+  const unsigned long long* my = keys + lane * kp;
+  const unsigned long long head = own ? my[0] : 0ull, tail = own ? my[k - 1] : 0ull;
+  const float4 v0 = lane < cpr ? ms(lane) : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+  const float4 v1 = lane + 32 < cpr ? ms(lane + 32) : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+  // (1) thresholds: the best tail (two reductions) and the k-th best head (rank among the heads)
+  const unsigned th = __reduce_max_sync(kFull, (unsigned)(tail >> 32));
+  const unsigned tl = __reduce_max_sync(kFull, (unsigned)(tail >> 32) == th ? (unsigned)tail : 0u);
+  unsigned long long T = ((unsigned long long)th << 32) | tl;
+  if (t >= k) {
+    int hr = 0;  // heads better than mine
+    for (int m = 0; m < t; ++m) hr += keys[m * kp] > head;
+    const unsigned bal = __ballot_sync(kFull, own && hr == k - 1);
+    const unsigned long long Th = __shfl_sync(kFull, head, __ffs(bal) - 1);
+    if (Th > T) T = Th;
+  }
+  // (2) softmax normaliser (independent of the top-k work)
+  const float M = warp_max_fast(fmaxf(v0.x, v1.x));
+  const float ML = M * kLog2e;
+  float z = 0.f;
+  z += (v0.y != 0.f || isnan(v0.y)) ? v0.y * ex2(fmaf(v0.x, kLog2e, -ML)) : 0.f;
+  z += (v1.y != 0.f || isnan(v1.y)) ? v1.y * ex2(fmaf(v1.x, kLog2e, -ML)) : 0.f;
+  const float Z = warp_sum(z);
+  const float rZ = __frcp_rn(Z);  // correctly rounded 1/Z (no division slow path)
+  // (3) survivors, compacted by ballots over the entry index j (lists are sorted: entries < T end
+  // a list's survivors, so the loop stops at the first j without any)
+  int ns = 0;
+  for (int j = 0; j < k; ++j) {
+    const unsigned long long key = own ? my[j] : 0ull;
+    const bool sv = own && key >= T;
+    const unsigned bal = __ballot_sync(kFull, sv);
+    if (!bal) break;
+    if (sv) surv[ns + __popc(bal & ((1u << lane) - 1u))] = key;
+    ns += __popc(bal);
+  }
+  __syncwarp();
+  // (4) exact ranks among the survivors (keys distinct); the top k emitted
+  auto out = [&](unsigned long long key, int rank) {
+    const float v = tk_val(key);
+    const float pj = ex2(fmaf(v, kLog2e, -ML)) * rZ;  // p = exp(x - M) / Z   (tau = 1, Q10)
+    emit(rank, tk_idx(key), pj, pc * pj);             // Eq.(3)
+  };
+  for (int s0 = lane; s0 < ns; s0 += 32) {
+    const unsigned long long key = surv[s0];
+    int r0 = 0, r1 = 0, q = 0;
+    for (; q + 1 < ns; q += 2) {
+      r0 += surv[q] > key;
+      r1 += surv[q + 1] > key;
+    }
+    if (q < ns) r0 += surv[q] > key;
+    if (r0 + r1 < k) out(key, r0 + r1);
   }
   __syncwarp();
   return (Z >= 1.0f) && !isinf(Z) && !isnan(M);

@@ -476,13 +476,12 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   }
 
   // ---- the layer's candidates (after the row merges): benefits b = cum / D_r (Eq.(13)) ----
-  if (wait_rows(L, crec)) {  // records and row requests already staged (crec, L.rreq)
+  if (wait_rows(L, crec)) {  // records and row requests already staged (crec, L.rreq); the
+                             // caller copies L.cb to P.cand_b after the frontier is published
     for (int q = tid; q < nct; q += NT) {
       const float cum = __int_as_float(crec[q].z);
       const float D = L.D[L.rreq[q / k]];
-      const float b = (D == 1.f) ? cum : __fdiv_rn(cum, D);
-      L.cb[q] = b;
-      P.cand_b[lbase + q] = b;
+      L.cb[q] = (D == 1.f) ? cum : __fdiv_rn(cum, D);
     }
   } else {
     for (int q = tid; q < nct; q += NT) {

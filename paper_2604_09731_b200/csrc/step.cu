@@ -453,7 +453,6 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
         const int2 fe = M.fe[row];
         const unsigned long long* keys = M.keys + (size_t)row * t * kp;
         const float2* ms = M.ms + (size_t)row * mss;
-        Cand* gout = P.cand + lbase + (size_t)row * k;
         int4* sout = crec + row * k;
         const bool ok = merge_row_tournament(
             k, cpr, t, M.pc[row],
@@ -461,20 +460,13 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
               const float2 v = ms[c];
               return make_float4(v.x, v.y, 0.f, 0.f);
             },
-            [&](int m, int j) { return keys[m * kp + j]; },
+            keys,
             [&](int rank, int tok, float p, float cum) {
               sout[rank] = make_int4(tok, __float_as_int(p), __float_as_int(cum), fe.y);
-              Cand cd;
-              cd.tok = tok;
-              cd.p = p;
-              cd.cum = cum;
-              cd.parent = fe.y;
-              gout[rank] = cd;
             });
         if (SMART_PROBES && P.dbg && tid == 0 && row == 0) P.dbg[901 + layer * 8] = clock64();
         if (lane == 0) {
           L.rreq[row] = fe.x;
-          P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(fe.x, M.slot[row]);
           if (!ok) atomicOr(P.err, kErrDraftNaN);  // Q23
         }
       }
@@ -490,11 +482,26 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     };
     select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, pub);
     consumer_sync();
+    // inspection copies (smart_get_candidates) after the frontier is out: the candidate records
+    // and each row's (request, slot), from the selection's staged records
+    {
+      const SelLayout L = sel_layout(dsm, bl, P.cap_rows * k, k, P.sort_cap);
+      const int4* crec = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(L.E) + sel_align((size_t)bl * 8) +
+                                                       2 * (size_t)P.sort_cap * 8);
+      int4* gc = reinterpret_cast<int4*>(P.cand + lbase);
+      for (int q = tid; q < R * k; q += kConsumers) {
+        gc[q] = crec[q];
+        P.cand_b[lbase + q] = L.cb[q];
+      }
+      for (int row = tid; row < R; row += kConsumers)
+        P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(M.fe[row].x, M.slot[row]);
+    }
     if (tid == 0) pb_max(P, layer, kPbSelDone);
     if (SMART_PROBES && P.dbg && tid == 0)  // the selection's clock64 phase stamps of this layer
       for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
   }
 
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1000] = gtime();
   // ---- the final trees, staged in shared memory with one round of loads (this CTA's writes) ----
   int* s_n = reinterpret_cast<int*>(dsm);                // [bl + 1] node counts, [bl + 1] scan scratch
   int* s_par = s_n + a16((size_t)(2 * bl + 2) * 4) / 4;  // [bl * T] parent, depth, token, target argmax
@@ -508,24 +515,27 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     s_tok[e] = P.tok[e];
   }
   consumer_sync();
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1001] = gtime();
   // verify rows: (request, node) of every tree row, request-major (A8 reads all of them)
-  int NR = 0;
+  int* s_off = s_n + bl + 1;  // exclusive scan of the node counts
   if (warp == 0) {
-    int* s_off = s_n + bl + 1;  // scratch copy for the scan (the counts stay in s_n)
     for (int r = lane; r < bl; r += 32) s_off[r] = s_n[r];
     __syncwarp();
-    NR = warp_excl_scan_smem(s_off, bl, lane);
-    for (int r = 0; r < bl; ++r) {
-      const int o = s_off[r], n = s_n[r];
-      for (int j = lane; j < n; j += 32) P.vrow_rn[o + j] = make_int2(r, j);
-      if (lane == 0) P.vrow_off[r] = o;
-    }
-    if (lane == 0) P.vrow_off[bl] = NR;
-    __syncwarp();
-    if (lane == 0) {
-      st_release_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
-      pb_max(P, kVerifySlot, kPbPublished);
-    }
+    const int tot = warp_excl_scan_smem(s_off, bl, lane);
+    if (lane == 0) s_off[bl] = tot;
+  }
+  consumer_sync();
+  const int NR = s_off[bl];
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    const int r = e / T, j = e - r * T;
+    if (j < s_n[r]) P.vrow_rn[s_off[r] + j] = make_int2(r, j);
+  }
+  for (int r = tid; r <= bl; r += kConsumers) P.vrow_off[r] = s_off[r];
+  consumer_sync();  // the table is written (cumulative release below)
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1002] = gtime();
+  if (tid == 0) {
+    st_release_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
+    pb_max(P, kVerifySlot, kPbPublished);
   }
   // ---- A7 while the target rows stream: ancestor-or-self bit rows, positions, parents, tokens ----
   const int MW = P.MW;
@@ -554,11 +564,19 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     }
   }
   for (int r = tid; r < bl && out.tree_len; r += kConsumers) out.tree_len[r] = s_n[r];
-  if (tid == 0) pb_max(P, kVerifySlot, kPbMerged);  // mask outputs written
-  NR = __shfl_sync(kFull, NR, 0);
-  if (warp == 0 && lane == 0) s_n[bl] = NR;
+  // first child of every node (children of a node are contiguous in canonical order: a layer's
+  // nodes are numbered by (frontier slot, rank)); -1 = leaf
+  int* s_fc = s_arg + (size_t)bl * T;
+  for (int e = tid; e < bl * T; e += kConsumers) s_fc[e] = -1;
   consumer_sync();
-  NR = s_n[bl];
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    const int r = e / T, j = e - r * T;
+    if (j >= 1 && j < s_n[r]) {
+      const int p = s_par[e];
+      if (s_par[e - 1] != p || j == 1) s_fc[(size_t)r * T + p] = j;
+    }
+  }
+  if (tid == 0) pb_max(P, kVerifySlot, kPbMerged);  // mask outputs written
   if (!verify || NR == 0) return;
 
   // ---- A8 walk once every verify slice has posted its row maxima ----
@@ -578,41 +596,40 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     }
   }
   consumer_sync();
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1003] = gtime();
   const int D = P.d > 0 ? P.d : 1;
-  for (int r = warp; r < bl; r += kConsumerWarps) {
+  unsigned long long accs = 0ull;
+  for (int r = tid; r < bl; r += kConsumers) {
     const int n = s_n[r];
     const int* sp = s_par + (size_t)r * T;
     const int* st = s_tok + (size_t)r * T;
     const int* sa = s_arg + (size_t)r * T;
+    const int* fc = s_fc + (size_t)r * T;
     int cur = 0, acc = 0, bon = -1;
-    for (;;) {
+    for (;;) {  // follow the child holding the target's argmax token, else stop
       const int tgt = sa[cur];
       int found = -1;
-      for (int j0 = cur + 1; j0 < n; j0 += 32) {
-        const int j = j0 + lane;
-        const bool f = j < n && sp[j] == cur && st[j] == tgt;
-        const unsigned bal = __ballot_sync(kFull, f);
-        if (bal) {
-          found = j0 + __ffs(bal) - 1;
+      for (int j = fc[cur]; j >= 0 && j < n && sp[j] == cur; ++j)
+        if (st[j] == tgt) {
+          found = j;
           break;
         }
-      }
       if (found < 0) {
         bon = tgt;
         break;
       }
-      if (lane == 0 && out.accept_path && acc < D) out.accept_path[(size_t)r * D + acc] = found;
+      if (out.accept_path && acc < D) out.accept_path[(size_t)r * D + acc] = found;
       ++acc;
       cur = found;
     }
-    if (lane == 0) {
-      if (out.accept_len) out.accept_len[r] = acc;
-      if (out.bonus) out.bonus[r] = bon;
-      atomicAdd(P.sum_accept, (unsigned long long)acc);
-    }
+    if (out.accept_len) out.accept_len[r] = acc;
+    if (out.bonus) out.bonus[r] = bon;
     if (out.accept_path)
-      for (int j = acc + lane; j < D; j += 32) out.accept_path[(size_t)r * D + j] = -1;
+      for (int j = acc; j < D; ++j) out.accept_path[(size_t)r * D + j] = -1;
+    accs += (unsigned long long)acc;
   }
+  for (int o = 16; o > 0; o >>= 1) accs += __shfl_xor_sync(kFull, accs, o);
+  if (lane == 0 && accs) atomicAdd(P.sum_accept, accs);
 }
 
 template <bool BF16>
@@ -659,7 +676,7 @@ size_t step_select_smem_bytes(const Params& P, int S, size_t sel_bytes) {
   const int rows_cap = P.cap_rows > P.b_loc ? P.cap_rows : P.b_loc;
   const int key_cap = S > rows_cap ? S : rows_cap;
   const size_t sel = a16(sel_bytes) + merge_bytes(rows_cap, key_cap, P.cpr, P.k);
-  const size_t fin = a16((size_t)(2 * P.b_loc + 2) * 4) + (size_t)4 * P.b_loc * P.T * 4;
+  const size_t fin = a16((size_t)(2 * P.b_loc + 2) * 4) + (size_t)5 * P.b_loc * P.T * 4;
   return sel > fin ? sel : fin;
 }
 

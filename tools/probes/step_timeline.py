@@ -65,3 +65,4 @@ for x in pc[::max(1, len(pc) // 40)]:
     print("  %7.2f %5.2f %5.2f  nch %d row %d sm %d cta %d" % x)
 import statistics as stt
 print("consume1 median %.2f max %.2f; rest median %.2f" % (stt.median(x[1] for x in pc), max(x[1] for x in pc), stt.median(x[2] for x in pc)))
+print("finalize: start %s trees staged %s vrow table %s | walk: slots loaded %s" % tuple(f(buf[j]) for j in (1000, 1001, 1002, 1003)))
