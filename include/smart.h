@@ -141,6 +141,10 @@ typedef struct {
                              (calls out of order / a broken launch sequence)               */
   int64_t nodes_local;    /* sum over local requests of drafted nodes                      */
   int64_t accepted_local; /* sum of accept lengths (after smart_verify_accept)              */
+  int64_t accepted_global;/* sum of accept lengths over all ranks (C2: one NCCL all-reduce at */
+  int64_t nodes_global;   /* the end of verify when a communicator is attached; else local)  */
+  int32_t step_kernel_grid; /* CTAs of the persistent whole-step kernel smart_run_step used for  */
+  int32_t reserved;         /* the last step (0: the per-layer kernels ran)                    */
   double E_global, S_final;
   smart_layer_trace layer[SMART_MAX_DEPTH];
 } smart_stats;

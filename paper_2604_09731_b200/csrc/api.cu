@@ -37,6 +37,7 @@ struct smart_ctx {
   bool fused_select = true;  // selection runs in the layer kernel's last CTA
   bool no_early = false;     // SMART_NO_EARLY=1: every layer kernel waits for the previous grid
   bool in_run_step = false;  // inside smart_run_step: the layer kernels are back to back (early start ok)
+  int last_step_grid = 0;    // grid of the step kernel for the last smart_run_step (0: per-layer path)
   // persistent whole-step kernel (step.cu) for smart_run_step: 0 = not usable for this config
   int step_grid = 0;
   size_t step_smem = 0, step_sel_bytes = 0;
@@ -84,6 +85,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool load() {
@@ -95,9 +97,10 @@ struct NcclApi {
     GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
     CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
     AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
     CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
     GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-    return GetUniqueId && CommInitRank && AllGather && CommDestroy && GetErrorString;
+    return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy && GetErrorString;
   }
 } g_nccl;
 
@@ -342,7 +345,8 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   add(&P.cand_rs, d * cap * 8);
   add(&P.trace, SMART_MAX_DEPTH * sizeof(DevTrace));
   add(&P.err, 4);
-  add(&P.sum_accept, 8);
+  add(&P.sum_accept, 16);
+  add(&P.sum_glob, 16);
   add(&P.E_glob, 8);
   add(&P.N_glob, 4);
   add(&P.vrow_off, (b + 1) * 4);
@@ -702,6 +706,20 @@ smart_status smart_build_mask(smart_ctx* c, uint32_t* d_mask, int32_t* d_pos, in
   return SMART_OK;
 }
 
+// C2: the end-of-step sums (accept lengths, drafted nodes) over all ranks for the
+// global acceptance rate beta = sum a / sum n, one NCCL all-reduce of two u64 on the
+// step's stream when a communicator is attached; otherwise the local sums are copied
+static smart_status end_of_step(smart_ctx* c, cudaStream_t s) {
+  if (c->nccl_comm && c->P.nranks > 1) {
+    ncclResult_t r = g_nccl.AllReduce(c->P.sum_accept, c->P.sum_glob, 2, ncclUint64, ncclSum,
+                                      static_cast<ncclComm_t>(c->nccl_comm), s);
+    if (r != ncclSuccess) return fail(c, SMART_ENCCL, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+  } else {
+    CUDA_TRY(c, cudaMemcpyAsync(c->P.sum_glob, c->P.sum_accept, 16, cudaMemcpyDeviceToDevice, s));
+  }
+  return SMART_OK;
+}
+
 smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld, int32_t* d_accept_len,
                                  int32_t* d_accept_path, int32_t* d_bonus, void* stream) {
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
@@ -716,7 +734,7 @@ smart_status smart_verify_accept(smart_ctx* c, const void* d_target, int64_t ld,
   launch_verify(c->P, d_target, ld_bytes, tma, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s);
   CUDA_TRY(c, cudaGetLastError());
   c->last_stream = s;
-  return SMART_OK;
+  return end_of_step(c, s);
 }
 
 smart_status smart_verify_sample(smart_ctx* c, const void* d_target, int64_t ld, double temperature, uint64_t seed,
@@ -735,7 +753,7 @@ smart_status smart_verify_sample(smart_ctx* c, const void* d_target, int64_t ld,
                 (float)(1.0 / temperature), (unsigned long long)seed);
   CUDA_TRY(c, cudaGetLastError());
   c->last_stream = s;
-  return SMART_OK;
+  return end_of_step(c, s);
 }
 
 smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32_t* d_root_pos, const void* d_draft,
@@ -761,13 +779,15 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
       launch_step(c->P, c->step_grid, c->step_smem, c->step_sel_bytes, d_draft, ldb, d_target, ldtb, d_root_tok,
                   d_root_pos, o, s);
       CUDA_TRY(c, cudaGetLastError());
+      c->last_step_grid = c->step_grid;
       c->next_layer = c->cfg.max_depth + 1;
       c->phase = 0;
       c->masked = true;
       c->last_stream = s;
-      return SMART_OK;
+      return d_target ? end_of_step(c, s) : SMART_OK;
     }
   }
+  c->last_step_grid = 0;
   smart_status st = smart_begin_step(c, d_root_tok, d_root_pos, stream);
   c->in_run_step = true;
   for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
@@ -799,12 +819,13 @@ smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {
   CUDA_TRY(c, cudaStreamSynchronize(c->last_stream));
   DevTrace tr[SMART_MAX_DEPTH];
   int err = 0;
-  unsigned long long acc = 0;
+  unsigned long long acc = 0, glob[2] = {0, 0};
   double E = 0;
   int N = 0;
   CUDA_TRY(c, cudaMemcpy(tr, c->P.trace, sizeof tr, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(&err, c->P.err, 4, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(&acc, c->P.sum_accept, 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(glob, c->P.sum_glob, 16, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(&E, c->P.E_glob, 8, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(&N, c->P.N_glob, 4, cudaMemcpyDeviceToHost));
   std::vector<int> nn(c->P.b_loc);
@@ -815,6 +836,9 @@ smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {
   long long nodes = 0;
   for (int v : nn) nodes += v - 1;
   out->nodes_local = nodes;
+  out->step_kernel_grid = c->last_step_grid;
+  out->accepted_global = (int64_t)glob[0];
+  out->nodes_global = (int64_t)glob[1];
   out->E_global = E;
   int le = 0;
   for (int l = 0; l < SMART_MAX_DEPTH; ++l) {

@@ -45,7 +45,8 @@ __global__ void begin_step_kernel(Params P, const int32_t* root_tok, const int32
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *P.fr_total[0] = P.b_loc;
     *P.err = 0;
-    *P.sum_accept = 0ull;
+    P.sum_accept[0] = 0ull;
+    P.sum_accept[1] = 0ull;
     *P.N_glob = 0;
     *P.E_glob = 0.0;
   }
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(1024) verify_walk_kernel(Params P, int32_t* ac
     if (accept_len) accept_len[r] = acc;
     if (bonus) bonus[r] = bon;
     atomicAdd(P.sum_accept, (unsigned long long)acc);
+    atomicAdd(P.sum_accept + 1, (unsigned long long)(n - 1));
   }
   if (accept_path)
     for (int j = acc + lane; j < D; j += 32) accept_path[(size_t)r * D + j] = -1;

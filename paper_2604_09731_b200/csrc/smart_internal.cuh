@@ -116,7 +116,8 @@ struct Params {
   // ---- select / stats ----
   DevTrace* trace;    // [SMART_MAX_DEPTH]
   int* err;           // [1]
-  unsigned long long* sum_accept;  // [1]
+  unsigned long long* sum_accept;  // [2]: sum of accept lengths, sum of drafted nodes (local)
+  unsigned long long* sum_glob;    // [2]: the same over all ranks (C2 all-reduce; = local on one rank)
   double* E_glob;     // [1] sum_r E_r after the last select
   int* N_glob;        // [1]
 

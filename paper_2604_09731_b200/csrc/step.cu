@@ -403,7 +403,8 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   if (tid == 0) {
     *P.fr_total[0] = bl;
     *P.err = 0;
-    *P.sum_accept = 0ull;
+    P.sum_accept[0] = 0ull;
+    P.sum_accept[1] = 0ull;
     *P.N_glob = 0;
     *P.E_glob = 0.0;
   }
@@ -598,7 +599,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   consumer_sync();
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1003] = gtime();
   const int D = P.d > 0 ? P.d : 1;
-  unsigned long long accs = 0ull;
+  unsigned long long accs = 0ull, nods = 0ull;
   for (int r = tid; r < bl; r += kConsumers) {
     const int n = s_n[r];
     const int* sp = s_par + (size_t)r * T;
@@ -627,9 +628,16 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     if (out.accept_path)
       for (int j = acc; j < D; ++j) out.accept_path[(size_t)r * D + j] = -1;
     accs += (unsigned long long)acc;
+    nods += (unsigned long long)(n - 1);
   }
-  for (int o = 16; o > 0; o >>= 1) accs += __shfl_xor_sync(kFull, accs, o);
-  if (lane == 0 && accs) atomicAdd(P.sum_accept, accs);
+  for (int o = 16; o > 0; o >>= 1) {
+    accs += __shfl_xor_sync(kFull, accs, o);
+    nods += __shfl_xor_sync(kFull, nods, o);
+  }
+  if (lane == 0 && (accs || nods)) {
+    atomicAdd(P.sum_accept, accs);
+    atomicAdd(P.sum_accept + 1, nods);
+  }
 }
 
 template <bool BF16>

@@ -69,6 +69,8 @@ class _LayerTrace(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("layers_executed", C.c_int32), ("error_flags", C.c_int32),
                 ("nodes_local", C.c_int64), ("accepted_local", C.c_int64),
+                ("accepted_global", C.c_int64), ("nodes_global", C.c_int64),
+                ("step_kernel_grid", C.c_int32), ("reserved", C.c_int32),
                 ("E_global", C.c_double), ("S_final", C.c_double),
                 ("layer", _LayerTrace * MAX_DEPTH)]
 
@@ -296,6 +298,8 @@ class Smart:
             layers.append({f: getattr(t, f) for f, _ in _LayerTrace._fields_})
         return dict(layers_executed=s.layers_executed, error_flags=s.error_flags,
                     nodes_local=s.nodes_local, accepted_local=s.accepted_local,
+                    accepted_global=s.accepted_global, nodes_global=s.nodes_global,
+                    step_kernel_grid=s.step_kernel_grid,
                     E_global=s.E_global, S_final=s.S_final, layers=layers)
 
     def tree(self) -> dict:

@@ -28,7 +28,7 @@ __global__ void merge_bench(const unsigned long long* gkeys, const float2* gms, 
       return make_float4(v.x, v.y, 0.f, 0.f);
     };
     if (VAR == 0) {
-      merge_row_tournament(k, cpr, t, 0.5f, msf, [&](int m, int j) { return kr[m * kp + j]; },
+      merge_row_tournament(k, cpr, t, 0.5f, msf, kr,
                            [&](int rank, int tok, float p, float cum) {
                              out[row * 32 + rank] = ((unsigned long long)tok << 32) | __float_as_uint(cum);
                            });
