@@ -40,28 +40,19 @@ struct __align__(16) StepShared {
   ConsShared cs;
   float2 msl[kMaxCpr * kConsumerWarps];  // (chunk, warp) softmax partials of the current slice
   // producer -> consumers: the value of event e (the row count of layer e + 2, or the verify rows)
-  // is rv[e], valid once ev > e (a monotonic counter: no phase aliasing however far ahead the
-  // producer runs)
+  // is rv[e], published by one arrive on its own mbarrier evb[e] (each completes exactly once per
+  // launch, so there is no phase aliasing however far ahead the producer runs)
   int rv[SMART_MAX_DEPTH + 2];
-  unsigned ev;
+  uint64_t evb[SMART_MAX_DEPTH + 2];
 };
 
 __device__ __forceinline__ void post_event(StepShared& sh, int e, int v) {
   sh.rv[e] = v;
-  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&sh.ev)), "r"((unsigned)(e + 1)) : "memory");
+  mbar_arrive(&sh.evb[e]);  // release (CTA scope)
 }
 __device__ __forceinline__ int wait_event(StepShared& sh, int e) {
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    for (;;) {
-      unsigned v;
-      asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&sh.ev)) : "memory");
-      if (v > (unsigned)e) break;
-      __nanosleep(32);
-    }
-  }
-  __syncwarp();
-  return *reinterpret_cast<volatile int*>(&sh.rv[e]);
+  mbar_wait(&sh.evb[e], 0u);  // acquire (CTA scope)
+  return sh.rv[e];
 }
 
 // row stride of the per-chunk partials (even: a layer's partials are whole 16-byte units)
@@ -497,6 +488,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
       for (int row = tid; row < R; row += kConsumers)
         P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(M.fe[row].x, M.slot[row]);
     }
+    consumer_sync();  // the scratch is reused by the next layer's selection / the final phase
     if (tid == 0) pb_max(P, layer, kPbSelDone);
     if (SMART_PROBES && P.dbg && tid == 0)  // the selection's clock64 phase stamps of this layer
       for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
@@ -654,7 +646,7 @@ step_kernel(Params P, size_t sel_bytes, const char* __restrict__ draft, long lon
       mbar_init(&pipe.full[s], 1);
       mbar_init(&pipe.empty[s], kConsumerWarps);
     }
-    sh.ev = 0u;
+    for (int e = 0; e < SMART_MAX_DEPTH + 2; ++e) mbar_init(&sh.evb[e], 1);
     mbar_fence_init();
     sh.cs.tau = 0ull;
   }

@@ -21,7 +21,7 @@ def short(name):
     m = re.search(r"([A-Za-z_][A-Za-z0-9_]*)(<[^()]*>)?\(", name)
     base = m.group(1) if m else name[:40]
     if "unnamed" in name or base in ("layer_kernel", "verify_kernel", "mask_kernel", "begin_step_kernel",
-                                     "select_kernel", "export_frontier_kernel"):
+                                     "select_kernel", "export_frontier_kernel", "step_kernel"):
         return base
     return "torch:" + base if "at::" in name else base
 
@@ -113,8 +113,12 @@ def full(path, out, traffic_json=None, workload="cfg3_llama8b_b32"):
                     to_bytes(row[ix["dram__bytes_write.sum"]], u[ix["dram__bytes_write.sum"]])
                 fam.setdefault(name, []).append(tb)
     if traffic_json:
-        alias = {"layer_kernel": "expand", "verify_kernel": "verify"}
-        js = {workload: {alias.get(k, k): sum(v) / len(v) for k, v in fam.items()}}
+        alias = {"layer_kernel": "expand", "verify_kernel": "verify", "step_kernel": "step"}
+        try:
+            js = json.load(open(traffic_json))
+        except Exception:
+            js = {}
+        js[workload] = {alias.get(k, k): sum(v) / len(v) for k, v in fam.items()}
         js[workload]["capture"] = path.split("/")[-1]
         with open(traffic_json, "w") as f:
             json.dump(js, f, indent=1)
