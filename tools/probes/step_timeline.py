@@ -18,7 +18,7 @@ cfg = S.Config(vocab=wl["V"], top_k=wl["k"], max_depth=wl["d"], max_frontier=wl[
 ctx = S.Smart(cfg, S.Cost(lam=fx["lam"], beta=fx["beta"], gamma=fx["gamma"], delta=fx["delta"], rho=fx["rho"],
                           eta=fx["eta"], c_T=fx["c_T"]))
 T = ctx.sizes["T"]
-d, tg, rt, rp = bench.make_set(0, wl, T, 0)
+d, tg, rt, rp = bench.make_set(0, wl, T, wl["b"], 0)
 dev = torch.device("cuda")
 dd, tt = bench.bf16_dev(d, dev), bench.bf16_dev(tg, dev)
 out = ctx.alloc_outputs()
