@@ -306,6 +306,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
   } else {
     // ---- consumer warps (expand_core.cuh) ----
     int wcnt = 0;  // entries in the warp's buffer (warp-uniform)
+    float wrun = -INFINITY;  // the warp's running max over the current slice
     int i = 0;
     for (int n = 0; n < nrows; ++n) {
       const int row = team + n * nteams;
@@ -330,7 +331,7 @@ layer_kernel(Params P, int layer, const char* __restrict__ logits, long long ld_
           load_direct<BF16>(rowp(n, row), c * CE, V, tid, raw);
         }
         consume_chunk<BF16, TMA>(P, sh.cs, tb.msl, raw, stage, TMA ? nullptr : rowp(n, row), c, mlo, mhi, i, wcnt,
-                                 bound);
+                                 bound, wrun);
         __syncwarp();
         if (TMA && lane == 0) mbar_arrive(&pipe.empty[s]);  // release the stage
         gstamp(P, t0 && i < 2, 20 + 3 * i);

@@ -23,6 +23,16 @@ namespace smart {
 #ifndef CONSUME_STAMPS
 #define CONSUME_STAMPS 0  // tools/ubench/consume.cu only: clock64 stamps of CTA 0, warp 0
 #endif
+#ifndef CONSUME_COUNTS
+#define CONSUME_COUNTS 0  // tools/ubench/consume.cu only: slow-path counters
+#endif
+#if CONSUME_COUNTS
+__device__ unsigned long long g_ccount[8];
+#define CCOUNT(i, v) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_ccount[i], (unsigned long long)(v))
+#else
+#define CCOUNT(i, v)
+#endif
 #if CONSUME_STAMPS
 __device__ unsigned long long g_cstamp[64];
 #define CSTAMP(i) \
@@ -100,6 +110,7 @@ struct __align__(16) ConsShared {
   unsigned long long tau;                                       // slice-wide bound hint (max over warps)
   __align__(16) unsigned pub[2][kConsumerWarps * kMaxK];        // slice start: top-j lane maxima per warp
   __align__(16) unsigned long long cl[kConsumerWarps * kMaxK];  // slice end: each warp's top-k
+  __align__(16) float wmax[kConsumerWarps];                     // each warp's running max over the slice
   WarpTopk w[kConsumerWarps];
 };
 
@@ -128,7 +139,7 @@ __device__ __forceinline__ void warp_compact(WarpTopk& w, int n, int k, int lane
 template <bool BF16, bool TMA>
 __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, float2* msl, const uint4 (&raw)[kVecPerThread],
                                               const char* stage, const char* rowp, int c, int mlo, int mhi, int i,
-                                              int& wcnt, unsigned long long& bound) {
+                                              int& wcnt, unsigned long long& bound, float& wrun) {
   constexpr int EPT = Traits<BF16>::EPT;
   constexpr int EPV = Traits<BF16>::EPV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -190,6 +201,8 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   if (c == mlo) {
     const int jr = max((k + kConsumerWarps - 1) / kConsumerWarps, 2);
     unsigned* pub = sh.pub[i & 1];
+    wrun = Mw;
+    if (lane == 0) sh.wmax[warp] = -INFINITY;  // this slice's values are posted after the barrier below
     unsigned rem = (m == m) ? float_orderable(m) : 0u;
     for (int r = 0; r < jr; ++r) {
       const unsigned cur = __reduce_max_sync(kFull, rem);
@@ -216,6 +229,35 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
       const unsigned long long b0 = ((unsigned long long)vk << 32) | 0x80000000ull;  // (v_k, INT_MAX)
       if (b0 > bound) bound = b0;
     }
+    if (lane == 0) *reinterpret_cast<volatile float*>(&sh.wmax[warp]) = wrun;
+  } else if (k <= kConsumerWarps) {
+    // later chunks: every warp's running max over the slice is an element of the row (distinct
+    // elements for distinct warps), so the k-th largest of the 8 posted maxima bounds the slice's
+    // k-th best value from below; stale or unposted entries are smaller (still valid) or -inf
+    wrun = fmaxf(wrun, Mw);
+    if (lane == 0) *reinterpret_cast<volatile float*>(&sh.wmax[warp]) = wrun;
+    float wv[kConsumerWarps];
+    asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(wv[0]), "=f"(wv[1]), "=f"(wv[2]), "=f"(wv[3]) : "r"(smem_u32(&sh.wmax[0])));
+    asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(wv[4]), "=f"(wv[5]), "=f"(wv[6]), "=f"(wv[7]) : "r"(smem_u32(&sh.wmax[4])));
+    float vkth;
+    if (k == kConsumerWarps) {
+      vkth = fminf(fminf(fminf(wv[0], wv[1]), fminf(wv[2], wv[3])), fminf(fminf(wv[4], wv[5]), fminf(wv[6], wv[7])));
+    } else {
+      vkth = INFINITY;  // the smallest value with fewer than k larger entries
+#pragma unroll
+      for (int x = 0; x < kConsumerWarps; ++x) {
+        int gt = 0;
+#pragma unroll
+        for (int y = 0; y < kConsumerWarps; ++y) gt += (wv[y] > wv[x]) || (wv[y] == wv[x] && y < x);
+        if (gt < k) vkth = fminf(vkth, wv[x]);
+      }
+    }
+    if (vkth > -INFINITY && vkth == vkth) {
+      const unsigned long long b0 = ((unsigned long long)float_orderable(vkth) << 32) | 0x80000000ull;
+      if (b0 > bound) bound = b0;
+    }
   }
   {
     // barrier-free CTA bound: every warp posts its k-th best after each compaction (a lower
@@ -225,7 +267,9 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   }
   float bv = bound ? tk_val(bound) : -INFINITY;
   CSTAMP(5 + 8 * (c - mlo));
+  CCOUNT(0, 1);
   if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
+    CCOUNT(1, 1);
     // vectors whose max reaches the bound are expanded cooperatively: each group of EPV lanes
     // takes one such vector (its elements re-read from the still-held ring stage), compares them
     // with the bound and appends the survivors at ballot-prefix positions
@@ -235,6 +279,7 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
       unsigned bal = __ballot_sync(kFull, vm[j] >= bv);
       while (bal) {
         if (wcnt > kSegBuf - 32) {  // keep room for a full pass: compact, tighten, re-filter
+          CCOUNT(3, 1);
           __syncwarp();
           warp_compact(W, wcnt, k, lane);
           wcnt = k;
@@ -267,11 +312,14 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
         const unsigned qb = __ballot_sync(kFull, q);
         if (q) W.buf[wcnt + __popc(qb & ((1u << lane) - 1u))] = tk_key(v, idx);
         wcnt += __popc(qb);
+        CCOUNT(2, __popc(qb));
+        CCOUNT(5, 1);
       }
     }
   }
   CSTAMP(6 + 8 * (c - mlo));
   if (wcnt >= 2 * k && c + 1 < mhi) {  // keep the warp's buffer short
+    CCOUNT(4, 1);
     __syncwarp();
     warp_compact(W, wcnt, k, lane);
     wcnt = k;

@@ -229,6 +229,7 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
 
   // ---- consumer warps ----
   int i = 0, ev = 0, wcnt = 0;
+  float wrun = -INFINITY;  // the warp's running max over the current slice
   while (R > 0 && layer <= P.d) {
     const int t = team_size(R, S, cpr);
     const int nteams = S / t, team = s / t, member = s - team * t;
@@ -249,7 +250,7 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
           const uint4* sv = reinterpret_cast<const uint4*>(stage);
 #pragma unroll
           for (int j = 0; j < kVecPerThread; ++j) raw[j] = sv[j * kConsumers + tid];
-          consume_chunk<BF16, true>(P, sh.cs, sh.msl, raw, stage, nullptr, c, mlo, mhi, i, wcnt, bound);
+          consume_chunk<BF16, true>(P, sh.cs, sh.msl, raw, stage, nullptr, c, mlo, mhi, i, wcnt, bound, wrun);
           __syncwarp();
           if (tid == 0 && c == mlo) pb_max(P, layer, kPbConsumed1);
           if (SMART_PROBES && P.dbg && layer == 2 && tid == 0 && c == mlo) P.dbg[1024 + 4 * s + 1] = gtime();

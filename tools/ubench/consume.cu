@@ -76,6 +76,7 @@ consume_bench(Params P, const char* __restrict__ logits, long long row_bytes, in
   }
   unsigned long long tfirst = 0;
   int i = 0, wcnt = 0;
+  float wrun = -INFINITY;
   for (int n = 0; n < nrows; ++n) {
     unsigned long long bound = 0ull;
     for (int c = c0; c < c1; ++c, ++i) {
@@ -87,7 +88,7 @@ consume_bench(Params P, const char* __restrict__ logits, long long row_bytes, in
       const uint4* sv = reinterpret_cast<const uint4*>(stage);
 #pragma unroll
       for (int j = 0; j < kVecPerThread; ++j) raw[j] = sv[j * kConsumers + tid];
-      consume_chunk<true, true>(P, sh.cs, sh.msl, raw, stage, nullptr, c, c0, c1, i, wcnt, bound);
+      consume_chunk<true, true>(P, sh.cs, sh.msl, raw, stage, nullptr, c, c0, c1, i, wcnt, bound, wrun);
       __syncwarp();
       if (lane == 0) mbar_arrive(&pipe.empty[st]);
     }
@@ -156,6 +157,14 @@ int main(int argc, char** argv) {
   }
   std::sort(ms.begin(), ms.end());
   const double bytes = (double)nrows_pool * row_bytes;
+#if CONSUME_COUNTS
+  {
+    unsigned long long cnt[8];
+    cudaMemcpyFromSymbol(cnt, g_ccount, sizeof cnt);
+    printf("counts over 15 launches: warp-chunks %llu, with candidates %llu, candidates %llu, expansion passes %llu, "
+           "mid-chunk compactions %llu, end-of-chunk compactions %llu\n", cnt[0], cnt[1], cnt[2], cnt[5], cnt[3], cnt[4]);
+  }
+#endif
   printf("V %d k %d: throughput mode, %d CTAs x %d rows: %.1f MB in %.2f us (median) = %.0f GB/s  [err %s]\n", V, k, G,
          rows_per_cta, bytes / 1e6, ms[ms.size() / 2] * 1e3, bytes / (ms[ms.size() / 2] * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
