@@ -464,7 +464,9 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
       const long long S = c->step_grid - 1;
       const long long lists = std::max<long long>(S, std::max<long long>(cap, b));
       const size_t kb = (size_t)lists * ((k + 1) & ~1ll) * 8, mb = (size_t)std::max<long long>(cap, b) * ((P.cpr + 1) & ~1) * 8;
-      e = cudaMalloc(&c->step_ws, ((kb + 255) & ~size_t(255)) + ((mb + 255) & ~size_t(255)) + sizeof(StepCtl));
+      const size_t tb = (size_t)std::max<long long>(cap, b) * 8;
+      e = cudaMalloc(&c->step_ws, ((kb + 255) & ~size_t(255)) + ((mb + 255) & ~size_t(255)) + ((tb + 255) & ~size_t(255)) +
+                                      sizeof(StepCtl));
       if (e != cudaSuccess) {
         release_ctx(c);
         return fail(nullptr, SMART_ECUDA, "step workspace: %s", cudaGetErrorString(e));
@@ -474,6 +476,9 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
       sb += (kb + 255) & ~size_t(255);
       P.seg_ms = reinterpret_cast<float2*>(sb);
       sb += (mb + 255) & ~size_t(255);
+      P.fr_tag = reinterpret_cast<unsigned long long*>(sb);
+      cudaMemset(P.fr_tag, 0, tb);
+      sb += (tb + 255) & ~size_t(255);
       P.ctl = reinterpret_cast<StepCtl*>(sb);
       cudaMemset(P.ctl, 0, sizeof(StepCtl));
     } else {

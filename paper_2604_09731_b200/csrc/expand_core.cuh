@@ -215,14 +215,25 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
     CSTAMP(4 + 8 * (c - mlo));
     const int np = kConsumerWarps * jr;  // multiple of 8
     unsigned vc = 0xffffffffu;
-    for (int e = lane; e < np; e += 32) {
-      const unsigned u = pub[e];
+    if (np == 16) {  // k <= 16: all 16 values in registers (four broadcast 16-byte loads issued together)
+      uint4 v4[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) v4[o] = *reinterpret_cast<const uint4*>(pub + 4 * o);
+      const unsigned u = lane < 16 ? pub[lane] : 0u;
       int gt = 0;
-      for (int o = 0; o < np; o += 4) {
-        const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
-        gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+#pragma unroll
+      for (int o = 0; o < 4; ++o) gt += (v4[o].x > u) + (v4[o].y > u) + (v4[o].z > u) + (v4[o].w > u);
+      if (lane < 16 && gt < k) vc = u;
+    } else {
+      for (int e = lane; e < np; e += 32) {
+        const unsigned u = pub[e];
+        int gt = 0;
+        for (int o = 0; o < np; o += 4) {
+          const uint4 v4 = *reinterpret_cast<const uint4*>(pub + o);  // broadcast reads
+          gt += (v4.x > u) + (v4.y > u) + (v4.z > u) + (v4.w > u);
+        }
+        if (gt < k && u < vc) vc = u;
       }
-      if (gt < k && u < vc) vc = u;
     }
     const unsigned vk = __reduce_min_sync(kFull, vc);
     if (vk != 0u && vk != 0xffffffffu) {  // 0: NaN maxima among the top k (row flagged; no bound)

@@ -358,10 +358,12 @@ struct NoWait {
   __device__ bool operator()(SelLayout&, int4*) const { return false; }
 };
 // pub(R_next): one thread publishes the next frontier (written and fenced by the caller's barrier
-// or __syncwarp); the per-layer kernels release P.fr_ready[layer]
+// or __syncwarp); the per-layer kernels release P.fr_ready[layer].  pub.entry(pos, r, node) is
+// called for every frontier entry as it is written (the step kernel also writes a tagged copy).
 struct PubReady {
   int* flag;
   __device__ void operator()(int) const { publish_flag(flag); }
+  __device__ void entry(int, int, int) const {}
 };
 
 __device__ __forceinline__ Cand load_cand(const Cand* p) {  // L2 (written by other CTAs)
@@ -866,6 +868,8 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         const int q = L.off[r] * k + c;
         const int idx = bits_below(r, c);
         P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+      pub.entry(L.base[r] + idx, r, L.nd[r] + 1 + idx);
+        pub.entry(L.base[r] + idx, r, L.nd[r] + 1 + idx);
         P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
       }
       if (lane < bl) P.fr_off[npar][lane] = incl - nx;
@@ -897,6 +901,7 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
       if (!((L.bm[r * nbw + (c >> 5)] >> (c & 31)) & 1u) || L.nxt[r] == 0) continue;
       const int idx = bits_below(r, c);
       P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
+      pub.entry(L.base[r] + idx, r, L.nd[r] + 1 + idx);
       P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
     }
     blk_sync<NT>();  // B8: the next frontier is complete

@@ -100,6 +100,9 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 // Polls are bounded (~2^24 tries, seconds): a broken protocol sets the sticky kErrTimeout
 // flag (SMART_EDEVICE from smart_get_stats) and lets the step run out instead of hanging the GPU.
 constexpr unsigned kPollLimit = 1u << 24;
@@ -119,6 +122,49 @@ __device__ __forceinline__ int wait_tag(const unsigned long long* f, unsigned ta
     __nanosleep(20);
   }
 }
+// the same without the acquire fence: for flags after which only self-validating words are read
+__device__ __forceinline__ int wait_tag_relaxed(const unsigned long long* f, unsigned tag, int* err) {
+  for (unsigned it = 0;; ++it) {
+    const unsigned long long v = ld_relaxed_u64(f);
+    if ((unsigned)(v >> 32) == tag) return (int)(unsigned)v;
+    if (it > kPollLimit) {
+      atomicOr(err, kErrTimeout);
+      return 0;
+    }
+    __nanosleep(20);
+  }
+}
+// a frontier entry's tag: unique per (launch, layer)
+__device__ __forceinline__ unsigned entry_tag(unsigned tag, int layer) { return (tag << 5) | (unsigned)layer; }
+// poll a tagged frontier entry; returns (r << 10 | node)
+__device__ __forceinline__ unsigned wait_entry(const unsigned long long* e, unsigned etag, int* err) {
+  for (unsigned it = 0;; ++it) {
+    const unsigned long long v = ld_relaxed_u64(e);
+    if ((unsigned)(v >> 32) == etag) return (unsigned)v;
+    if (it > kPollLimit) {
+      atomicOr(err, kErrTimeout);
+      return 0u;
+    }
+  }
+}
+
+// the step kernel's frontier publication: every entry also as a self-validating tagged word, the
+// row count as a tagged flag, all with plain stores (no release fence on the critical path: what
+// the streaming CTAs read behind the flag is the tagged entries themselves)
+struct StepPub {
+  const Params* P;
+  unsigned tag;
+  int layer;
+  __device__ void entry(int pos, int r, int node) const {
+    if (layer < P->d)
+      st_relaxed_u64(&P->fr_tag[pos],
+                     ((unsigned long long)entry_tag(tag, layer + 1) << 32) | ((unsigned)r << 10) | (unsigned)node);
+  }
+  __device__ void operator()(int tot) const {
+    if (layer < P->d) st_relaxed_u64(&P->ctl->flag[layer + 1], ((unsigned long long)tag << 32) | (unsigned)tot);
+  }
+};
+
 // poll an arrival counter until it reaches `want`
 __device__ __forceinline__ void wait_count(const int* c, int want, int* err) {
   for (unsigned it = 0; ld_relaxed_s32(c) < want; ++it) {
@@ -185,17 +231,17 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
       if (team < nteams) {
         for (int row = team; row < R; row += nteams) {
           int r = row, node = 0;  // layer 1: the roots
-          if (layer > 1) {
-            const int2 fe = __ldcg(&P.fr[par][row]);
-            r = fe.x;
-            node = fe.y;
+          if (layer > 1) {  // the row's self-validating frontier entry
+            const unsigned w = wait_entry(&P.fr_tag[row], entry_tag(tag, layer), P.err);
+            r = (int)(w >> 10);
+            node = (int)(w & 1023u);
           }
           const char* base = P.row_mode == SMART_ROWS_POSITION ? draft + ((long long)r * P.d + (layer - 1)) * ld_d
                                                                 : draft + ((long long)r * T + node) * ld_d;
           for (int c = mlo; c < mhi; ++c) issue(base, c);
         }
       }
-      const int Rn = layer < P.d ? wait_tag(&P.ctl->flag[layer + 1], tag, P.err) : 0;
+      const int Rn = layer < P.d ? wait_tag_relaxed(&P.ctl->flag[layer + 1], tag, P.err) : 0;
       if (layer < P.d) {
         pb_min(P, layer + 1, kPbFlagMin);
         pb_max(P, layer + 1, kPbFlagMax);
@@ -469,11 +515,8 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
       if (tid == 0) pb_max(P, layer, kPbMerged);
       return true;
     };
-    auto pub = [&](int tot) {
-      if (layer < P.d) st_release_u64(&P.ctl->flag[layer + 1], ((unsigned long long)tag << 32) | (unsigned)tot);
-      pb_max(P, layer, kPbPublished);
-    };
-    select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, pub);
+    select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, StepPub{&P, tag, layer});
+    if (tid == 0) pb_max(P, layer, kPbPublished);
     consumer_sync();
     // inspection copies (smart_get_candidates) after the frontier is out: the candidate records
     // and each row's (request, slot), from the selection's staged records
