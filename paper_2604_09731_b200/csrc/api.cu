@@ -464,7 +464,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
       const long long S = c->step_grid - 1;
       const long long lists = std::max<long long>(S, std::max<long long>(cap, b));
       const size_t kb = (size_t)lists * ((k + 1) & ~1ll) * 8, mb = (size_t)std::max<long long>(cap, b) * ((P.cpr + 1) & ~1) * 8;
-      const size_t tb = (size_t)std::max<long long>(cap, b) * 8;
+      const size_t tb = (size_t)std::max<long long>(cap, b * T) * 8;  // frontier entries, then the verify rows
       e = cudaMalloc(&c->step_ws, ((kb + 255) & ~size_t(255)) + ((mb + 255) & ~size_t(255)) + ((tb + 255) & ~size_t(255)) +
                                       sizeof(StepCtl));
       if (e != cudaSuccess) {

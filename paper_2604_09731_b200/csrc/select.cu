@@ -19,7 +19,14 @@ __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int
     if (threadIdx.x == 0) *P.fr_total[layer & 1] = 0;
     return;
   }
+  tl_start(P, 40 + layer);
   select_layer<kSelectThreads>(P, layer, mode, smem, NoWait{}, PubReady{&P.fr_ready[layer]});
+  tl_end(P, 40 + layer);
+  if (SMART_PROBES && P.dbg) {  // this layer's clock64 phase stamps (select_layer's stamp() slots)
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
+  }
 }
 
 __global__ void export_frontier_kernel(Params P, int parity, int32_t* out, int32_t* count) {

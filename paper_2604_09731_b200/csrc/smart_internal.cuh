@@ -130,8 +130,8 @@ struct Params {
   unsigned long long* seg_keys;  // slice top-k lists of the current layer, dense [row * t + member][kp]
   float2* seg_ms;                // per-chunk softmax partials (M_c, S_c) of the current layer [row][cpr]
   StepCtl* ctl;
-  unsigned long long* fr_tag;    // [max(cap_rows, b_loc)] self-validating frontier entries:
-                                 // ((tag << 5 | layer) << 32) | r << 10 | node
+  unsigned long long* fr_tag;    // [max(cap_rows, b_loc * T)] self-validating frontier entries
+                                 // ((tag << 5 | layer) << 32) | r << 10 | node; then the verify rows (layer 31)
   int step_S;                    // streaming CTAs (the grid's last CTA runs the selection)
 
   // ---- multi-rank exchange (select phase 0 -> NCCL all-gather -> select phase 1) ----

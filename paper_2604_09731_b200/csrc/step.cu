@@ -250,7 +250,7 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
       R = Rn;
       ++layer;
     }
-    const int NR = wait_tag(&P.ctl->flag[kVerifySlot], tag, P.err);
+    const int NR = wait_tag_relaxed(&P.ctl->flag[kVerifySlot], tag, P.err);
     pb_min(P, kVerifySlot, kPbFlagMin);
     pb_max(P, kVerifySlot, kPbFlagMax);
     post_event(sh, ev++, NR);
@@ -259,9 +259,9 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
       int row = rr.lo / cpr, c = rr.lo - row * cpr;
       const char* base = nullptr;
       for (int q = rr.lo; q < rr.hi; ++q) {
-        if (q == rr.lo || c == 0) {
-          const int2 e = __ldcg(&P.vrow_rn[row]);
-          base = target + ((long long)e.x * T + e.y) * ld_t;
+        if (q == rr.lo || c == 0) {  // the row's self-validating verify entry
+          const unsigned w = wait_entry(&P.fr_tag[row], entry_tag(tag, 31), P.err);
+          base = target + ((long long)(w >> 10) * T + (w & 1023u)) * ld_t;
         }
         issue(base, c);
         if (++c == cpr) {
@@ -334,7 +334,8 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
   int q = rr.lo, row = rr.lo / cpr, c0 = rr.lo - row * cpr;
   while (q < rr.hi) {
     const int nch = min(cpr - c0, rr.hi - q);
-    const int2 rn = __ldcg(&P.vrow_rn[row]);
+    const unsigned rw = wait_entry(&P.fr_tag[row], entry_tag(tag, 31), P.err);
+    const int2 rn = make_int2((int)(rw >> 10), (int)(rw & 1023u));
     float bv = -INFINITY;
     int bi = kIdxSentinel;
     for (int c = c0; c < c0 + nch; ++c, ++i) {
@@ -539,41 +540,45 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   }
 
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1000] = gtime();
-  // ---- the final trees, staged in shared memory with one round of loads (this CTA's writes) ----
+  // ---- verify rows first: (request, node) of every tree row, request-major (A8 reads all of
+  // them), as self-validating tagged words (entry tag of layer 31) and the row count as a tagged
+  // flag, plain stores: nothing else is needed before the target rows can stream ----
   int* s_n = reinterpret_cast<int*>(dsm);                // [bl + 1] node counts, [bl + 1] scan scratch
   int* s_par = s_n + a16((size_t)(2 * bl + 2) * 4) / 4;  // [bl * T] parent, depth, token, target argmax
   int* s_dep = s_par + (size_t)bl * T;
   int* s_tok = s_dep + (size_t)bl * T;
   int* s_arg = s_tok + (size_t)bl * T;
-  for (int r = tid; r < bl; r += kConsumers) s_n[r] = P.n_nodes[r];
+  int* s_off = s_n + bl + 1;  // exclusive scan of the node counts
+  for (int r = tid; r < bl; r += kConsumers) s_off[r] = s_n[r] = P.n_nodes[r];
+  consumer_sync();
+  if (warp == 0) {
+    const int tot = warp_excl_scan_smem(s_off, bl, lane);
+    if (lane == 0) s_off[bl] = tot;
+  }
+  consumer_sync();
+  const int NR = s_off[bl];
+  const unsigned vtag = entry_tag(tag, 31);
+  for (int e = tid; e < bl * T; e += kConsumers) {
+    const int r = e / T, j = e - r * T;
+    if (j < s_n[r]) {
+      P.vrow_rn[s_off[r] + j] = make_int2(r, j);
+      st_relaxed_u64(&P.fr_tag[s_off[r] + j], ((unsigned long long)vtag << 32) | ((unsigned)r << 10) | (unsigned)j);
+    }
+  }
+  for (int r = tid; r <= bl; r += kConsumers) P.vrow_off[r] = s_off[r];
+  if (tid == 0) {
+    st_relaxed_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
+    pb_max(P, kVerifySlot, kPbPublished);
+  }
+  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1001] = gtime();
+  // ---- the final trees, staged in shared memory with one round of loads (this CTA's writes) ----
   for (int e = tid; e < bl * T; e += kConsumers) {
     s_par[e] = P.parent[e];
     s_dep[e] = P.depth[e];
     s_tok[e] = P.tok[e];
   }
   consumer_sync();
-  if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1001] = gtime();
-  // verify rows: (request, node) of every tree row, request-major (A8 reads all of them)
-  int* s_off = s_n + bl + 1;  // exclusive scan of the node counts
-  if (warp == 0) {
-    for (int r = lane; r < bl; r += 32) s_off[r] = s_n[r];
-    __syncwarp();
-    const int tot = warp_excl_scan_smem(s_off, bl, lane);
-    if (lane == 0) s_off[bl] = tot;
-  }
-  consumer_sync();
-  const int NR = s_off[bl];
-  for (int e = tid; e < bl * T; e += kConsumers) {
-    const int r = e / T, j = e - r * T;
-    if (j < s_n[r]) P.vrow_rn[s_off[r] + j] = make_int2(r, j);
-  }
-  for (int r = tid; r <= bl; r += kConsumers) P.vrow_off[r] = s_off[r];
-  consumer_sync();  // the table is written (cumulative release below)
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1002] = gtime();
-  if (tid == 0) {
-    st_release_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
-    pb_max(P, kVerifySlot, kPbPublished);
-  }
   // ---- A7 while the target rows stream: ancestor-or-self bit rows, positions, parents, tokens ----
   const int MW = P.MW;
   for (int e = tid; e < bl * T; e += kConsumers) {
