@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1) select_kernel(Params P, int
   if (SMART_PROBES && P.dbg) {  // this layer's clock64 phase stamps (select_layer's stamp() slots)
     __syncthreads();
     if (threadIdx.x == 0)
-      for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
+      for (int j = 9; j <= 22; ++j) P.dbg[3000 + layer * 16 + (j - 9)] = P.dbg[32 + j];
   }
 }
 

@@ -536,7 +536,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     consumer_sync();  // the scratch is reused by the next layer's selection / the final phase
     if (tid == 0) pb_max(P, layer, kPbSelDone);
     if (SMART_PROBES && P.dbg && tid == 0)  // the selection's clock64 phase stamps of this layer
-      for (int j = 9; j <= 22; ++j) P.dbg[700 + layer * 16 + (j - 9)] = P.dbg[32 + j];
+      for (int j = 9; j <= 22; ++j) P.dbg[3000 + layer * 16 + (j - 9)] = P.dbg[32 + j];
   }
 
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1000] = gtime();

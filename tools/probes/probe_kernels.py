@@ -63,7 +63,7 @@ for kid, nm in rows:
 names = {9: "start", 10: "benefits", 11: "req-rank", 12: "sort", 13: "A5 cut", 15: "bitmaps", 16: "B6",
          17: "counts", 18: "frontier", 19: "published", 14: "adm flags", 22: "end"}
 for l in range(1, wl["d"] + 1):
-    c = {j: int(buf[700 + l * 16 + (j - 9)]) for j in range(9, 23)}
+    c = {j: int(buf[3000 + l * 16 + (j - 9)]) for j in range(9, 23)}
     base = c[9]
     if base:
         print(f"select{l} phases (cycles):", ", ".join(f"{names[j]} {c[j]-base}" for j in (10, 11, 12, 13, 15, 16, 17, 18, 19, 14, 22) if c[j]))
