@@ -463,22 +463,27 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
     if (c->step_grid >= 2) {
       const long long S = c->step_grid - 1;
       const long long lists = std::max<long long>(S, std::max<long long>(cap, b));
-      const size_t kb = (size_t)lists * ((k + 1) & ~1ll) * 8, mb = (size_t)std::max<long long>(cap, b) * ((P.cpr + 1) & ~1) * 8;
+      const long long rows = std::max<long long>(cap, b);
+      const size_t kb = (size_t)lists * k * 16, mb = (size_t)rows * P.cpr * 16, cb = (size_t)rows * k * 16;
       const size_t tb = (size_t)std::max<long long>(cap, b * T) * 8;  // frontier entries, then the verify rows
-      e = cudaMalloc(&c->step_ws, ((kb + 255) & ~size_t(255)) + ((mb + 255) & ~size_t(255)) + ((tb + 255) & ~size_t(255)) +
-                                      sizeof(StepCtl));
+      auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+      const size_t lines = up(kb) + up(mb) + up(cb);
+      e = cudaMalloc(&c->step_ws, lines + up(tb) + sizeof(StepCtl));
       if (e != cudaSuccess) {
         release_ctx(c);
         return fail(nullptr, SMART_ECUDA, "step workspace: %s", cudaGetErrorString(e));
       }
       char* sb = static_cast<char*>(c->step_ws);
-      P.seg_keys = reinterpret_cast<unsigned long long*>(sb);
-      sb += (kb + 255) & ~size_t(255);
-      P.seg_ms = reinterpret_cast<float2*>(sb);
-      sb += (mb + 255) & ~size_t(255);
+      cudaMemset(sb, 0, lines);  // tag 0: never a launch's tag
+      P.seg_key = reinterpret_cast<uint4*>(sb);
+      sb += up(kb);
+      P.seg_ms = reinterpret_cast<uint4*>(sb);
+      sb += up(mb);
+      P.seg_cand = reinterpret_cast<uint4*>(sb);
+      sb += up(cb);
       P.fr_tag = reinterpret_cast<unsigned long long*>(sb);
       cudaMemset(P.fr_tag, 0, tb);
-      sb += (tb + 255) & ~size_t(255);
+      sb += up(tb);
       P.ctl = reinterpret_cast<StepCtl*>(sb);
       cudaMemset(P.ctl, 0, sizeof(StepCtl));
     } else {

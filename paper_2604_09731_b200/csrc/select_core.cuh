@@ -366,6 +366,253 @@ struct PubReady {
   __device__ void entry(int, int, int) const {}
 };
 
+// bits [lo, hi) of 32-bit word w of a candidate bitmap, for the candidate range [lo, hi)
+__device__ __forceinline__ unsigned word_range(int lo, int hi, int w) {
+  const int a = min(max(lo - 32 * w, 0), 32), b = min(max(hi - 32 * w, 0), 32);
+  const unsigned hm = b >= 32 ? ~0u : ((1u << b) - 1u);
+  const unsigned lm = a >= 32 ? ~0u : ((1u << a) - 1u);
+  return hm & ~lm;
+}
+
+// ---------------------------------------------------------------------------------------------
+// select_tiny: A3-A6 of a small layer (<= kTinyCand candidates, <= 32 requests; NODE_SUM with
+// PREFIX or FROZEN, one rank) by one warp, two candidates per lane (q = lane, lane + 32), without
+// block barriers.  Same decisions and the same floating-point association as select_layer's
+// block path: within-request rank by (b desc, c asc) and eligibility rank < e_r (A3), the rank of
+// each eligible key among the eligible keys (A4), the tile up-scan fp64 prefix and the first
+// failing entry (A5, Eq.(16)), admitted counts / offsets / node indices by ballots over the
+// request's candidate range, E_r += admitted cum in canonical order, the same xor-tree totals and
+// the same argmax_j reduction.  Called after select_layer's B2 (state, e_r bases, benefits staged).
+// ---------------------------------------------------------------------------------------------
+constexpr int kTinyCand = 64;
+template <class GetCand, class Pub>
+__device__ __forceinline__ void select_tiny(const Params& P, int layer, const SelLayout& L, int R, int ne, long long N0,
+                                            double E0, GetCand get_cand, Pub pub) {
+  const int lane = threadIdx.x & 31;
+  const int k = P.k, bl = P.b_loc, nct = R * k, npar = layer & 1;
+  const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+  DevTrace& tr = P.trace[layer - 1];
+  const int bc = (P.cost_scope == SMART_COST_LOCAL) ? bl : P.b_glob;
+  auto sp = [&](double E, int j) {
+    const double C = L.ctab[j];
+    return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
+  };
+  const double ac = P.alpha * P.c_T;
+  const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
+  const double dc0 = L.dtab[0];
+  auto rule_ok = [&](double bj, double before, int j) {  // Eq.(16), as select_layer
+    if (P.selection == SMART_FROZEN)
+      return (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > rhs0 * dc0) : (bj > 0.0);
+    const double C = L.ctab[j];
+    return (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[j]) : (bj > 0.0);
+  };
+  const int nw = nct > 32 ? 2 : 1;  // candidate words in use (warp-uniform)
+  // ---- A3: request, benefit, within-request rank, eligible key ----
+  int rq[2], s0q[2];
+  float bq[2];
+  bool el[2];
+  unsigned long long key[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int q = lane + 32 * i;
+    rq[i] = 0;
+    s0q[i] = 0;
+    bq[i] = 0.f;
+    el[i] = false;
+    key[i] = ~0ull;
+    if (q < nct) {
+      const int r = L.rreq[q / k];
+      const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+      const int e_r = (r + 1 < bl ? L.base[r + 1] : ne) - L.base[r];
+      const float b = L.cb[q];
+      int rank = 0;
+#pragma unroll 8
+      for (int j = s0; j < s1; ++j) {
+        const float bj = L.cb[j];
+        rank += (bj > b) || (bj == b && j < q);
+      }
+      rq[i] = r;
+      s0q[i] = s0;
+      bq[i] = b;
+      if (rank < e_r) {
+        el[i] = true;
+        key[i] = sel_key(b, P.b_off + r, q - s0);
+      }
+    }
+  }
+  stamp(P, lane == 0, 11);
+  // ---- A4: eligible keys compacted (ballot order), then each key's rank among them ----
+  const unsigned e0 = __ballot_sync(kFull, el[0]), e1 = __ballot_sync(kFull, el[1]);
+  const unsigned below = (1u << lane) - 1u;
+  if (el[0]) L.keys[__popc(e0 & below)] = key[0];
+  if (el[1]) L.keys[__popc(e0) + __popc(e1 & below)] = key[1];
+  __syncwarp();
+  int g0 = 0, g1 = 0;
+#pragma unroll 8
+  for (int j = 0; j < ne; ++j) {
+    const unsigned long long kj = L.keys[j];  // broadcast
+    g0 += kj < key[0];
+    g1 += kj < key[1];
+  }
+  __syncwarp();
+  if (el[0]) L.keys2[g0] = key[0];
+  if (el[1]) L.keys2[g1] = key[1];
+  __syncwarp();
+  stamp(P, lane == 0, 12);
+  // ---- A5: tile up-scans, tile 1 after tile 0's total; the first failing entry ----
+  double bj[2], before[2];
+  double t0tot = 0.0;
+  unsigned fail[2] = {0u, 0u};
+  before[1] = bj[1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (i >= nw) break;
+    const int j = lane + 32 * i;
+    const bool act = j < ne;
+    bj[i] = act ? (double)sel_key_b(L.keys2[j]) : 0.0;
+    double incl = bj[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    double excl = __shfl_up_sync(kFull, incl, 1);
+    if (lane == 0) excl = 0.0;
+    double bf = 0.0;
+    if (i == 1) bf += t0tot;
+    bf += excl;
+    before[i] = bf;
+    if (i == 0) t0tot = __shfl_sync(kFull, incl, 31);
+    fail[i] = __ballot_sync(kFull, act && !rule_ok(bj[i], bf, j));
+  }
+  const int js = fail[0] ? __ffs(fail[0]) - 1 : fail[1] ? 32 + __ffs(fail[1]) - 1 : ne;
+  stamp(P, lane == 0, 13);
+  stamp(P, lane == 0, 15);
+  stamp(P, lane == 0, 16);
+  // ---- A6: admitted bitmaps, per-request counts and next-frontier offsets ----
+  const bool adm0 = el[0] && g0 < js, adm1 = el[1] && g1 < js;
+  const unsigned a0 = __ballot_sync(kFull, adm0), a1 = __ballot_sync(kFull, adm1);
+  int nx = 0, a = 0, rs0 = 0, rs1 = 0;
+  if (lane < bl) {
+    rs0 = L.off[lane] * k;
+    rs1 = rs0 + L.cnt[lane] * k;
+    a = __popc(a0 & word_range(rs0, rs1, 0)) + __popc(a1 & word_range(rs0, rs1, 1));
+    nx = (L.fin[lane] || a == 0 || L.nd[lane] + a >= P.B) ? 0 : a;  // Alg.1 line 10
+  }
+  int incl = nx;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int bnext = incl - nx, tot = __shfl_sync(kFull, incl, 31);
+  stamp(P, lane == 0, 17);
+  // node index of an admitted candidate = admitted candidates of its request before it
+  int idx[2], nxr[2], bnr[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int q = lane + 32 * i;
+    idx[i] = __popc(a0 & word_range(s0q[i], q, 0)) + __popc(a1 & word_range(s0q[i], q, 1));
+    nxr[i] = __shfl_sync(kFull, nx, rq[i] & 31);
+    bnr[i] = __shfl_sync(kFull, bnext, rq[i] & 31);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if ((i == 0 ? adm0 : adm1) && nxr[i] > 0) {
+      const int r = rq[i], pos = bnr[i] + idx[i], node = L.nd[r] + 1 + idx[i];
+      P.fr[npar][pos] = make_int2(r, node);
+      pub.entry(pos, r, node);
+      P.fr_cum[npar][pos] = bq[i];  // NODE_SUM: b == cum
+    }
+  }
+  if (lane < bl) P.fr_off[npar][lane] = bnext;
+  if (lane == 31) *P.fr_total[npar] = incl;
+  __syncwarp();
+  stamp(P, lane == 0, 18);
+  if (lane == 0) pub(tot);
+  stamp(P, lane == 0, 19);
+  // ---- after the flag: state the next layer's streaming CTAs do not read ----
+  if (lane < bl) P.fr_cnt[npar][lane] = nx;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int q = lane + 32 * i;
+    const bool ad = i == 0 ? adm0 : adm1;
+    if (q < nct) P.cand_adm[lbase + q] = ad ? 1 : 0;
+    if (ad) {
+      const Cand cd = get_cand(q);
+      const int r = rq[i], node = L.nd[r] + 1 + idx[i];
+      const size_t o = (size_t)r * P.T + node;
+      P.cand_node[lbase + q] = node;
+      P.tok[o] = cd.tok;
+      P.parent[o] = cd.parent;
+      P.depth[o] = layer;
+      P.p[o] = cd.p;
+      P.cum[o] = cd.cum;
+    }
+  }
+  stamp(P, lane == 0, 14);
+  if (lane < bl) {
+    if ((L.fin[lane] || a == 0 || L.nd[lane] + a >= P.B) && L.cnt[lane] > 0) P.finished[lane] = 1;
+    P.n_nodes[lane] = L.nd[lane] + 1 + a;
+    if (a > 0) {
+      double esum = 0.0;  // canonical order (ascending candidate index)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        unsigned bits = (w == 0 ? a0 : a1) & word_range(rs0, rs1, w);
+        while (bits) {
+          esum += (double)L.cb[w * 32 + __ffs(bits) - 1];
+          bits &= bits - 1u;
+        }
+      }
+      L.E[lane] += esum;  // node sum (Q11)
+      P.E_r[lane] = L.E[lane];
+    }
+  }
+  __syncwarp();
+  const double Ea = warp_det_sum(L.E, bl, lane);
+  // trace: argmax_j S_j from the kept prefixes (same association as select_layer)
+  double bestS = sp(E0, 0);
+  int bestj = 0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int j = lane + 32 * i;
+    if (j < ne) {
+      const double Sa = sp(E0 + before[i] + bj[i], j + 1);
+      if (Sa > bestS || (Sa == bestS && j + 1 < bestj)) {
+        bestS = Sa;
+        bestj = j + 1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double os = __shfl_xor_sync(kFull, bestS, o);
+    const int oj = __shfl_xor_sync(kFull, bestj, o);
+    if (os > bestS || (os == bestS && oj < bestj)) {
+      bestS = os;
+      bestj = oj;
+    }
+  }
+  if (lane == 0) {
+    tr.S_after = sp(Ea, js) / bc;
+    *P.N_glob = (int)(N0 + js);
+    *P.E_glob = Ea;
+    tr.executed = R > 0 ? 1 : 0;
+    tr.n_rows = R;
+    tr.n_cand = nct;
+    tr.n_elig = ne;
+    tr.n_admit = js;
+    tr.argmax_j = bestj;
+    tr.N0 = (int)N0;
+    tr.E0 = E0;
+    tr.S0 = sp(E0, 0) / bc;
+    tr.dc0 = dc0;
+    tr.saturated = (N0 + ne >= P.sat_from) ? 1 : 0;
+    if (tr.saturated) atomicOr(P.err, kErrSaturated);
+  }
+  stamp(P, lane == 0, 22);
+}
+
 __device__ __forceinline__ Cand load_cand(const Cand* p) {  // L2 (written by other CTAs)
   const int4 v = __ldcg(reinterpret_cast<const int4*>(p));
   Cand c;
@@ -502,6 +749,11 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
   stamp(P, tid == 0, 10);
   int ne = ss.bcast_i[2];
   long long N0 = ss.bcast_l[1];
+  if (mode == kSelFull && !base && !pmean && nct <= kTinyCand && bl <= 32) {
+    // small layer: the rest by warp 0 alone (the caller's next barrier waits for it)
+    if (warp == 0) select_tiny(P, layer, L, R, ne, N0, ss.bcast_d[2], get_cand, pub);
+    return;
+  }
   if (mode != kSelGlobal) {
     // within-request rank by (b desc, c asc); eligible if rank < e_r (early exit past e_r)
     for (int q = tid; q < nct; q += NT) {
@@ -851,12 +1103,14 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         nx = finished_r(lane, a) ? 0 : a;
         L.nxt[lane] = nx;
       }
+      stamp(P, tid == 0, 20);
       int incl = nx;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(kFull, incl, o);
         if (lane >= o) incl += t;
       }
+      stamp(P, tid == 0, 21);
       if (lane < bl) L.base[lane] = incl - nx;
       __syncwarp();
       stamp(P, tid == 0, 17);
@@ -868,7 +1122,6 @@ __device__ void select_layer(const Params& P, int layer, int mode, char* smem, W
         const int q = L.off[r] * k + c;
         const int idx = bits_below(r, c);
         P.fr[npar][L.base[r] + idx] = make_int2(r, L.nd[r] + 1 + idx);
-      pub.entry(L.base[r] + idx, r, L.nd[r] + 1 + idx);
         pub.entry(L.base[r] + idx, r, L.nd[r] + 1 + idx);
         P.fr_cum[npar][L.base[r] + idx] = pmean ? get_cand(q).cum : L.cb[q];  // NODE_SUM: b == cum
       }

@@ -45,9 +45,10 @@ struct Cand {
 // sees a previous step's flags and nothing needs resetting between steps; the last CTA to exit
 // advances the epoch.
 constexpr int kVerifySlot = SMART_MAX_DEPTH + 1;
+constexpr int kStepMaxGrid = 512;  // persistent step kernel: CTAs per launch at most
 struct StepCtl {
   unsigned long long flag[SMART_MAX_DEPTH + 2];  // [l]: layer-l frontier rows published; [kVerifySlot]: verify rows
-  int arrive[SMART_MAX_DEPTH + 2];               // slices of layer l streamed (reset by the select CTA)
+  unsigned long long vdone[kStepMaxGrid];        // [s]: streaming CTA s posted its verify row maxima (tag)
   int exit_cnt;
   unsigned epoch;
 };
@@ -127,8 +128,10 @@ struct Params {
   unsigned long long* vbest;  // [b_loc*T] target argmax key of each tree row (red.max; cleared by the walk)
 
   // ---- persistent whole-step kernel (step.cu) ----
-  unsigned long long* seg_keys;  // slice top-k lists of the current layer, dense [row * t + member][kp]
-  float2* seg_ms;                // per-chunk softmax partials (M_c, S_c) of the current layer [row][cpr]
+  // self-validating 16-byte lines {a, tag, b, tag} (tag = entry tag of the launch and layer):
+  uint4* seg_key;   // slice top-k lists of the current layer, [row * t + member][k] (key lo, key hi)
+  uint4* seg_ms;    // per-chunk softmax partials of the current layer, [row][cpr] (M_c, S_c)
+  uint4* seg_cand;  // the merged candidates of the current layer, [row][k] (token, p)
   StepCtl* ctl;
   unsigned long long* fr_tag;    // [max(cap_rows, b_loc * T)] self-validating frontier entries
                                  // ((tag << 5 | layer) << 32) | r << 10 | node; then the verify rows (layer 31)

@@ -6,24 +6,24 @@
 //
 // Layout: gridDim.x - 1 streaming CTAs and one selection CTA, all co-resident
 // (grid = SMs x occupancy).  Layers are separated by flags in global memory, not by kernel
-// boundaries:
+// boundaries, and every cross-SM hop is a self-validating tagged word or 16-byte line (tag =
+// launch epoch and layer) polled with relaxed loads: no arrival counters, no fences per layer.
 //  * streaming CTA s, layer l with R frontier rows: team size t = min(cpr, S / R, 32) (t = 1 when
 //    R > S); CTA s is member s % t of team s / t, which streams rows team, team + S/t, ...; the
 //    member's slice of a row is chunks [m cpr / t, (m+1) cpr / t).  A producer lane bulk-copies the
 //    chunks into the TMA ring (cp.async.bulk + mbarrier), 8 consumer warps reduce them
-//    (expand_core.cuh) and write the slice's top-k list and per-chunk softmax partials to global
-//    memory, then one red.release.gpu arrival per slice.  Layer 1's rows are the roots (r, 0): no
-//    wait.  For layer l >= 2 the producer lane polls flag[l] (ld.acquire.gpu) and reads its rows'
-//    frontier entries; consumers learn the row count from it through a shared-memory mbarrier.
-//  * the selection CTA keeps the per-request state, waits for the R * t arrivals of a layer, stages
-//    all slice lists and partials in shared memory with one round of L2 loads, merges every row
-//    (one warp per row: Z, threshold, survivors, rank; expand_core.cuh merge_row) straight into the
-//    selection's staged candidate records, runs A3-A6 (select_layer) and publishes the next
-//    frontier as flag[l+1] = (tag << 32 | R').  After the last layer it writes the verify-row table
-//    and publishes flag[kVerifySlot]; the streaming CTAs stream every tree row of the target logits
-//    (exact argmax, red.max on the row's slot) while it writes the mask outputs; then it walks.
-// There is no leader merge and no cluster: the only cross-SM hops per layer are the slice arrivals
-// and the frontier flag.
+//    (expand_core.cuh) and write the slice's top-k list and per-chunk softmax partials as tagged
+//    lines.  Member 0 of the team then polls the row's t lists and cpr partials, merges them (one
+//    warp: Z and a k-round tournament) and writes the row's k candidates (token, p) as tagged
+//    lines.  Layer 1's rows are the roots (r, 0); for layer l >= 2 the producer lane polls
+//    flag[l] and its rows' tagged frontier entries; consumers learn the row count through a
+//    shared-memory mbarrier.
+//  * the selection CTA keeps the per-request state, polls the layer's R * k candidate lines into
+//    its staged records (cum = cum(parent) * p, Eq.(3)), runs A3-A6 (select_layer) and publishes
+//    the next frontier as tagged entries and flag[l+1] = (tag << 32 | R').  After the last layer it
+//    writes the verify-row table and publishes flag[kVerifySlot]; the streaming CTAs stream every
+//    tree row of the target logits (exact argmax, red.max on the row's slot, then one release word
+//    per CTA) while it writes the mask outputs; then it walks.
 #include "expand_core.cuh"
 #include "select_core.cuh"
 #include "verify_core.cuh"
@@ -45,6 +45,17 @@ struct __align__(16) StepShared {
   int rv[SMART_MAX_DEPTH + 2];
   uint64_t evb[SMART_MAX_DEPTH + 2];
 };
+// the team merge (member 0 of a row's team) stages the row's t slice lists (stride kp) and cpr
+// partials in the warps' top-k buffers (dead between slices): no extra shared memory, so two
+// streaming CTAs still fit one SM
+static_assert(sizeof(WarpTopk) * kConsumerWarps >= (size_t)kTeamMax * kMaxK * 8 + kMaxCpr * sizeof(float2),
+              "team-merge staging must fit the warp buffers");
+__device__ __forceinline__ unsigned long long* merge_keys(StepShared& sh) {
+  return reinterpret_cast<unsigned long long*>(&sh.cs.w[0]);
+}
+__device__ __forceinline__ float2* merge_ms(StepShared& sh) {
+  return reinterpret_cast<float2*>(reinterpret_cast<char*>(&sh.cs.w[0]) + (size_t)kTeamMax * kMaxK * 8);
+}
 
 __device__ __forceinline__ void post_event(StepShared& sh, int e, int v) {
   sh.rv[e] = v;
@@ -54,9 +65,6 @@ __device__ __forceinline__ int wait_event(StepShared& sh, int e) {
   mbar_wait(&sh.evb[e], 0u);  // acquire (CTA scope)
   return sh.rv[e];
 }
-
-// row stride of the per-chunk partials (even: a layer's partials are whole 16-byte units)
-__host__ __device__ inline int ms_stride(int cpr) { return (cpr + 1) & ~1; }
 
 __host__ __device__ inline int team_size(int R, int S, int cpr) {
   if (R <= 0 || R >= S) return 1;
@@ -92,14 +100,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -107,22 +107,8 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 // flag (SMART_EDEVICE from smart_get_stats) and lets the step run out instead of hanging the GPU.
 constexpr unsigned kPollLimit = 1u << 24;
 
-// poll a (tag << 32 | value) flag of this launch; returns the value (0 on timeout)
-__device__ __forceinline__ int wait_tag(const unsigned long long* f, unsigned tag, int* err) {
-  for (unsigned it = 0;; ++it) {
-    const unsigned long long v = ld_relaxed_u64(f);
-    if ((unsigned)(v >> 32) == tag) {
-      fence_acq_rel_gpu();
-      return (int)(unsigned)v;
-    }
-    if (it > kPollLimit) {
-      atomicOr(err, kErrTimeout);
-      return 0;
-    }
-    __nanosleep(20);
-  }
-}
-// the same without the acquire fence: for flags after which only self-validating words are read
+// poll a (tag << 32 | value) flag of this launch; returns the value (0 on timeout).  No acquire
+// fence: after a flag only self-validating words are read
 __device__ __forceinline__ int wait_tag_relaxed(const unsigned long long* f, unsigned tag, int* err) {
   for (unsigned it = 0;; ++it) {
     const unsigned long long v = ld_relaxed_u64(f);
@@ -148,6 +134,30 @@ __device__ __forceinline__ unsigned wait_entry(const unsigned long long* e, unsi
   }
 }
 
+// Self-validating 16-byte lines {a, tag, b, tag}: each 8-byte half carries the tag, so a torn
+// access is caught.  The slice lists / partials and the merged candidates of a layer are polled on
+// the data itself: no arrival counter (serialised at one L2 address) and no release/acquire fence
+// on the hop (tools/ubench/handoff.cu: 16 slices, 1.47 us with counter + fences, 0.1 us tagged).
+__device__ __forceinline__ void st_line(uint4* p, unsigned a, unsigned b, unsigned tag) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(tag), "r"(b), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ uint2 wait_line(const uint4* p, unsigned tag, int* err) {
+  for (unsigned it = 0;; ++it) {
+    unsigned a, t0, b, t1;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(t0), "=r"(b), "=r"(t1)
+                 : "l"(p)
+                 : "memory");
+    if (t0 == tag && t1 == tag) return make_uint2(a, b);
+    if (it > kPollLimit) {
+      atomicOr(err, kErrTimeout);
+      return make_uint2(0u, 0u);
+    }
+    __nanosleep(32);  // a waiting warp must not take issue slots from the SM's streaming warps
+  }
+}
+
 // the step kernel's frontier publication: every entry also as a self-validating tagged word, the
 // row count as a tagged flag, all with plain stores (no release fence on the critical path: what
 // the streaming CTAs read behind the flag is the tagged entries themselves)
@@ -165,17 +175,6 @@ struct StepPub {
   }
 };
 
-// poll an arrival counter until it reaches `want`
-__device__ __forceinline__ void wait_count(const int* c, int want, int* err) {
-  for (unsigned it = 0; ld_relaxed_s32(c) < want; ++it) {
-    if (it > kPollLimit) {
-      atomicOr(err, kErrTimeout);
-      return;
-    }
-    __nanosleep(20);
-  }
-  fence_acq_rel_gpu();
-}
 
 // timeline probes (SMART_PROBES=1 builds only): dbg[256 + 16 * layer + slot], globaltimer ns;
 // "max" slots keep the latest time, "min" slots the complement of the earliest (atomicMax of ~t)
@@ -192,6 +191,46 @@ __device__ __forceinline__ void pb_max(const Params& P, int layer, int slot) {
 }
 __device__ __forceinline__ void pb_min(const Params& P, int layer, int slot) {
   if (SMART_PROBES && P.dbg) atomicMax(&P.dbg[256 + 16 * layer + slot], ~gtime());
+}
+
+// ---------------------------------------------------------------------------------------------
+// team merge (A1 finish + A2 of one row), by member 0 of the row's team once its own slice is
+// out: the row's t slice lists and cpr per-chunk partials are polled as tagged lines into shared
+// memory, warp 0 merges them (k-round tournament, expand_core.cuh) and writes the row's k
+// candidates (token, p) as tagged lines; the selection CTA forms cum = cum(parent) * p (Eq.(3))
+// from its own frontier.  Rows merge in parallel on their teams instead of one after another on
+// the selection CTA.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int row, int t, unsigned lt) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int k = P.k, kp = list_stride(k), cpr = P.cpr;
+  const int nkl = t * k, nl = nkl + cpr;
+  const uint4* gk = P.seg_key + (size_t)row * t * k;
+  const uint4* gm = P.seg_ms + (size_t)row * cpr;
+  unsigned long long* mk = merge_keys(sh);
+  float2* mm = merge_ms(sh);
+  for (int e = tid; e < nl; e += kConsumers) {
+    if (e < nkl) {
+      const uint2 v = wait_line(gk + e, lt, P.err);
+      mk[(e / k) * kp + e % k] = ((unsigned long long)v.y << 32) | v.x;
+    } else {
+      const uint2 v = wait_line(gm + (e - nkl), lt, P.err);
+      mm[e - nkl] = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+    }
+  }
+  consumer_sync();
+  if (warp == 0) {
+    uint4* gc = P.seg_cand + (size_t)row * k;
+    const bool ok = merge_row_tournament(
+        k, cpr, t, 1.f,
+        [&](int c) {
+          const float2 v = mm[c];
+          return make_float4(v.x, v.y, 0.f, 0.f);
+        },
+        mk, [&](int rank, int tok, float p, float) { st_line(gc + rank, (unsigned)tok, __float_as_uint(p), lt); });
+    if (!ok && (tid & 31) == 0) atomicOr(P.err, kErrDraftNaN);  // Q23
+  }
+  consumer_sync();  // the warp buffers are the next slice's again
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -227,7 +266,6 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
       const int t = team_size(R, S, cpr);
       const int nteams = S / t, team = s / t, member = s - team * t;
       const int mlo = member * cpr / t, mhi = (member + 1) * cpr / t;
-      const int par = (layer - 1) & 1;
       if (team < nteams) {
         for (int row = team; row < R; row += nteams) {
           int r = row, node = 0;  // layer 1: the roots
@@ -309,17 +347,21 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
           P.dbg[1024 + 4 * s + 2] = gtime();
           P.dbg[1024 + 4 * s + 3] = (unsigned long long)(mhi - mlo) | ((unsigned long long)row << 8) | ((unsigned long long)smid_reg() << 16);
         }
-        unsigned long long* gk = P.seg_keys + (size_t)(row * t + member) * kp;
-        float2* gm = P.seg_ms + (size_t)row * ms_stride(cpr) + mlo;
+        const unsigned lt = entry_tag(tag, layer);
+        uint4* gk = P.seg_key + (size_t)(row * t + member) * k;
+        uint4* gm = P.seg_ms + (size_t)row * cpr + mlo;
         slice_end_merge(
-            sh.cs, sh.msl, k, mhi - mlo, [&](int rank, unsigned long long key) { gk[rank] = key; },
-            [&](int cc, float Mc, float Sc) { gm[cc] = make_float2(Mc, Sc); });
-        consumer_sync();  // the slice's records are written (cumulative release below)
+            sh.cs, sh.msl, k, mhi - mlo,
+            [&](int rank, unsigned long long key) {
+              if (rank < k) st_line(gk + rank, (unsigned)key, (unsigned)(key >> 32), lt);
+            },
+            [&](int cc, float Mc, float Sc) { st_line(gm + cc, __float_as_uint(Mc), __float_as_uint(Sc), lt); });
+        consumer_sync();  // sh.cl / msl are reused by the next slice
         if (tid == 0) {
           pb_max(P, layer, kPbSliceMax);
-          red_add_release_gpu(&P.ctl->arrive[layer], 1);
           sh.cs.tau = 0ull;  // next slice (read only after the next slice's first barrier)
         }
+        if (member == 0) team_merge(P, sh, row, t, lt);
       }
     }
     R = wait_event(sh, ev++);
@@ -362,46 +404,35 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
   consumer_sync();
   if (tid == 0) {
     pb_max(P, kVerifySlot, kPbSliceMax);
-    red_add_release_gpu(&P.ctl->arrive[kVerifySlot], 1);
+    // release (cumulative over the barrier: the CTA's red.max on the row slots), one word per CTA
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&P.ctl->vdone[s]), "l"((unsigned long long)tag << 32)
+                 : "memory");
   }
 }
 
 // ---------------------------------------------------------------------------------------------
 // selection CTA
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
 
 struct MergeLayout {
-  int2* fe;                 // [rows] frontier entry (request, node)
-  float* pc;                // [rows] parent cum
-  int* slot;                // [rows] frontier slot within the request
-  unsigned long long* keys; // staged slice lists [R * t * kp]
-  float2* ms;               // staged per-chunk partials [R * cpr]
+  int2* fe;    // [rows] frontier entry (request, node)
+  float* pc;   // [rows] parent cum
+  int* slot;   // [rows] frontier slot within the request
 };
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t merge_bytes(int rows_cap, int key_cap, int cpr, int k) {
-  return a16((size_t)rows_cap * 8) + a16((size_t)rows_cap * 4) + a16((size_t)rows_cap * 4) +
-         a16((size_t)key_cap * list_stride(k) * 8) + a16((size_t)rows_cap * ms_stride(cpr) * 8);
+__host__ __device__ inline size_t merge_bytes(int rows_cap) {
+  return a16((size_t)rows_cap * 8) + a16((size_t)rows_cap * 4) + a16((size_t)rows_cap * 4);
 }
 
-__device__ inline MergeLayout merge_layout(char* p, int rows_cap, int key_cap, int cpr, int k) {
+__device__ inline MergeLayout merge_layout(char* p, int rows_cap) {
   MergeLayout M;
   M.fe = reinterpret_cast<int2*>(p);
   p += a16((size_t)rows_cap * 8);
   M.pc = reinterpret_cast<float*>(p);
   p += a16((size_t)rows_cap * 4);
   M.slot = reinterpret_cast<int*>(p);
-  p += a16((size_t)rows_cap * 4);
-  M.keys = reinterpret_cast<unsigned long long*>(p);
-  p += a16((size_t)key_cap * list_stride(k) * 8);
-  M.ms = reinterpret_cast<float2*>(p);
   return M;
 }
 
@@ -412,8 +443,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   if (warp >= kConsumerWarps) return;
   const int S = P.step_S, k = P.k, cpr = P.cpr, kp = list_stride(k), T = P.T, bl = P.b_loc;
   const int rows_cap = P.cap_rows > bl ? P.cap_rows : bl;
-  const int key_cap = S > rows_cap ? S : rows_cap;
-  MergeLayout M = merge_layout(dsm + a16(sel_bytes), rows_cap, key_cap, cpr, k);
+  MergeLayout M = merge_layout(dsm + a16(sel_bytes), rows_cap);
 
   // ---- begin step: S_0 = A_0 = {root} for every request ----
   for (int r = tid; r < bl; r += kConsumers) {
@@ -462,57 +492,19 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
         M.fe[row] = fe;
         M.pc[row] = P.fr_cum[par][row];
         M.slot[row] = row - P.fr_off[par][fe.x];
-      }
-      if (tid == 0) {
-        const int want = R * t;
-        wait_count(&P.ctl->arrive[layer], want, P.err);
-        P.ctl->arrive[layer] = 0;  // no further arrivals this step
-        pb_max(P, layer, kPbArrived);
+        L.rreq[row] = fe.x;
       }
       consumer_sync();
       if (tid == 0) pb_max(P, layer, kPbSync1);
-      // one round of L2 loads (cp.async, 16-byte units): every slice list and chunk partial
-      {
-        const int nk2 = R * t * kp / 2;  // kp even
-        const int nm2 = R * ms_stride(cpr) / 2;
-        const int4* gk = reinterpret_cast<const int4*>(P.seg_keys);
-        const int4* gm = reinterpret_cast<const int4*>(P.seg_ms);
-        int4* sk = reinterpret_cast<int4*>(M.keys);
-        int4* smv = reinterpret_cast<int4*>(M.ms);
-        for (int e = tid; e < nk2; e += kConsumers) cp_async16(sk + e, gk + e);
-        for (int e = tid; e < nm2; e += kConsumers) cp_async16(smv + e, gm + e);
-        cp_async_wait_all();
+      // the rows' merged candidates (team merges), polled as tagged lines straight into the
+      // selection's staged records: cum = cum(parent) * p (Eq.(3)), parent = the row's node
+      const unsigned lt = entry_tag(tag, layer);
+      for (int q = tid; q < R * k; q += kConsumers) {
+        const uint2 v = wait_line(P.seg_cand + q, lt, P.err);
+        const int row = q / k;
+        crec[q] = make_int4((int)v.x, (int)v.y, __float_as_int(__fmul_rn(M.pc[row], __uint_as_float(v.y))), M.fe[row].y);
       }
       consumer_sync();
-      if (tid == 0) pb_max(P, layer, kPbStaged);
-      // row merges (k-round tournaments over the t sorted slice lists), one warp per row,
-      // straight into the selection's staged records
-      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[900 + layer * 8] = clock64();
-      const int mss = ms_stride(cpr);
-      for (int row = warp; row < R; row += kConsumerWarps) {
-        const int2 fe = M.fe[row];
-        const unsigned long long* keys = M.keys + (size_t)row * t * kp;
-        const float2* ms = M.ms + (size_t)row * mss;
-        int4* sout = crec + row * k;
-        const bool ok = merge_row_tournament(
-            k, cpr, t, M.pc[row],
-            [&](int c) {
-              const float2 v = ms[c];
-              return make_float4(v.x, v.y, 0.f, 0.f);
-            },
-            keys,
-            [&](int rank, int tok, float p, float cum) {
-              sout[rank] = make_int4(tok, __float_as_int(p), __float_as_int(cum), fe.y);
-            });
-        if (SMART_PROBES && P.dbg && tid == 0 && row == 0) P.dbg[901 + layer * 8] = clock64();
-        if (lane == 0) {
-          L.rreq[row] = fe.x;
-          if (!ok) atomicOr(P.err, kErrDraftNaN);  // Q23
-        }
-      }
-      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[902 + layer * 8] = clock64();
-      consumer_sync();
-      if (SMART_PROBES && P.dbg && tid == 0) P.dbg[903 + layer * 8] = clock64();
       if (tid == 0) pb_max(P, layer, kPbMerged);
       return true;
     };
@@ -622,13 +614,18 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   if (!verify || NR == 0) return;
 
   // ---- A8 walk once every verify slice has posted its row maxima ----
-  if (tid == 0) {
+  {
+    // every verify CTA's done word (polled in parallel; relaxed load + fence = acquire)
     const int want = range_ctas(NR * cpr, S, P.min_units);
-    wait_count(&P.ctl->arrive[kVerifySlot], want, P.err);
-    P.ctl->arrive[kVerifySlot] = 0;
-    pb_max(P, kVerifySlot, kPbArrived);
+    bool seen = false;
+    for (int c = tid; c < want; c += kConsumers) {
+      (void)wait_tag_relaxed(&P.ctl->vdone[c], tag, P.err);
+      seen = true;
+    }
+    if (seen) fence_acq_rel_gpu();
   }
   consumer_sync();
+  if (tid == 0) pb_max(P, kVerifySlot, kPbArrived);
   for (int e = tid; e < bl * T; e += kConsumers) {
     const int r = e / T;
     if (e - r * T < s_n[r]) {
@@ -723,8 +720,7 @@ size_t step_stream_smem_bytes() { return (size_t)kStages * kChunkBytes + sizeof(
 
 size_t step_select_smem_bytes(const Params& P, int S, size_t sel_bytes) {
   const int rows_cap = P.cap_rows > P.b_loc ? P.cap_rows : P.b_loc;
-  const int key_cap = S > rows_cap ? S : rows_cap;
-  const size_t sel = a16(sel_bytes) + merge_bytes(rows_cap, key_cap, P.cpr, P.k);
+  const size_t sel = a16(sel_bytes) + merge_bytes(rows_cap);
   const size_t fin = a16((size_t)(2 * P.b_loc + 2) * 4) + (size_t)5 * P.b_loc * P.T * 4;
   return sel > fin ? sel : fin;
 }
@@ -755,7 +751,7 @@ int step_grid(const Params& P, size_t sel_bytes, size_t* smem_out) {
       cudaGetLastError();
       return 0;
     }
-    grid = nsm * occ;
+    grid = std::min(nsm * occ, kStepMaxGrid);
     const size_t need = std::max(step_stream_smem_bytes(), step_select_smem_bytes(P, grid - 1, sel_bytes));
     if (need <= smem) break;
     smem = need;  // fewer CTAs per SM: recompute the grid (the scratch shrinks with S)

@@ -48,12 +48,12 @@ print(f"kernel end {f(g(0,8))} us")
 for l in range(1, wl["d"] + 1):
     c = [int(buf[900 + l * 8 + j]) for j in range(4)]
     print(f"layer {l}: merge cycles row0 {c[1]-c[0]}, warp0 rows {c[2]-c[0]}, barrier {c[3]-c[2]}")
-names = {9: "start", 10: "benefits", 11: "req-rank", 12: "sort", 13: "A5 cut", 15: "bitmaps", 16: "B6",
+names = {9: "start", 10: "benefits", 11: "req-rank", 12: "sort", 13: "A5 cut", 15: "bitmaps", 16: "B6", 20: "popc", 21: "scan",
          17: "counts", 18: "frontier", 19: "published", 14: "adm flags", 22: "end"}
 for l in range(1, wl["d"] + 1):
     c = {j: int(buf[3000 + l * 16 + (j - 9)]) for j in range(9, 23)}
     base = c[9]
-    print(f"layer {l} select phases (cycles from start):", ", ".join(f"{names[j]} {c[j]-base}" for j in (10, 11, 12, 13, 15, 16, 17, 18, 19, 14, 22) if c[j]))
+    print(f"layer {l} select phases (cycles from start):", ", ".join(f"{names[j]} {c[j]-base}" for j in (10, 11, 12, 13, 15, 16, 20, 21, 17, 18, 19, 14, 22) if c[j]))
 pc = []
 for sidx in range(4096 // 4 - 256):
     a, b_, c_, m = (int(buf[1024 + 4 * sidx + j]) for j in range(4))
