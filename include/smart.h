@@ -128,6 +128,11 @@ typedef struct {
   int32_t argmax_j;       /* argmax_j S_j over prefixes (reported, Q7)                      */
   int32_t N0;             /* drafted nodes before the layer (global)                        */
   int32_t saturated;      /* cost exponent clamped (Q17)                                    */
+  int32_t select_path;    /* which selection ran (diagnostic): 0 the block selection, 1 the
+                             small-batch one-warp path, 2 the same with the full sorted list
+                             rebuilt for argmax_j, 3 the small path handed over to the block one */
+  int32_t n_screened;     /* small-batch path: candidates above its benefit threshold (the
+                             only ones ranked); 0 on the block path         */
   double E0;              /* sum_r E_r before the layer (global request order)              */
   double S0;              /* S before the layer (per request, Eq.(1) generalised)           */
   double S_after;         /* S after the layer                                              */

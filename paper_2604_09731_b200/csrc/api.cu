@@ -861,6 +861,8 @@ smart_status smart_get_stats(smart_ctx* c, smart_stats* out) {
     t.argmax_j = tr[l].argmax_j;
     t.N0 = tr[l].N0;
     t.saturated = tr[l].saturated;
+    t.select_path = tr[l].select_path;
+    t.n_screened = tr[l].n_screened;
     t.E0 = tr[l].E0;
     t.S0 = tr[l].S0;
     t.S_after = tr[l].S_after;

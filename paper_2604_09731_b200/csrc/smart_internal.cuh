@@ -55,7 +55,7 @@ struct StepCtl {
 
 // device copy of one layer's trace (same fields as smart_layer_trace)
 struct DevTrace {
-  int32_t executed, n_rows, n_cand, n_elig, n_admit, argmax_j, N0, saturated;
+  int32_t executed, n_rows, n_cand, n_elig, n_admit, argmax_j, N0, saturated, select_path, n_screened;
   double E0, S0, S_after, dc0;
 };
 

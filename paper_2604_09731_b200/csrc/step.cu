@@ -24,6 +24,8 @@
 //    writes the verify-row table and publishes flag[kVerifySlot]; the streaming CTAs stream every
 //    tree row of the target logits (exact argmax, red.max on the row's slot, then one release word
 //    per CTA) while it writes the mask outputs; then it walks.
+#include <cstdlib>
+
 #include "expand_core.cuh"
 #include "select_core.cuh"
 #include "verify_core.cuh"
@@ -436,6 +438,464 @@ __device__ inline MergeLayout merge_layout(char* p, int rows_cap) {
   return M;
 }
 
+// ---------------------------------------------------------------------------------------------
+// select_small: A3-A6 of one layer for small batches (one rank, <= 32 requests, NODE_SUM, PREFIX
+// or FROZEN) -- the same decisions, node numbering, fp64 associations and trace as select_layer,
+// computed on the few candidates that can matter, in one warp, with the per-request state in
+// registers (lane r of warp 0 holds request r).  The selection CTA runs once per layer, so its
+// code is always cold in the 32 KB instruction cache: this path is short, straight-line code
+// instead of select_layer's generic phases.
+//  * theta (known before the layer's candidates arrive): Eq.(16) admits the candidate at sorted
+//    position j only if alpha c_T b_j C(N0+j) > (rhs0 + c_T before_j) dc(N0+j) with before_j >= 0,
+//    so every admitted candidate has b > theta = min_j rhs0 dc(N0+j) / (alpha c_T C(N0+j))
+//    (FROZEN: the j = 0 term is its whole rule).  Every candidate that beats an above-theta one
+//    within its request (A3) or globally (A4) is itself above theta, so ranks, eligibility and the
+//    order of the above-theta eligible candidates are exact among them alone, and the first sorted
+//    position at or below theta fails the rule: the cut lies in the above-theta prefix (cfg3: 30
+//    above-theta candidates of 256 at layer 1, 28 admitted).
+//  * one warp, lane = one above-theta candidate: "better than" / same-request / lower-index masks,
+//    within-request rank = popc(better & same) < e_r (A3, Eq.(8)), sorted position = popc(better &
+//    eligible) (A4), tile 0 of the block path's A5 scan and rule (same association), node index =
+//    admitted candidates of the request with a lower canonical index (A6).
+//  * trace argmax_j S_j: exact over the above-theta prefix; beyond it every benefit is <= theta, so
+//    S_j <= c_T (omega b + E0 + P + (j - n) theta) / C(N0+j); if that bound stays below the best S
+//    (1e-9 margin) the argmax is final, else the full list is rebuilt (small_trace_full).
+// Falls back (returns false; the records are staged for select_layer) when theta is not usable,
+// more than 32 candidates are above it, or the eligible list is longer than kA5Par.
+// ---------------------------------------------------------------------------------------------
+struct SmallState {  // lane r of warp 0: request r's state before the layer
+  int cnt, off, nd, fin;
+  double E;
+};
+struct SmallShared {
+  double theta, E0, th_cut, th_arg;
+  long long N0;
+  int ne, n_above, need_full, bestj;
+  int a[32];
+  unsigned long long akeys[64];
+};
+
+__device__ __forceinline__ void small_state_load(const Params& P, int par, int lane, SmallState& st) {
+  if (lane < P.b_loc) {
+    st.cnt = P.fr_cnt[par][lane];
+    st.off = P.fr_off[par][lane];
+    st.nd = P.n_nodes[lane] - 1;
+    st.fin = P.finished[lane];
+    st.E = P.E_r[lane];
+  } else {
+    st.cnt = st.off = st.nd = st.fin = 0;
+    st.E = 0.0;
+  }
+}
+
+// the full sorted eligible list of a layer for the trace argmax (rare: only when the bound of
+// select_small cannot exclude the positions below theta); all 256 threads, block-path association
+__device__ __forceinline__ void small_trace_full(const Params& P, char* dsm, SmallShared& sh, int nct, int ne, double E0,
+                                              int bc) {
+  SelLayout L = sel_layout(dsm, P.b_loc, P.cap_rows * P.k, P.k, P.sort_cap);
+  L.keys = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(L.E) + sel_align((size_t)P.b_loc * 8));
+  L.keys2 = L.keys + P.sort_cap;
+  const int* ebase = L.base;
+  __shared__ double tile[kA5Par / 32], wS[kConsumerWarps];
+  __shared__ int wJ[kConsumerWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, k = P.k, bl = P.b_loc;
+  for (int q = tid; q < nct; q += kConsumers) {
+    const int r = L.rreq[q / k];
+    const int s0 = L.off[r] * k, s1 = s0 + L.cnt[r] * k;
+    const int e_r = (r + 1 < bl ? ebase[r + 1] : ne) - ebase[r];
+    const float b = L.cb[q];
+    int rank = 0;
+    for (int j = s0; j < s1; ++j) {
+      const float bj = L.cb[j];
+      rank += (bj > b) || (bj == b && j < q);
+    }
+    if (rank < e_r) L.keys2[ebase[r] + rank] = sel_key(b, P.b_off + r, q - s0);
+  }
+  consumer_sync();
+  for (int i = tid; i < ne; i += kConsumers) {
+    const unsigned long long key = L.keys2[i];
+    int rank = 0;
+    for (int f = 0; f < ne; ++f) rank += L.keys2[f] < key;
+    L.keys[rank] = key;
+  }
+  consumer_sync();
+  const bool act = tid < ne;
+  const double bj = act ? (double)sel_key_b(L.keys[tid]) : 0.0;
+  double incl = bj;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += u;
+  }
+  double excl = __shfl_up_sync(kFull, incl, 1);
+  if (lane == 0) excl = 0.0;
+  if (lane == 31) tile[warp] = incl;
+  consumer_sync();
+  double before = 0.0;
+  for (int w = 0; w < warp; ++w) before += tile[w];
+  before += excl;
+  double bestS = -1.0;
+  int bestj = 1 << 30;
+  if (act) {
+    const double C = L.ctab[tid + 1];
+    bestS = C > 0.0 ? P.c_T * ((double)P.omega * bc + (E0 + before + bj)) / C : 0.0;
+    bestj = tid + 1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double os = __shfl_xor_sync(kFull, bestS, o);
+    const int oj = __shfl_xor_sync(kFull, bestj, o);
+    if (os > bestS || (os == bestS && oj < bestj)) {
+      bestS = os;
+      bestj = oj;
+    }
+  }
+  if (lane == 0) {
+    wS[warp] = bestS;  // per-warp winners
+    wJ[warp] = bestj;
+  }
+  consumer_sync();
+  if (tid == 0) {
+    const double C0 = L.ctab[0];
+    double S = C0 > 0.0 ? P.c_T * ((double)P.omega * bc + E0) / C0 : 0.0;
+    int j = 0;
+    for (int w = 0; w < kConsumerWarps; ++w)
+      if (wJ[w] <= ne && (wS[w] > S || (wS[w] == S && wJ[w] < j))) {
+        S = wS[w];
+        j = wJ[w];
+      }
+    sh.bestj = j;
+  }
+  consumer_sync();
+}
+
+template <class Pub>
+__device__ __forceinline__ bool select_small(const Params& P, int layer, int R, char* dsm, const MergeLayout& M,
+                                             const MergeLayout& Mn, bool rows_in_smem, SmallState& st,
+                                             SmallShared& sh, unsigned tag, Pub pub) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int par = (layer - 1) & 1, npar = layer & 1;
+  const int k = P.k, bl = P.b_loc, nct = R * k, T = P.T;
+  const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+  SelLayout L = sel_layout(dsm, bl, P.cap_rows * k, k, P.sort_cap);
+  L.keys = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(L.E) + sel_align((size_t)bl * 8));
+  L.keys2 = L.keys + P.sort_cap;
+  int4* const crec = reinterpret_cast<int4*>(L.keys + 2 * (size_t)P.sort_cap);
+  const int bc = (P.cost_scope == SMART_COST_LOCAL) ? bl : P.b_glob;
+  const double ac = P.alpha * P.c_T;
+  stamp(P, tid == 0, 9);
+  // ---- before the candidates: A3 budgets (lane r), N0, E0, the cost window, theta and the
+  // argmax threshold (warp 0); the rows' descriptors (from the last layer's shared copy) ----
+  int e = 0, eb = 0;
+  if (warp == 0) {
+    if (lane < bl) {
+      int q = P.B - st.nd;
+      if (q > P.Wq) q = P.Wq;
+      if (q < 0) q = 0;
+      e = min(q, st.cnt * k);  // e_r = min(B - n_r, W, |U_r|)
+    }
+    int incl = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    eb = incl - e;
+    const int ne = __shfl_sync(kFull, incl, 31);
+    int nd = lane < bl ? st.nd : 0;
+    double Ev = lane < bl ? st.E : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      nd += __shfl_xor_sync(kFull, nd, o);
+      Ev += __shfl_xor_sync(kFull, Ev, o);  // warp_det_sum of one tile (Q13)
+    }
+    const long long N0 = nd;
+    const double rhs0 = P.c_T * ((double)P.omega * bc + Ev);
+    const int ncw = min(nct, P.sort_cap) + 2;
+    double th = INFINITY;
+    bool ok = ac > 0.0 && P.c_T >= 0.0 && rhs0 >= 0.0;
+#pragma unroll 1
+    for (int j = lane; j < ncw; j += 32) {
+      const long long N = min(N0 + j, (long long)P.n_cost - 1);
+      const double C = P.cost_tab[N], dcj = P.dc_tab[N];
+      L.ctab[j] = C;
+      L.dtab[j] = dcj;
+      const double tj = C > 0.0 ? rhs0 * dcj * __drcp_rn(ac * C) : 0.0;
+      ok = ok && dcj >= 0.0 && tj == tj;
+      th = fmin(th, tj);
+    }
+    __syncwarp();  // the window written by the other lanes
+    // argmax threshold: on a convex window (dC nondecreasing over prefix lengths 0..ne+1) with
+    // sorted benefits, S_j is unimodal (S_{j+1} lies between S_j and b_j / dC_j), and a step can
+    // raise S only if b_j > s_j dC_j >= s_0 min dC (s = S / c_T): every benefit <= th2 = s_0 min dC
+    // ends the rise for good; 1e-9 below keeps the computed S of later prefixes under the maximum
+    bool cvx = L.ctab[0] > 0.0;
+    double dmin = INFINITY;
+#pragma unroll 1
+    for (int j = lane; j <= ne; j += 32) {
+      const double d0 = L.ctab[j + 1] - L.ctab[j];
+      dmin = fmin(dmin, d0);
+      if (j + 1 <= ne) cvx = cvx && (L.ctab[j + 2] - L.ctab[j + 1]) >= d0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      th = fmin(th, __shfl_xor_sync(kFull, th, o));
+      dmin = fmin(dmin, __shfl_xor_sync(kFull, dmin, o));
+    }
+    ok = __all_sync(kFull, ok) && th > 0.0 && th < INFINITY;
+    cvx = __all_sync(kFull, cvx) && dmin > 0.0 && dmin < INFINITY;
+    if (lane == 0) {
+      const double thc = ok ? th * (1.0 - 1e-12) : -1.0;
+      const double th2 = cvx ? ((double)P.omega * bc + Ev) / L.ctab[0] * dmin * (1.0 - 1e-9) : -1.0;
+      sh.th_cut = thc;
+      sh.th_arg = th2;
+      sh.theta = (thc >= 0.0 && th2 > 0.0) ? fmin(thc, th2) : thc;  // the screening threshold
+      sh.E0 = Ev;
+      sh.N0 = N0;
+      sh.ne = ne;
+      sh.n_above = 0;
+    }
+  }
+  if (!rows_in_smem) {  // after a block-path layer: the rows from its global frontier
+    for (int row = tid; row < R; row += kConsumers) {
+      const int2 fe = P.fr[par][row];
+      M.fe[row] = fe;
+      M.pc[row] = P.fr_cum[par][row];
+      M.slot[row] = row - P.fr_off[par][fe.x];
+    }
+  }
+  consumer_sync();
+  stamp(P, tid == 0, 10);
+  if (tid == 0) pb_max(P, layer, kPbSync1);
+  // ---- the rows' merged candidates: records, benefits, screened keys (warp ballots) ----
+  const double theta = sh.theta;
+  {
+    const unsigned lt = entry_tag(tag, layer);
+#pragma unroll 1
+    for (int q0 = warp * 32; q0 < nct; q0 += kConsumers) {
+      const int q = q0 + lane;
+      bool ab = false;
+      unsigned long long key = 0ull;
+      if (q < nct) {
+        const uint2 v = wait_line(P.seg_cand + q, lt, P.err);
+        const int row = q / k, h = q - row * k;
+        const int2 fe = M.fe[row];
+        const float cum = __fmul_rn(M.pc[row], __uint_as_float(v.y));  // Eq.(3)
+        crec[q] = make_int4((int)v.x, (int)v.y, __float_as_int(cum), fe.y);
+        L.cb[q] = cum;  // NODE_SUM: b = cum (Eq.(13) with D = 1)
+        if (h == 0) L.rreq[row] = fe.x;
+        P.cand_adm[lbase + q] = 0;
+        ab = (double)cum > theta;
+        key = sel_key(cum, P.b_off + fe.x, M.slot[row] * k + h);
+      }
+      const unsigned m = __ballot_sync(kFull, ab);
+      if (m) {
+        int pos = 0;
+        if (lane == __ffs(m) - 1) pos = atomicAdd(&sh.n_above, __popc(m));
+        pos = __shfl_sync(kFull, pos, __ffs(m) - 1) + __popc(m & ((1u << lane) - 1u));
+        if (ab && pos < 64) sh.akeys[pos] = key;
+      }
+    }
+  }
+  consumer_sync();
+  stamp(P, tid == 0, 11);
+  if (tid == 0) pb_max(P, layer, kPbMerged);
+  const int nA = sh.n_above, ne = sh.ne;
+  if (theta < 0.0 || nA > 32 || ne > kA5Par) return false;
+
+  if (warp == 0) {
+    const double E0 = sh.E0, th_cut = sh.th_cut, th_arg = sh.th_arg;
+    const long long N0 = sh.N0;
+    const double rhs0 = P.c_T * ((double)P.omega * bc + E0);
+    // ---- A3 + A4 among the screened candidates (lane = one of them) ----
+    const bool own = lane < nA;
+    const unsigned long long key = own ? sh.akeys[lane] : ~0ull;
+    const int r = own ? sel_key_r(key) - P.b_off : 0;
+    const unsigned c = (unsigned)(key & 0xffffu);
+    const int er = __shfl_sync(kFull, e, r);
+    unsigned lt = 0u, same = 0u, clo = 0u;
+#pragma unroll 1
+    for (int j = 0; j < nA; ++j) {
+      const unsigned long long kj = sh.akeys[j];  // broadcast
+      const unsigned bit = 1u << j;
+      lt |= kj < key ? bit : 0u;
+      same |= (((kj ^ key) >> 16) & 0xffffull) == 0ull ? bit : 0u;
+      clo |= (unsigned)(kj & 0xffffu) < c ? bit : 0u;
+    }
+    const bool elig = own && __popc(lt & same) < er;
+    const unsigned Mq = __ballot_sync(kFull, elig);
+    const int g = __popc(lt & Mq);
+    if (elig) L.keys[g] = key;
+    if (lane < bl) sh.a[lane] = 0;
+    __syncwarp();
+    stamp(P, lane == 0, 12);
+    // ---- A5: tile 0 of the block path's scan over the sorted prefix ----
+    const int ns = __popc(Mq);
+    const bool act = lane < ns;
+    const double bj = act ? (double)sel_key_b(L.keys[lane]) : 0.0;
+    double incl = bj;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    double excl = __shfl_up_sync(kFull, incl, 1);
+    if (lane == 0) excl = 0.0;
+    double before = 0.0;
+    before += excl;
+    const int ncut = __popc(__ballot_sync(kFull, act && bj > th_cut));
+    const int narg = __popc(__ballot_sync(kFull, act && bj > th_arg));
+    bool pass;
+    if (P.selection == SMART_FROZEN) {
+      pass = (L.ctab[0] > 0.0) ? (ac * bj * L.ctab[0] > rhs0 * L.dtab[0]) : (bj > 0.0);
+    } else {
+      const double C = L.ctab[lane];
+      pass = (C > 0.0) ? (ac * bj * C > (rhs0 + P.c_T * before) * L.dtab[lane]) : (bj > 0.0);
+    }
+    const unsigned fail = __ballot_sync(kFull, lane < ncut && !pass);
+    const int js = fail ? __ffs(fail) - 1 : ncut;
+    stamp(P, lane == 0, 13);
+    // ---- A6: per-request admits, next-frontier counts / offsets, entries, the flag ----
+    const bool adm = elig && g < js;
+    const unsigned A = __ballot_sync(kFull, adm);
+    const int idx = __popc(same & clo & A);  // canonical order within the request
+    if (adm) sh.a[r] = __popc(same & A);
+    __syncwarp();
+    const int a = lane < bl ? sh.a[lane] : 0;
+    const bool fcond = st.fin || a == 0 || st.nd + a >= P.B;  // Alg.1 line 10
+    const int nx = (lane < bl && !fcond) ? a : 0;
+    int inx = nx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, inx, o);
+      if (lane >= o) inx += u;
+    }
+    const int base = inx - nx, tot = __shfl_sync(kFull, inx, 31);
+    const int basr = __shfl_sync(kFull, base, r), ndr = __shfl_sync(kFull, st.nd, r);
+    const int nxr = __shfl_sync(kFull, nx, r), offr = __shfl_sync(kFull, st.off, r);
+    stamp(P, lane == 0, 17);
+    const int node = ndr + 1 + idx;
+    const float bf = own ? sel_key_b(key) : 0.f;
+    if (adm && nxr > 0) {
+      const int pos = basr + idx;
+      pub.entry(pos, r, node);
+      Mn.fe[pos] = make_int2(r, node);  // the next layer's rows, kept in shared memory
+      Mn.pc[pos] = bf;                  // NODE_SUM: b == cum
+      Mn.slot[pos] = idx;
+      P.fr[npar][pos] = make_int2(r, node);
+      P.fr_cum[npar][pos] = bf;
+    }
+    __syncwarp();
+    stamp(P, lane == 0, 18);
+    if (lane == 0) pub(tot);
+    stamp(P, lane == 0, 19);
+    // ---- after the flag: node records, per-request state, E, trace ----
+    if (lane < bl) P.fr_off[npar][lane] = base;
+    if (lane == 0) *P.fr_total[npar] = tot;
+    if (adm) {
+      const int q = offr * k + (int)c;
+      const int4 rec = crec[q];
+      const size_t o = (size_t)r * T + node;
+      P.tok[o] = rec.x;
+      P.parent[o] = rec.w;
+      P.depth[o] = layer;
+      P.p[o] = __int_as_float(rec.y);
+      P.cum[o] = __int_as_float(rec.z);
+      P.cand_node[lbase + q] = node;
+      P.cand_adm[lbase + q] = 1;
+      L.cslot[r * L.wf + idx] = bf;
+    }
+    __syncwarp();
+    if (lane < bl) {
+      if (a > 0) {
+        double esum = 0.0;  // canonical order
+#pragma unroll 1
+        for (int u = 0; u < a; ++u) esum += (double)L.cslot[lane * L.wf + u];
+        st.E += esum;  // node sum (Q11)
+        P.E_r[lane] = st.E;
+      }
+      const bool fnew = fcond && st.cnt > 0;
+      if (fnew) P.finished[lane] = 1;
+      P.n_nodes[lane] = st.nd + 1 + a;
+      P.fr_cnt[npar][lane] = nx;
+      st.fin = st.fin || fnew;
+      st.nd += a;
+      st.cnt = nx;
+      st.off = base;
+    }
+    double Ea = lane < bl ? st.E : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Ea += __shfl_xor_sync(kFull, Ea, o);
+    // argmax_j S_j over the prefixes up to narg (block path's association and tie rule): final
+    // when narg == ne or the window is convex (th_arg > 0), else the full list (small_trace_full)
+    auto sp = [&](double E, int j) {  // b*S at N0 + j (window)
+      const double C = L.ctab[j];
+      return C > 0.0 ? P.c_T * ((double)P.omega * bc + E) / C : 0.0;
+    };
+    double bestS = sp(E0, 0);
+    int bestj = 0;
+    if (lane < narg) {
+      const double Sa = sp(E0 + before + bj, lane + 1);
+      if (Sa > bestS) {
+        bestS = Sa;
+        bestj = lane + 1;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_xor_sync(kFull, bestS, o);
+      const int oj = __shfl_xor_sync(kFull, bestj, o);
+      if (os > bestS || (os == bestS && oj < bestj)) {
+        bestS = os;
+        bestj = oj;
+      }
+    }
+    const bool full = narg < ne && !(th_arg > 0.0);
+    if (lane == 0) {
+      DevTrace& tr = P.trace[layer - 1];
+      tr.S_after = sp(Ea, js) / bc;
+      *P.N_glob = (int)(N0 + js);
+      *P.E_glob = Ea;
+      tr.executed = R > 0 ? 1 : 0;
+      tr.n_rows = R;
+      tr.n_cand = nct;
+      tr.n_elig = ne;
+      tr.n_admit = js;
+      tr.argmax_j = bestj;
+      tr.N0 = (int)N0;
+      tr.E0 = E0;
+      tr.S0 = sp(E0, 0) / bc;
+      tr.dc0 = L.dtab[0];
+      tr.saturated = (N0 + ne >= P.sat_from) ? 1 : 0;
+      if (tr.saturated) atomicOr(P.err, kErrSaturated);
+      tr.select_path = full ? 2 : 1;
+      tr.n_screened = nA;
+      sh.need_full = full ? 1 : 0;
+    }
+    stamp(P, lane == 0, 22);
+  }
+  consumer_sync();
+  if (sh.need_full) {
+    // the full sorted eligible list for argmax_j (rare): A3 inputs of this layer from the rows
+    if (warp == 0 && lane < bl) L.base[lane] = eb;
+    for (int rr = tid; rr < bl; rr += kConsumers) {
+      L.cnt[rr] = 0;
+      L.off[rr] = R;
+    }
+    consumer_sync();
+    for (int row = tid; row < R; row += kConsumers) {
+      const int rq = L.rreq[row];
+      atomicAdd(&L.cnt[rq], 1);
+      atomicMin(&L.off[rq], row);
+    }
+    consumer_sync();
+    small_trace_full(P, dsm, sh, nct, ne, sh.E0, bc);
+    if (tid == 0) P.trace[layer - 1].argmax_j = sh.bestj;
+  }
+  stamp(P, tid == 0, 16);
+  return true;
+}
+
 template <bool BF16>
 __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const int32_t* root_tok,
                             const int32_t* root_pos, const StepOut& out, bool verify, unsigned tag) {
@@ -444,6 +904,8 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   const int S = P.step_S, k = P.k, cpr = P.cpr, kp = list_stride(k), T = P.T, bl = P.b_loc;
   const int rows_cap = P.cap_rows > bl ? P.cap_rows : bl;
   MergeLayout M = merge_layout(dsm + a16(sel_bytes), rows_cap);
+  // the small path's row descriptors by layer parity (select_small writes the next layer's)
+  const MergeLayout Mb[2] = {M, merge_layout(dsm + a16(sel_bytes) + merge_bytes(rows_cap), rows_cap)};
 
   // ---- begin step: S_0 = A_0 = {root} for every request ----
   for (int r = tid; r < bl; r += kConsumers) {
@@ -478,6 +940,16 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     *P.E_glob = 0.0;
   }
   consumer_sync();
+  // small batches: select_small with the per-request state in warp 0's registers
+  const bool small = P.nranks == 1 && bl <= 32 && P.accept_model == SMART_NODE_SUM &&
+                     (P.selection == SMART_PREFIX || P.selection == SMART_FROZEN) && P.debug_mode != 7;
+  __shared__ SmallShared ssm;
+  SmallState st;
+  st.cnt = lane < bl ? 1 : 0;
+  st.off = lane;
+  st.nd = st.fin = 0;
+  st.E = 0.0;
+  bool rows_in_smem = false;  // layer 1: the roots, from the global frontier written above
 
   for (int layer = 1; layer <= P.d; ++layer) {
     const int par = (layer - 1) & 1;
@@ -485,7 +957,9 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     if (R == 0) break;
     const int t = team_size(R, S, cpr);
     const size_t lbase = (size_t)(layer - 1) * P.cap_rows * k;
+    bool staged = false;  // select_small fell back with the records staged
     auto wait_merge = [&](SelLayout& L, int4* crec) -> bool {
+      if (staged) return true;
       // row descriptors (this CTA's own writes) while the rows stream
       for (int row = tid; row < R; row += kConsumers) {
         const int2 fe = P.fr[par][row];
@@ -508,7 +982,24 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
       if (tid == 0) pb_max(P, layer, kPbMerged);
       return true;
     };
-    select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, StepPub{&P, tag, layer});
+    bool done = false;
+    if (small) {
+      done = select_small(P, layer, R, dsm, Mb[layer & 1], Mb[(layer + 1) & 1], rows_in_smem, st, ssm, tag,
+                          StepPub{&P, tag, layer});
+      staged = !done;  // records and row requests are staged for the generic selection
+      rows_in_smem = done;
+    }
+    if (!done) {
+      select_layer<kConsumers>(P, layer, kSelFull, dsm, wait_merge, StepPub{&P, tag, layer});
+      if (small) {
+        consumer_sync();
+        if (tid == 0) {
+          P.trace[layer - 1].select_path = 3;
+          P.trace[layer - 1].n_screened = ssm.n_above;
+        }
+        if (warp == 0) small_state_load(P, layer & 1, lane, st);
+      }
+    }
     if (tid == 0) pb_max(P, layer, kPbPublished);
     consumer_sync();
     // inspection copies (smart_get_candidates) after the frontier is out: the candidate records
@@ -518,12 +1009,13 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
       const int4* crec = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(L.E) + sel_align((size_t)bl * 8) +
                                                        2 * (size_t)P.sort_cap * 8);
       int4* gc = reinterpret_cast<int4*>(P.cand + lbase);
+      const MergeLayout& Mc = small ? Mb[layer & 1] : M;  // this layer's row descriptors
       for (int q = tid; q < R * k; q += kConsumers) {
         gc[q] = crec[q];
         P.cand_b[lbase + q] = L.cb[q];
       }
       for (int row = tid; row < R; row += kConsumers)
-        P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(M.fe[row].x, M.slot[row]);
+        P.cand_rs[(size_t)(layer - 1) * P.cap_rows + row] = make_int2(Mc.fe[row].x, Mc.slot[row]);
     }
     consumer_sync();  // the scratch is reused by the next layer's selection / the final phase
     if (tid == 0) pb_max(P, layer, kPbSelDone);
@@ -720,7 +1212,7 @@ size_t step_stream_smem_bytes() { return (size_t)kStages * kChunkBytes + sizeof(
 
 size_t step_select_smem_bytes(const Params& P, int S, size_t sel_bytes) {
   const int rows_cap = P.cap_rows > P.b_loc ? P.cap_rows : P.b_loc;
-  const size_t sel = a16(sel_bytes) + merge_bytes(rows_cap);
+  const size_t sel = a16(sel_bytes) + 2 * merge_bytes(rows_cap);
   const size_t fin = a16((size_t)(2 * P.b_loc + 2) * 4) + (size_t)5 * P.b_loc * P.T * 4;
   return sel > fin ? sel : fin;
 }
@@ -751,6 +1243,7 @@ int step_grid(const Params& P, size_t sel_bytes, size_t* smem_out) {
       cudaGetLastError();
       return 0;
     }
+    if (const char* o = getenv("SMART_STEP_OCC")) occ = std::max(1, std::min(occ, atoi(o)));  // experiments only
     grid = std::min(nsm * occ, kStepMaxGrid);
     const size_t need = std::max(step_stream_smem_bytes(), step_select_smem_bytes(P, grid - 1, sel_bytes));
     if (need <= smem) break;

@@ -62,7 +62,8 @@ class _Sizes(C.Structure):
 class _LayerTrace(C.Structure):
     _fields_ = [("executed", C.c_int32), ("n_rows", C.c_int32), ("n_cand", C.c_int32),
                 ("n_elig", C.c_int32), ("n_admit", C.c_int32), ("argmax_j", C.c_int32),
-                ("N0", C.c_int32), ("saturated", C.c_int32), ("E0", C.c_double), ("S0", C.c_double),
+                ("N0", C.c_int32), ("saturated", C.c_int32), ("select_path", C.c_int32),
+                ("n_screened", C.c_int32), ("E0", C.c_double), ("S0", C.c_double),
                 ("S_after", C.c_double), ("dc0", C.c_double)]
 
 

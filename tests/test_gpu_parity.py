@@ -174,6 +174,37 @@ def test_run_step_equals_separate_calls():
         np.testing.assert_array_equal(a[key], b[key])
 
 
+# ---- the step kernel's small-batch selection (select_small) and its hand-overs:
+# each case is compared with the oracle on both paths (_run) and the step kernel's per-layer
+# select_path trace shows the branch taken: 1 the one-warp threshold path, 2 the same with the full
+# sorted list rebuilt for argmax_j (non-convex cost window), 3 handed over to the block selection
+# (more than 64 candidates above the threshold / a long eligible list, or theta unusable) -------
+
+SMALL = {
+    "convex_cfg3like": (Case(V=30000, k=8, d=5, W=8, b=32, B_verify=200, seed=90, a_lo=8.0, a_hi=14.0, sigma_m=0.5,
+                             cost=(0.0117, 0.0, 0.05, 0.02, 1.3, 2.4631, 2.4631)), {1}),
+    "concave_cost": (Case(V=30000, k=6, d=5, W=6, b=8, B_verify=96, seed=48, a_lo=6.0, a_hi=12.0, sigma_m=0.5,
+                          cost=(0.001, 0.0, 0.2, 0.05, 0.7, 1.5, 1.0)), {2}),
+    "many_above": (Case(V=20000, k=8, d=4, W=8, b=32, B_verify=2048, seed=60,
+                        cost=(0.0001, 0.0, 0.0, 0.0, 1.0, 1.0, 1.0)), {3}),  # 63-77 admitted per layer
+    "omega0_node_sum": (Case(V=30000, k=5, d=5, W=5, b=6, B_verify=60, omega=0, seed=72, a_lo=6.0, a_hi=12.0,
+                             sigma_m=0.5, cost=(0.01, 0.0, 0.05, 0.02, 1.2, 1.5, 1.0)), {3}),
+}
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_small_selection_paths(name):
+    case, want = SMALL[name]
+    orc, gpu, layers = _run(case)
+    assert sum(1 for l in range(case.d) if orc.trace[l, 3] > 0) >= 2, "the case must admit in >= 2 layers"
+    T = _T(case)
+    draft, target, rt, rp = make_inputs(case, T)
+    step = run_gpu(case, draft, target, rt, rp, use_run_step=True)
+    paths = [step["stats"]["layers"][l]["select_path"] for l in range(case.d) if step["stats"]["layers"][l]["executed"]]
+    assert want & set(paths), paths
+    assert set(paths) <= {1, 2, 3}, paths
+
+
 # ---- BASELINE.json configs at full size ------------------------------------------------------
 
 FULL = {

@@ -39,6 +39,7 @@ mn = lambda l, sl: (~np.uint64(g(l, sl))) if g(l, sl) else 0
 t0 = int(mn(0, 3))
 f = lambda v: f"{(int(v) - t0) / 1e3:7.2f}" if v else "   -   "
 print("rows per layer", rows, "nodes", st["nodes_local"], "err", st["error_flags"])
+print("select path per layer", [st["layers"][l]["select_path"] for l in range(len(rows))], "screened", [st["layers"][l]["n_screened"] for l in range(len(rows))], "admitted", [st["layers"][l]["n_admit"] for l in range(len(rows))], "eligible", [st["layers"][l]["n_elig"] for l in range(len(rows))])
 print("layer | flag seen min/max | 1st chunk min/max | 1st consumed | posted | slice end max | arrived | sync1 | staged | merged | published | sel done")
 for l in range(1, wl["d"] + 1):
     print(f"{l:5d} | {f(mn(l,3))} {f(g(l,4))} | {f(mn(l,6))} {f(g(l,7))} | {f(g(l,11))} | {f(g(l,12))} | {f(g(l,5))} | {f(g(l,0))} | {f(g(l,9))} | {f(g(l,10))} | {f(g(l,1))} | {f(g(l,2))} | {f(g(l,8))}")
@@ -53,7 +54,11 @@ names = {9: "start", 10: "benefits", 11: "req-rank", 12: "sort", 13: "A5 cut", 1
 for l in range(1, wl["d"] + 1):
     c = {j: int(buf[3000 + l * 16 + (j - 9)]) for j in range(9, 23)}
     base = c[9]
-    print(f"layer {l} select phases (cycles from start):", ", ".join(f"{names[j]} {c[j]-base}" for j in (10, 11, 12, 13, 15, 16, 20, 21, 17, 18, 19, 14, 22) if c[j]))
+    if st["layers"][l - 1]["select_path"] in (1, 2):
+        sn = {10: "rows", 11: "polled", 12: "A3/A4", 13: "A5 cut", 17: "counts", 18: "entries", 19: "flag", 22: "trace", 16: "end"}
+        print(f"layer {l} select_small phases (cycles from start):", ", ".join(f"{sn[j]} {c[j]-base}" for j in (10, 11, 12, 13, 17, 18, 19, 22, 16) if c[j]))
+    else:
+        print(f"layer {l} select phases (cycles from start):", ", ".join(f"{names[j]} {c[j]-base}" for j in (10, 11, 12, 13, 15, 16, 20, 21, 17, 18, 19, 14, 22) if c[j]))
 pc = []
 for sidx in range(4096 // 4 - 256):
     a, b_, c_, m = (int(buf[1024 + 4 * sidx + j]) for j in range(4))

@@ -1,118 +1,73 @@
-// latency microbenchmark (debug aid): one warp, dependent chains of common ops
+// Dependent-chain latencies of the warp-level operations the selection / merge code is built
+// from (one warp, or 8 warps for bar.sync), in SM cycles (clock64).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/ubench/lat.cu -o /tmp/lat
 #include <cstdio>
-#include <cuda_runtime.h>
-__global__ void k(unsigned long long* out, int n, const unsigned long long* g) {
-  __shared__ unsigned long long s[1024];
+
+constexpr int N = 256;
+
+template <int OP>
+__global__ void chain(unsigned* out, long long* cyc, unsigned seed) {
+  __shared__ unsigned sm[1024];
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s[i] = (i * 7 + 3) & 1023;
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) sm[i] = (i * 7 + 3) & 1023;
   __syncthreads();
-  if (threadIdx.x >= 32) return;
-  unsigned long long t0, t1;
-  // (a) dependent LDS chain
-  unsigned long long x = lane;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) x = s[x & 1023];
-  t1 = clock64();
-  if (lane == 0) out[0] = (t1 - t0) / n;
-  // (b) independent LDS, 2 accumulators
-  int r0 = 0, r1 = 0;
-  unsigned long long key = s[lane] + x;
-  t0 = clock64();
-  for (int i = 0; i + 1 < n; i += 2) {
-    r0 += s[i & 1023] > key;
-    r1 += s[(i + 1) & 1023] > key;
-  }
-  t1 = clock64();
-  if (lane == 0) out[1] = (t1 - t0) / n + (r0 + r1 == 12345);
-  // (c) dependent SHFL
-  int v = lane + (int)x;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) v = __shfl_sync(0xffffffffu, v, (v + i) & 31);
-  t1 = clock64();
-  if (lane == 0) out[2] = (t1 - t0) / n + (v == 12345);
-  // (d) dependent VOTE+POPC
-  int w = lane + (int)x;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) w += __popc(__ballot_sync(0xffffffffu, (w & 1)));
-  t1 = clock64();
-  if (lane == 0) out[3] = (t1 - t0) / n + (w == 12345);
-  // (e) dependent REDUX
-  unsigned u = lane + (unsigned)x;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) u = __reduce_max_sync(0xffffffffu, u + lane);
-  t1 = clock64();
-  if (lane == 0) out[4] = (t1 - t0) / n + (u == 12345);
-  // (f) dependent IADD chain
-  int a = lane + (int)x;
-  t0 = clock64();
+  unsigned v = seed + lane;
+  double d = (double)v;
+  float f = (float)v;
+  long long t0 = clock64();
 #pragma unroll 1
-  for (int i = 0; i < n; ++i) a = a * 3 + i;
-  t1 = clock64();
-  if (lane == 0) out[5] = (t1 - t0) / n + (a == 12345);
-  // (g) dependent global load chain (L2/L1)
-  unsigned long long y = lane;
-  t0 = clock64();
-  for (int i = 0; i < 64; ++i) y = __ldcg(&g[y & 4095]);
-  t1 = clock64();
-  if (lane == 0) out[6] = (t1 - t0) / 64 + (y == 12345);
-  // (h) double add chain
-  double d = lane;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) d = d * 1.0000001 + 0.5;
-  t1 = clock64();
-  if (lane == 0) out[7] = (t1 - t0) / n + (d == 12345.0);
-  // (i) double shfl
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) d = __shfl_xor_sync(0xffffffffu, d, 1) + 1.0;
-  t1 = clock64();
-  if (lane == 0) out[8] = (t1 - t0) / n + (d == 12345.0);
-  // (j) named barrier with 1 warp
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) asm volatile("bar.sync 1, 32;");
-  t1 = clock64();
-  if (lane == 0) out[9] = (t1 - t0) / n;
-  // (k) clock64 overhead
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) { unsigned long long c = clock64(); a += (int)c; }
-  t1 = clock64();
-  if (lane == 0) out[10] = (t1 - t0) / n + (a == 12345);
-  // (l) double division chain
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) d = 3.0 / (d + 1.0);
-  t1 = clock64();
-  if (lane == 0) out[11] = (t1 - t0) / n + (d == 12345.0);
-  // (m) float division chain
-  float f = lane + 1.f;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) f = 3.f / (f + 1.f);
-  t1 = clock64();
-  if (lane == 0) out[12] = (t1 - t0) / n + (f == 12345.f);
-  // (n) smem atomicOr
-  __shared__ unsigned bm[64];
-  if (lane < 64) bm[lane] = 0;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) atomicOr(&bm[(lane + i) & 63], 1u << (i & 31));
-  t1 = clock64();
-  if (lane == 0) out[13] = (t1 - t0) / n;
-  // (o) F2F f32->f64 + DMUL dep
-  float q = lane;
-  t0 = clock64();
-  for (int i = 0; i < n; ++i) q = (float)((double)q * 1.0000001);
-  t1 = clock64();
-  if (lane == 0) out[14] = (t1 - t0) / n + (q == 12345.f);
+  for (int i = 0; i < N; ++i) {
+    if (OP == 0) v = __shfl_xor_sync(0xffffffffu, v, 1) + 1u;
+    if (OP == 1) v = __reduce_min_sync(0xffffffffu, v) + lane;
+    if (OP == 2) v = __ballot_sync(0xffffffffu, v & 1u) + lane;
+    if (OP == 3) v = sm[v & 1023];
+    if (OP == 4) { asm volatile("bar.sync 1, 256;" ::: "memory"); v += 1; }
+    if (OP == 5) f = f * 1.0001f + 1.0f;
+    if (OP == 6) d = d * 1.0001 + 1.0;
+    if (OP == 7) v = __match_any_sync(0xffffffffu, v & 3u) + lane;
+    if (OP == 8) v = (unsigned)__shfl_sync(0xffffffffu, (int)v, v & 31) + 1u;
+    if (OP == 9) { unsigned r; asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=r"(r) : "f"(__uint_as_float(v))); v = r + lane; }
+    if (OP == 10) v = __popc(__ballot_sync(0xffffffffu, v & 1u)) + v;
+    if (OP == 11) { __syncwarp(); v += 1; }
+    if (OP == 12) v = (unsigned)__shfl_up_sync(0xffffffffu, (int)v, 1) + 1u;
+    if (OP == 13) d = __shfl_xor_sync(0xffffffffu, d, 1) + 1.0;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  out[threadIdx.x] = v + (unsigned)f + (unsigned)d;
 }
+
+template <int OP>
+void run(const char* name, int threads) {
+  unsigned* o;
+  long long* c;
+  cudaMalloc(&o, 4096);
+  cudaMalloc(&c, 8);
+  long long h = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    chain<OP><<<1, threads>>>(o, c, 5u);
+    cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  }
+  printf("%-28s %6.1f cycles per dependent step\n", name, (double)h / N);
+  cudaFree(o);
+  cudaFree(c);
+}
+
 int main() {
-  unsigned long long *o, *g, h[16] = {};
-  cudaMalloc(&o, 16 * 8);
-  cudaMalloc(&g, 4096 * 8);
-  unsigned long long hg[4096];
-  for (int i = 0; i < 4096; ++i) hg[i] = (i * 131 + 7) & 4095;
-  cudaMemcpy(g, hg, sizeof hg, cudaMemcpyHostToDevice);
-  for (int rep = 0; rep < 3; ++rep) k<<<1, 288>>>(o, 256, g);
-  cudaDeviceSynchronize();
-  cudaMemcpy(h, o, 16 * 8, cudaMemcpyDeviceToHost);
-  const char* nm[] = {"LDS dep", "LDS indep/elem", "SHFL dep", "VOTE+POPC dep", "REDUX dep", "IMAD dep",
-                      "LDG.cg dep (L2)", "DFMA dep", "SHFL.f64+DADD dep", "BAR 1 warp", "CS2R clock", "DDIV dep", "FDIV dep", "ATOMS.OR", "F2F+DMUL+F2F dep"};
-  for (int i = 0; i < 15; ++i) printf("%-22s %llu cycles\n", nm[i], h[i]);
+  run<0>("shfl.bfly u32 + iadd", 32);
+  run<12>("shfl.up u32 + iadd", 32);
+  run<8>("shfl.idx (var src) + iadd", 32);
+  run<13>("shfl.bfly f64 + dadd", 32);
+  run<1>("redux.min u32 + iadd", 32);
+  run<9>("redux.max f32 + iadd", 32);
+  run<2>("vote.ballot + iadd", 32);
+  run<10>("ballot + popc + iadd", 32);
+  run<7>("match.any + iadd", 32);
+  run<3>("lds (pointer chase)", 32);
+  run<11>("syncwarp + iadd", 32);
+  run<4>("bar.sync 8 warps", 256);
+  run<5>("ffma", 32);
+  run<6>("dfma", 32);
+  printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
