@@ -32,7 +32,7 @@ struct smart_ctx {
   smart_cost cost;
   int device = 0;
   int num_sms = 0;
-  int grid_expand = 0, grid_verify = 0;
+  int grid_expand = 0, grid_verify = 0, grid_verify_sample = 0;
   size_t select_smem = 0;
   bool fused_select = true;  // selection runs in the layer kernel's last CTA
   bool no_early = false;     // SMART_NO_EARLY=1: every layer kernel waits for the previous grid
@@ -415,6 +415,7 @@ smart_status smart_create(const smart_config* cfg, const smart_cost* cost, int d
   // launch geometry: persistent streaming grids sized to the SM count
   c->grid_expand = expand_grid(P.cpr, P.k);
   c->grid_verify = c->num_sms * verify_occupancy();
+  c->grid_verify_sample = c->num_sms * verify_occupancy(true);
   // selection: fused into the layer kernel when its scratch fits the stream ring, else the
   // standalone 1024-thread select kernel
   long long elig_cap = b * frontier_width(&c->cfg, P.B, T);
@@ -759,7 +760,7 @@ smart_status smart_verify_sample(smart_ctx* c, const void* d_target, int64_t ld,
   const long long ld_bytes = (long long)ld * c->P.esz;
   const bool tma = ((reinterpret_cast<uintptr_t>(d_target) & 15) == 0) && (ld_bytes % 16 == 0) &&
                    (((long long)c->P.V * c->P.esz) % 16 == 0);
-  launch_verify(c->P, d_target, ld_bytes, tma, d_accept_len, d_accept_path, d_bonus, c->grid_verify, s, true,
+  launch_verify(c->P, d_target, ld_bytes, tma, d_accept_len, d_accept_path, d_bonus, c->grid_verify_sample, s, true,
                 (float)(1.0 / temperature), (unsigned long long)seed);
   CUDA_TRY(c, cudaGetLastError());
   c->last_stream = s;

@@ -464,7 +464,7 @@ static void verify_attr(int sm) {
                        cudaSharedmemCarveoutMaxShared);
 }
 
-int verify_occupancy() {
+int verify_occupancy(bool sample) {
   int n = 0;
   const int sm = (int)verify_smem_bytes(1024);
   verify_attr<true, true, false>(sm);
@@ -475,8 +475,13 @@ int verify_occupancy() {
   verify_attr<true, false, true>(sm);
   verify_attr<false, true, true>(sm);
   verify_attr<false, false, true>(sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true, false>, kLayerThreads,
-                                                verify_smem_bytes(1024));
+  // the T > 0 kernel holds more registers: its own occupancy sizes its grid (no second wave)
+  if (sample)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true, true>, kLayerThreads,
+                                                  verify_smem_bytes(1024));
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, verify_kernel<true, true, false>, kLayerThreads,
+                                                  verify_smem_bytes(1024));
   return n > 0 ? n : 1;
 }
 

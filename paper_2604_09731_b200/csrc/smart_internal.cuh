@@ -363,7 +363,7 @@ void launch_verify(const Params& P, const void* target, long long ld_bytes, bool
 size_t verify_smem_bytes(int T);
 size_t walk_smem_bytes(int T);
 cudaError_t walk_set_smem_bytes(size_t bytes);
-int verify_occupancy();
+int verify_occupancy(bool sample = false);
 cudaError_t mask_set_smem_bytes(size_t bytes);
 size_t mask_smem_bytes(int T, int b);
 struct StepOut {
