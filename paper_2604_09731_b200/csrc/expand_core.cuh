@@ -103,6 +103,8 @@ __device__ __forceinline__ void load_direct(const char* row, int chunk_base, int
 struct WarpTopk {
   unsigned long long buf[kSegBuf];  // candidates of the current row slice (appended; compacted)
   unsigned long long list[kMaxK];   // compacted top-k, sorted best first
+  int cnt;                          // append cursor of the owner-lane expansion
+  int pad[3];
 };
 
 // consumer-side shared state of a streaming CTA
@@ -279,7 +281,50 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
   float bv = bound ? tk_val(bound) : -INFINITY;
   CSTAMP(5 + 8 * (c - mlo));
   CCOUNT(0, 1);
-  if (__any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
+  bool done = false;
+  if (TMA && __any_sync(kFull, m >= bv)) {
+    // owner-lane expansion: a lane re-reads its qualifying vectors from the still-held stage and
+    // marks the elements reaching the bound; the candidates are appended at positions from a
+    // warp-local shared cursor (the buffer is compacted by rank later, so order is irrelevant)
+    CCOUNT(1, 1);
+    uint32_t cm = 0u;
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      if (vm[j] >= bv) {
+        const uint4 q = reinterpret_cast<const uint4*>(stage)[j * kConsumers + tid];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) {
+          const float xv = BF16 ? __uint_as_float((e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16))
+                                : __uint_as_float(w[e]);
+          if (xv >= bv && elem_index<BF16>(cbase, tid, j * EPV + e) < V) cm |= 1u << (j * EPV + e);
+        }
+      }
+    }
+    const int n = __popc(cm);
+    const int tot = __reduce_add_sync(kFull, (unsigned)n);
+    if (wcnt + tot <= kSegBuf) {
+      if (lane == 0) W.cnt = wcnt;
+      __syncwarp();
+      if (n) {
+        int pos = atomicAdd(&W.cnt, n);
+        while (cm) {
+          const int b = __ffs(cm) - 1;
+          cm &= cm - 1u;
+          const int j = b / EPV, e = b % EPV;
+          const uint4 q = reinterpret_cast<const uint4*>(stage)[j * kConsumers + tid];
+          const uint32_t wv = (BF16 ? e >> 1 : e) == 0 ? q.x : (BF16 ? e >> 1 : e) == 1 ? q.y : (BF16 ? e >> 1 : e) == 2 ? q.z : q.w;
+          const float xv = BF16 ? __uint_as_float((e & 1) ? (wv & 0xffff0000u) : (wv << 16)) : __uint_as_float(wv);
+          W.buf[pos++] = tk_key(xv, elem_index<BF16>(cbase, tid, b));
+        }
+      }
+      __syncwarp();
+      wcnt += tot;
+      CCOUNT(2, tot);
+      done = true;
+    }
+  }
+  if (!done && __any_sync(kFull, m >= bv)) {  // most chunks of a long slice have no candidate at all
     CCOUNT(1, 1);
     // vectors whose max reaches the bound are expanded cooperatively: each group of EPV lanes
     // takes one such vector (its elements re-read from the still-held ring stage), compares them
@@ -369,11 +414,22 @@ __device__ __forceinline__ void slice_end_merge(const ConsShared& sh, const floa
     const unsigned long long key = sh.cl[tid];
     const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(sh.cl);
     int r0 = 0, r1 = 0;
+    if (k <= kConsumerWarps) {
+      // k <= 8: at most 64 entries, all 32 broadcast loads issued back to back (no loop-carried
+      // latency), the padding beyond nl never counted
+#pragma unroll
+      for (int f = 0; f < kConsumerWarps * kConsumerWarps / 2; ++f) {
+        const ulonglong2 v = c2[f];
+        r0 += (2 * f < nl && v.x > key);
+        r1 += (2 * f + 1 < nl && v.y > key);
+      }
+    } else {
 #pragma unroll 4
-    for (int f = 0; f < nl / 2; ++f) {
-      const ulonglong2 v = c2[f];
-      r0 += (v.x > key);
-      r1 += (v.y > key);
+      for (int f = 0; f < nl / 2; ++f) {
+        const ulonglong2 v = c2[f];
+        r0 += (v.x > key);
+        r1 += (v.y > key);
+      }
     }
     const int rank = r0 + r1;
     if (rank < k) out_key(rank, key);

@@ -469,10 +469,10 @@ struct SmallState {  // lane r of warp 0: request r's state before the layer
 };
 struct SmallShared {
   double theta, E0, th_cut, th_arg;
-  long long N0;
+  long long N0, N0next;
   int ne, n_above, need_full, bestj;
   int a[32];
-  unsigned long long akeys[64];
+  __align__(16) unsigned long long akeys[64];
 };
 
 __device__ __forceinline__ void small_state_load(const Params& P, int par, int lane, SmallState& st) {
@@ -583,9 +583,29 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
   int4* const crec = reinterpret_cast<int4*>(L.keys + 2 * (size_t)P.sort_cap);
   const int bc = (P.cost_scope == SMART_COST_LOCAL) ? bl : P.b_glob;
   const double ac = P.alpha * P.c_T;
+  // the frontier buffers of this layer (par) and the next (npar), selected without indexing the
+  // kernel parameter arrays by a runtime value (that copies them to local memory)
+  int2* const fr_p = par ? P.fr[1] : P.fr[0];
+  float* const frc_p = par ? P.fr_cum[1] : P.fr_cum[0];
+  int* const fro_p = par ? P.fr_off[1] : P.fr_off[0];
+  int2* const fr_n = npar ? P.fr[1] : P.fr[0];
+  float* const frc_n = npar ? P.fr_cum[1] : P.fr_cum[0];
+  int* const fro_n = npar ? P.fr_off[1] : P.fr_off[0];
+  int* const frn_n = npar ? P.fr_cnt[1] : P.fr_cnt[0];
+  int* const frt_n = npar ? P.fr_total[1] : P.fr_total[0];
   stamp(P, tid == 0, 9);
-  // ---- before the candidates: A3 budgets (lane r), N0, E0, the cost window, theta and the
-  // argmax threshold (warp 0); the rows' descriptors (from the last layer's shared copy) ----
+  // ---- before the candidates: the cost window from N0 (all threads, one round of loads); A3
+  // budgets (lane r), E0, theta and the argmax threshold (warp 0); the rows' descriptors ----
+  {
+    const long long N0w = sh.N0next;  // drafted nodes before the layer (the last layer's N0 + js)
+    const int ncw = min(nct, P.sort_cap) + 2;
+    for (int j = tid; j < ncw; j += kConsumers) {
+      const long long N = min(N0w + j, (long long)P.n_cost - 1);
+      L.ctab[j] = P.cost_tab[N];
+      L.dtab[j] = P.dc_tab[N];
+    }
+  }
+  consumer_sync();
   int e = 0, eb = 0;
   if (warp == 0) {
     if (lane < bl) {
@@ -616,15 +636,11 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
     bool ok = ac > 0.0 && P.c_T >= 0.0 && rhs0 >= 0.0;
 #pragma unroll 1
     for (int j = lane; j < ncw; j += 32) {
-      const long long N = min(N0 + j, (long long)P.n_cost - 1);
-      const double C = P.cost_tab[N], dcj = P.dc_tab[N];
-      L.ctab[j] = C;
-      L.dtab[j] = dcj;
+      const double C = L.ctab[j], dcj = L.dtab[j];
       const double tj = C > 0.0 ? rhs0 * dcj * __drcp_rn(ac * C) : 0.0;
       ok = ok && dcj >= 0.0 && tj == tj;
       th = fmin(th, tj);
     }
-    __syncwarp();  // the window written by the other lanes
     // argmax threshold: on a convex window (dC nondecreasing over prefix lengths 0..ne+1) with
     // sorted benefits, S_j is unimodal (S_{j+1} lies between S_j and b_j / dC_j), and a step can
     // raise S only if b_j > s_j dC_j >= s_0 min dC (s = S / c_T): every benefit <= th2 = s_0 min dC
@@ -658,10 +674,10 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
   }
   if (!rows_in_smem) {  // after a block-path layer: the rows from its global frontier
     for (int row = tid; row < R; row += kConsumers) {
-      const int2 fe = P.fr[par][row];
+      const int2 fe = fr_p[row];
       M.fe[row] = fe;
-      M.pc[row] = P.fr_cum[par][row];
-      M.slot[row] = row - P.fr_off[par][fe.x];
+      M.pc[row] = frc_p[row];
+      M.slot[row] = row - fro_p[fe.x];
     }
   }
   consumer_sync();
@@ -702,6 +718,8 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
   if (tid == 0) pb_max(P, layer, kPbMerged);
   const int nA = sh.n_above, ne = sh.ne;
   if (theta < 0.0 || nA > 32 || ne > kA5Par) return false;
+  if (warp == 0 && lane >= nA && lane < ((nA + 3) & ~3)) sh.akeys[lane] = ~0ull;  // padding for the 4-wide loop
+  __syncwarp();
 
   if (warp == 0) {
     const double E0 = sh.E0, th_cut = sh.th_cut, th_arg = sh.th_arg;
@@ -714,13 +732,21 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
     const unsigned c = (unsigned)(key & 0xffffu);
     const int er = __shfl_sync(kFull, e, r);
     unsigned lt = 0u, same = 0u, clo = 0u;
+    // four screened keys per step (two 16-byte broadcast loads issued together); the padding
+    // keys ~0 beyond nA (written with the screen) are never better, same-request or lower-index
+    const ulonglong2* ak2 = reinterpret_cast<const ulonglong2*>(sh.akeys);
 #pragma unroll 1
-    for (int j = 0; j < nA; ++j) {
-      const unsigned long long kj = sh.akeys[j];  // broadcast
-      const unsigned bit = 1u << j;
-      lt |= kj < key ? bit : 0u;
-      same |= (((kj ^ key) >> 16) & 0xffffull) == 0ull ? bit : 0u;
-      clo |= (unsigned)(kj & 0xffffu) < c ? bit : 0u;
+    for (int j0 = 0; j0 < nA; j0 += 4) {
+      const ulonglong2 p0 = ak2[j0 >> 1], p1 = ak2[(j0 >> 1) + 1];
+      const unsigned long long kq[4] = {p0.x, p0.y, p1.x, p1.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned long long kj = kq[u];
+        const unsigned bit = 1u << (j0 + u);
+        lt |= kj < key ? bit : 0u;
+        same |= (((kj ^ key) >> 16) & 0xffffull) == 0ull ? bit : 0u;
+        clo |= (unsigned)(kj & 0xffffu) < c ? bit : 0u;
+      }
     }
     const bool elig = own && __popc(lt & same) < er;
     const unsigned Mq = __ballot_sync(kFull, elig);
@@ -782,16 +808,16 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       Mn.fe[pos] = make_int2(r, node);  // the next layer's rows, kept in shared memory
       Mn.pc[pos] = bf;                  // NODE_SUM: b == cum
       Mn.slot[pos] = idx;
-      P.fr[npar][pos] = make_int2(r, node);
-      P.fr_cum[npar][pos] = bf;
+      fr_n[pos] = make_int2(r, node);
+      frc_n[pos] = bf;
     }
     __syncwarp();
     stamp(P, lane == 0, 18);
     if (lane == 0) pub(tot);
     stamp(P, lane == 0, 19);
     // ---- after the flag: node records, per-request state, E, trace ----
-    if (lane < bl) P.fr_off[npar][lane] = base;
-    if (lane == 0) *P.fr_total[npar] = tot;
+    if (lane < bl) fro_n[lane] = base;
+    if (lane == 0) *frt_n = tot;
     if (adm) {
       const int q = offr * k + (int)c;
       const int4 rec = crec[q];
@@ -817,7 +843,7 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       const bool fnew = fcond && st.cnt > 0;
       if (fnew) P.finished[lane] = 1;
       P.n_nodes[lane] = st.nd + 1 + a;
-      P.fr_cnt[npar][lane] = nx;
+      frn_n[lane] = nx;
       st.fin = st.fin || fnew;
       st.nd += a;
       st.cnt = nx;
@@ -870,6 +896,7 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       if (tr.saturated) atomicOr(P.err, kErrSaturated);
       tr.select_path = full ? 2 : 1;
       tr.n_screened = nA;
+      sh.N0next = N0 + js;
       sh.need_full = full ? 1 : 0;
     }
     stamp(P, lane == 0, 22);
@@ -950,6 +977,8 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   st.nd = st.fin = 0;
   st.E = 0.0;
   bool rows_in_smem = false;  // layer 1: the roots, from the global frontier written above
+  if (tid == 0) ssm.N0next = 0;
+  consumer_sync();
 
   for (int layer = 1; layer <= P.d; ++layer) {
     const int par = (layer - 1) & 1;
@@ -998,6 +1027,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
           P.trace[layer - 1].n_screened = ssm.n_above;
         }
         if (warp == 0) small_state_load(P, layer & 1, lane, st);
+        if (tid == 0) ssm.N0next = *P.N_glob;
       }
     }
     if (tid == 0) pb_max(P, layer, kPbPublished);
