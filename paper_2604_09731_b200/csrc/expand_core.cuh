@@ -546,11 +546,18 @@ __device__ __forceinline__ bool merge_row_tournament(int k, int cpr, int t, floa
   const float rZ = __frcp_rn(Z);  // correctly rounded 1/Z (no division slow path)
   unsigned long long mine = 0ull;  // lane r keeps the r-th best key
   for (int r = 0; r < k; ++r) {
-    const unsigned hi = __reduce_max_sync(kFull, (unsigned)(cur >> 32));
-    const unsigned lo = __reduce_max_sync(kFull, (unsigned)(cur >> 32) == hi ? (unsigned)cur : 0u);
-    const unsigned long long win = ((unsigned long long)hi << 32) | lo;
+    // one warp max on the value word; the low (index) word only when values tie (rare)
+    const unsigned hv = (unsigned)(cur >> 32);
+    const unsigned hi = __reduce_max_sync(kFull, hv);
+    unsigned bal = __ballot_sync(kFull, hv == hi);
+    if (bal & (bal - 1u)) {
+      const unsigned lo = __reduce_max_sync(kFull, hv == hi ? (unsigned)cur : 0u);
+      bal = __ballot_sync(kFull, hv == hi && (unsigned)cur == lo);
+    }
+    const int wl = __ffs(bal) - 1;  // keys are distinct: exactly one winner
+    const unsigned long long win = ((unsigned long long)hi << 32) | (unsigned)__shfl_sync(kFull, (unsigned)cur, wl);
     mine = lane == r ? win : mine;
-    const bool adv = own && cur == win;  // keys are distinct: exactly one lane advances
+    const bool adv = lane == wl;
     cur = adv ? nxt : cur;
     h += adv ? 1 : 0;
     unsigned long long ld;

@@ -182,7 +182,7 @@ struct StepPub {
 // "max" slots keep the latest time, "min" slots the complement of the earliest (atomicMax of ~t)
 enum { kPbArrived = 0, kPbMerged = 1, kPbPublished = 2, kPbFlagMin = 3, kPbFlagMax = 4, kPbSliceMax = 5,
        kPbChunkMin = 6, kPbChunkMax = 7, kPbSelDone = 8, kPbSync1 = 9, kPbStaged = 10, kPbConsumed1 = 11,
-       kPbPosted = 12 };
+       kPbPosted = 12, kPbTeamIn = 13, kPbTeamOut = 14 };
 __device__ __forceinline__ unsigned smid_reg() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -203,7 +203,7 @@ __device__ __forceinline__ void pb_min(const Params& P, int layer, int slot) {
 // from its own frontier.  Rows merge in parallel on their teams instead of one after another on
 // the selection CTA.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int row, int t, unsigned lt) {
+__device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int row, int t, unsigned lt, int layer) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const int k = P.k, kp = list_stride(k), cpr = P.cpr;
   const int nkl = t * k, nl = nkl + cpr;
@@ -221,7 +221,36 @@ __device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int 
     }
   }
   consumer_sync();
-  if (warp == 0) {
+  if (tid == 0) pb_max(P, layer, kPbTeamIn);  // all lists in (latest row)
+  if (P.debug_mode == 8) {  // experiment: every key ranked among all t lists in parallel
+    const int lane = tid & 31;
+    const float2 v0 = lane < cpr ? mm[lane] : make_float2(-INFINITY, 0.f);
+    const float2 v1 = lane + 32 < cpr ? mm[lane + 32] : make_float2(-INFINITY, 0.f);
+    const float M = warp_max_fast(fmaxf(v0.x, v1.x));
+    const float ML = M * kLog2e;
+    float z = 0.f;
+    z += (v0.y != 0.f || isnan(v0.y)) ? v0.y * ex2(fmaf(v0.x, kLog2e, -ML)) : 0.f;
+    z += (v1.y != 0.f || isnan(v1.y)) ? v1.y * ex2(fmaf(v1.x, kLog2e, -ML)) : 0.f;
+    const float rZ = __frcp_rn(warp_sum(z));
+    if (k & 1)
+      for (int m = tid; m < t; m += kConsumers) mk[m * kp + k] = 0ull;
+    consumer_sync();
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(mk);
+    uint4* gc = P.seg_cand + (size_t)row * k;
+    for (int e = tid; e < t * k; e += kConsumers) {
+      const int m = e / k, i = e - m * k;
+      const unsigned long long key = mk[m * kp + i];
+      int r0 = 0, r1 = 0;
+#pragma unroll 8
+      for (int f = 0; f < t * kp / 2; ++f) {
+        const ulonglong2 v = k2[f];
+        r0 += v.x > key;
+        r1 += v.y > key;
+      }
+      if (r0 + r1 < k)
+        st_line(gc + r0 + r1, (unsigned)tk_idx(key), __float_as_uint(ex2(fmaf(tk_val(key), kLog2e, -ML)) * rZ), lt);
+    }
+  } else if (warp == 0) {
     uint4* gc = P.seg_cand + (size_t)row * k;
     const bool ok = merge_row_tournament(
         k, cpr, t, 1.f,
@@ -233,6 +262,7 @@ __device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int 
     if (!ok && (tid & 31) == 0) atomicOr(P.err, kErrDraftNaN);  // Q23
   }
   consumer_sync();  // the warp buffers are the next slice's again
+  if (tid == 0) pb_max(P, layer, kPbTeamOut);  // row candidates out (latest row)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -363,7 +393,7 @@ __device__ void stream_role(const Params& P, char* dsm, const char* __restrict__
           pb_max(P, layer, kPbSliceMax);
           sh.cs.tau = 0ull;  // next slice (read only after the next slice's first barrier)
         }
-        if (member == 0) team_merge(P, sh, row, t, lt);
+        if (member == 0) team_merge(P, sh, row, t, lt, layer);
       }
     }
     R = wait_event(sh, ev++);

@@ -40,9 +40,9 @@ t0 = int(mn(0, 3))
 f = lambda v: f"{(int(v) - t0) / 1e3:7.2f}" if v else "   -   "
 print("rows per layer", rows, "nodes", st["nodes_local"], "err", st["error_flags"])
 print("select path per layer", [st["layers"][l]["select_path"] for l in range(len(rows))], "screened", [st["layers"][l]["n_screened"] for l in range(len(rows))], "admitted", [st["layers"][l]["n_admit"] for l in range(len(rows))], "eligible", [st["layers"][l]["n_elig"] for l in range(len(rows))])
-print("layer | flag seen min/max | 1st chunk min/max | 1st consumed | posted | slice end max | arrived | sync1 | staged | merged | published | sel done")
+print("layer | flag seen min/max | 1st chunk min/max | 1st consumed | posted | slice end max | team lists in | team out | sync1 | merged | published | sel done")
 for l in range(1, wl["d"] + 1):
-    print(f"{l:5d} | {f(mn(l,3))} {f(g(l,4))} | {f(mn(l,6))} {f(g(l,7))} | {f(g(l,11))} | {f(g(l,12))} | {f(g(l,5))} | {f(g(l,0))} | {f(g(l,9))} | {f(g(l,10))} | {f(g(l,1))} | {f(g(l,2))} | {f(g(l,8))}")
+    print(f"{l:5d} | {f(mn(l,3))} {f(g(l,4))} | {f(mn(l,6))} {f(g(l,7))} | {f(g(l,11))} | {f(g(l,12))} | {f(g(l,5))} | {f(g(l,13))} | {f(g(l,14))} | {f(g(l,9))} | {f(g(l,1))} | {f(g(l,2))} | {f(g(l,8))}")
 v = 17
 print(f"verify: published {f(g(v,2))} flag seen {f(mn(v,3))}-{f(g(v,4))} mask done {f(g(v,1))} slices end {f(g(v,5))} arrived {f(g(v,0))}")
 print(f"kernel end {f(g(0,8))} us")
