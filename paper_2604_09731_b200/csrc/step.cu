@@ -222,35 +222,7 @@ __device__ __forceinline__ void team_merge(const Params& P, StepShared& sh, int 
   }
   consumer_sync();
   if (tid == 0) pb_max(P, layer, kPbTeamIn);  // all lists in (latest row)
-  if (P.debug_mode == 8) {  // experiment: every key ranked among all t lists in parallel
-    const int lane = tid & 31;
-    const float2 v0 = lane < cpr ? mm[lane] : make_float2(-INFINITY, 0.f);
-    const float2 v1 = lane + 32 < cpr ? mm[lane + 32] : make_float2(-INFINITY, 0.f);
-    const float M = warp_max_fast(fmaxf(v0.x, v1.x));
-    const float ML = M * kLog2e;
-    float z = 0.f;
-    z += (v0.y != 0.f || isnan(v0.y)) ? v0.y * ex2(fmaf(v0.x, kLog2e, -ML)) : 0.f;
-    z += (v1.y != 0.f || isnan(v1.y)) ? v1.y * ex2(fmaf(v1.x, kLog2e, -ML)) : 0.f;
-    const float rZ = __frcp_rn(warp_sum(z));
-    if (k & 1)
-      for (int m = tid; m < t; m += kConsumers) mk[m * kp + k] = 0ull;
-    consumer_sync();
-    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(mk);
-    uint4* gc = P.seg_cand + (size_t)row * k;
-    for (int e = tid; e < t * k; e += kConsumers) {
-      const int m = e / k, i = e - m * k;
-      const unsigned long long key = mk[m * kp + i];
-      int r0 = 0, r1 = 0;
-#pragma unroll 8
-      for (int f = 0; f < t * kp / 2; ++f) {
-        const ulonglong2 v = k2[f];
-        r0 += v.x > key;
-        r1 += v.y > key;
-      }
-      if (r0 + r1 < k)
-        st_line(gc + r0 + r1, (unsigned)tk_idx(key), __float_as_uint(ex2(fmaf(tk_val(key), kLog2e, -ML)) * rZ), lt);
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
     uint4* gc = P.seg_cand + (size_t)row * k;
     const bool ok = merge_row_tournament(
         k, cpr, t, 1.f,
