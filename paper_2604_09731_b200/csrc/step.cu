@@ -799,6 +799,9 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       if (lane >= o) inx += u;
     }
     const int base = inx - nx, tot = __shfl_sync(kFull, inx, 31);
+    // the row count first: the streaming CTAs take their team layout from it and then poll their
+    // rows' self-validating entries, which follow
+    if (lane == 0) pub(tot);
     const int basr = __shfl_sync(kFull, base, r), ndr = __shfl_sync(kFull, st.nd, r);
     const int nxr = __shfl_sync(kFull, nx, r), offr = __shfl_sync(kFull, st.off, r);
     stamp(P, lane == 0, 17);
@@ -815,7 +818,6 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
     }
     __syncwarp();
     stamp(P, lane == 0, 18);
-    if (lane == 0) pub(tot);
     stamp(P, lane == 0, 19);
     // ---- after the flag: node records, per-request state, E, trace ----
     if (lane < bl) fro_n[lane] = base;
