@@ -278,6 +278,10 @@ __device__ __forceinline__ void consume_chunk(const Params& P, ConsShared& sh, f
     const unsigned long long tt = *reinterpret_cast<volatile unsigned long long*>(&sh.tau);
     if (tt > bound) bound = tt;
   }
+  if (CONSUME_EXPERIMENT == 4) {  // ubench only: an oracle-quality bound from the first chunk on
+    const unsigned long long b9 = ((unsigned long long)float_orderable(9.0f) << 32) | 0x80000000ull;
+    if (b9 > bound) bound = b9;
+  }
   float bv = bound ? tk_val(bound) : -INFINITY;
   CSTAMP(5 + 8 * (c - mlo));
   CCOUNT(0, 1);
