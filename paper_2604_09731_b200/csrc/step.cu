@@ -639,21 +639,24 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
 #pragma unroll 1
     for (int j = lane; j < ncw; j += 32) {
       const double C = L.ctab[j], dcj = L.dtab[j];
-      const double tj = C > 0.0 ? rhs0 * dcj * __drcp_rn(ac * C) : 0.0;
+      // a float reciprocal (rel. error < 1e-7; the 1e-5 margin below covers it): a
+        // correctly rounded fp64 one is a ~30-instruction call per entry
+        const double tj = C > 0.0 ? rhs0 * dcj * (double)__frcp_rn((float)(ac * C)) : 0.0;
       ok = ok && dcj >= 0.0 && tj == tj;
       th = fmin(th, tj);
     }
     // argmax threshold: on a convex window (dC nondecreasing over prefix lengths 0..ne+1) with
     // sorted benefits, S_j is unimodal (S_{j+1} lies between S_j and b_j / dC_j), and a step can
     // raise S only if b_j > s_j dC_j >= s_0 min dC (s = S / c_T): every benefit <= th2 = s_0 min dC
-    // ends the rise for good; 1e-9 below keeps the computed S of later prefixes under the maximum
+    // ends the rise for good; 1e-6 below keeps the computed S of later prefixes under the maximum
+    // (the convexity test allows 1e-9 of rounding in dC: exactly linear costs qualify)
     bool cvx = L.ctab[0] > 0.0;
     double dmin = INFINITY;
 #pragma unroll 1
     for (int j = lane; j <= ne; j += 32) {
       const double d0 = L.ctab[j + 1] - L.ctab[j];
       dmin = fmin(dmin, d0);
-      if (j + 1 <= ne) cvx = cvx && (L.ctab[j + 2] - L.ctab[j + 1]) >= d0;
+      if (j + 1 <= ne) cvx = cvx && (L.ctab[j + 2] - L.ctab[j + 1]) >= d0 - 1e-9 * fabs(d0);  // convex up to rounding
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -663,8 +666,8 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
     ok = __all_sync(kFull, ok) && th > 0.0 && th < INFINITY;
     cvx = __all_sync(kFull, cvx) && dmin > 0.0 && dmin < INFINITY;
     if (lane == 0) {
-      const double thc = ok ? th * (1.0 - 1e-12) : -1.0;
-      const double th2 = cvx ? ((double)P.omega * bc + Ev) / L.ctab[0] * dmin * (1.0 - 1e-9) : -1.0;
+      const double thc = ok ? th * (1.0 - 1e-5) : -1.0;
+      const double th2 = cvx ? ((double)P.omega * bc + Ev) / L.ctab[0] * dmin * (1.0 - 1e-6) : -1.0;
       sh.th_cut = thc;
       sh.th_arg = th2;
       sh.theta = (thc >= 0.0 && th2 > 0.0) ? fmin(thc, th2) : thc;  // the screening threshold

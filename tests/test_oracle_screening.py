@@ -17,7 +17,7 @@ import numpy as np
 from inputs import synth
 
 
-def _instance(orc, rng, concave=False):
+def _instance(orc, rng, concave=False, linear=False):
     b = int(rng.integers(1, 6))
     k = int(rng.integers(2, 7))
     d = int(rng.integers(2, 6))
@@ -26,7 +26,7 @@ def _instance(orc, rng, concave=False):
                      alpha=float(rng.choice([0.6, 0.8, 1.0])), omega=int(rng.integers(0, 2)),
                      selection=int(rng.integers(0, 2)), accept_model=orc.NODE_SUM,
                      marginal=int(rng.integers(0, 2)), dtype=orc.FP32)
-    cost = orc.Cost(lam=float(rng.uniform(0.005, 0.2)), gamma=float(rng.uniform(0, 0.3)),
+    cost = orc.Cost(lam=float(rng.uniform(0.005, 0.2)), gamma=0.0 if linear else float(rng.uniform(0, 0.3)),
                     delta=float(rng.uniform(0.005, 0.1)),
                     rho=float(rng.uniform(0.4, 0.9) if concave else rng.uniform(1.0, 1.6)),
                     eta=float(rng.uniform(0.5, 2.0)) if cfg.omega else 0.0, c_T=1.0)
@@ -85,8 +85,8 @@ def test_admitted_benefits_exceed_theta(orc):
 def test_argmax_within_th2_prefix_on_convex_windows(orc):
     rng = np.random.default_rng(7)
     certified = 0
-    for it in range(120):
-        cfg, cost, pool = _instance(orc, rng, concave=False)
+    for it in range(160):
+        cfg, cost, pool = _instance(orc, rng, concave=False, linear=it % 4 == 0)  # linear: convex up to rounding
         res = orc.step(cfg, cost, pool)
         for l in range(1, cfg.d + 1):
             if not res.trace[l - 1, 12]:
@@ -94,9 +94,9 @@ def test_argmax_within_th2_prefix_on_convex_windows(orc):
             cands = res.layer_cands(l)
             N0, E0, ne, C, dc = _layer_terms(orc, cfg, cost, res, l)
             dC = np.diff(C[: ne + 2])
-            if not (C[0] > 0 and np.all(np.diff(dC) >= 0) and dC.min() > 0):
+            if not (C[0] > 0 and np.all(np.diff(dC) >= -1e-9 * np.abs(dC[:-1])) and dC.min() > 0):
                 continue
-            th2 = (cfg.omega * cfg.b + E0) / C[0] * dC.min() * (1 - 1e-9)
+            th2 = (cfg.omega * cfg.b + E0) / C[0] * dC.min() * (1 - 1e-6)
             elig = _eligible(orc, cfg, res, l, cands)
             bs = np.sort(cands["b"][elig])[::-1]
             narg = int(np.sum(bs > th2))

@@ -22,11 +22,11 @@ cfg = S.Config(vocab=wl["V"], top_k=wl["k"], max_depth=wl["d"], max_frontier=wl[
                budget_verify=wl["B_verify"], alpha=0.8, bonus=1, logits_dtype=S.BF16, row_mode=S.ROWS_NODE)
 ctx = S.Smart(cfg, cost)
 T = ctx.sizes["T"]
-d, tg, rt, rp = bench.make_set(0, wl, T, 0)
+d, tg, rt, rp = bench.make_set(0, wl, T, wl["b"], 0)
 dd = bench.bf16_dev(d, torch.device("cuda"))
 L = S.lib()
 L.smart_debug_probes.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
-buf = np.zeros(1024, np.uint64)
+buf = np.zeros(4096, np.uint64)
 for rep in range(3):
     ctx.begin_step()
     for layer in range(1, 4):
@@ -39,5 +39,5 @@ for rep in range(3):
         st = [int(buf[32 + j]) for j in range(32)]
         dd_ = lambda a, b: st[b] - st[a] if st[a] and st[b] else None
         if rep == 2:
-            print(f"layer {layer}: stage", dd_(9, 10), "elig+rank", dd_(10, 11), "sort", dd_(11, 12), "rule", dd_(12, 13),
+            print(f"layer {layer}: theta(w1)", dd_(9, 20), "pre-B2(t0)", dd_(9, 21), "stage", dd_(9, 10), "elig+rank", dd_(10, 11), "sort", dd_(11, 12), "rule", dd_(12, 13),
                   "commit", dd_(13, 14), "tail", dd_(14, 22), "trace", ctx.stats()["layers"][layer - 1])

@@ -27,7 +27,7 @@ tt = bench.bf16_dev(tg, dev)
 out = ctx.alloc_outputs()
 L = S.lib()
 L.smart_debug_probes.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
-buf = np.zeros(1024, np.uint64)
+buf = np.zeros(4096, np.uint64)
 s = torch.cuda.Stream()
 
 
