@@ -1155,12 +1155,25 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   }
   consumer_sync();
   if (tid == 0) pb_max(P, kVerifySlot, kPbArrived);
+  // every node, in parallel: the target's argmax token and the child holding it (-1: none; the
+  // children of a node are contiguous in canonical order, sibling tokens distinct), so that the
+  // walk below is a chain of single loads
   for (int e = tid; e < bl * T; e += kConsumers) {
-    const int r = e / T;
-    if (e - r * T < s_n[r]) {
+    const int r = e / T, u = e - r * T, n = s_n[r];
+    if (u < n) {
       unsigned long long* slot = P.vbest + e;
-      s_arg[e] = (int)(0xffffffffu - (uint32_t)__ldcg(slot));
+      const int tgt = (int)(0xffffffffu - (uint32_t)__ldcg(slot));
       *slot = 0ull;  // cleared for the next step
+      s_arg[e] = tgt;
+      const int* sp = s_par + (size_t)r * T;
+      const int* stk = s_tok + (size_t)r * T;
+      int nx = -1;
+      for (int j = s_fc[e]; j >= 0 && j < n && sp[j] == u; ++j)
+        if (stk[j] == tgt) {
+          nx = j;
+          break;
+        }
+      s_fc[e] = nx;  // (this thread's own entry: read above, not read by any other thread)
     }
   }
   consumer_sync();
@@ -1169,21 +1182,13 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   unsigned long long accs = 0ull, nods = 0ull;
   for (int r = tid; r < bl; r += kConsumers) {
     const int n = s_n[r];
-    const int* sp = s_par + (size_t)r * T;
-    const int* st = s_tok + (size_t)r * T;
     const int* sa = s_arg + (size_t)r * T;
     const int* fc = s_fc + (size_t)r * T;
     int cur = 0, acc = 0, bon = -1;
     for (;;) {  // follow the child holding the target's argmax token, else stop
-      const int tgt = sa[cur];
-      int found = -1;
-      for (int j = fc[cur]; j >= 0 && j < n && sp[j] == cur; ++j)
-        if (st[j] == tgt) {
-          found = j;
-          break;
-        }
+      const int found = fc[cur];  // that child, found above
       if (found < 0) {
-        bon = tgt;
+        bon = sa[cur];
         break;
       }
       if (out.accept_path && acc < D) out.accept_path[(size_t)r * D + acc] = found;
