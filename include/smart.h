@@ -181,6 +181,26 @@ smart_status smart_attach_exchange(smart_ctx* ctx, int rank, int nranks, void* d
 smart_status smart_select_finish(smart_ctx* ctx, int32_t layer, int32_t* d_frontier,
                                  int32_t* d_frontier_count, void* stream);
 
+/* Peer exchange (NEXT #4; the per-layer exchange without a collective call).
+ * Every rank owns one receive buffer of smart_peer_exchange_bytes() bytes (device memory,
+ * 256-byte aligned, zeroed once by its owner): nranks records of smart_exchange_record_bytes()
+ * bytes, then one 8-byte tag word per rank.  d_recv_bufs[g] is rank g's buffer as seen from this
+ * process -- the same device pointers in one process, cudaIpcOpenMemHandle mappings across
+ * processes (smart_ipc_get_handle / smart_ipc_open_handle; peer access over NVLink).  After
+ * smart_attach_peer_exchange, smart_select(layer) runs the local phase and writes its record
+ * straight into every rank's buffer (slot `rank`), then the tag word (step counter << 32 | layer)
+ * with release semantics at system scope; smart_select_finish(layer) polls the nranks tag words of
+ * its own buffer (acquire; a sticky SMART_EDEVICE timeout flag instead of a hang) and runs the
+ * global phase.  Decisions are the same bits as with the all-gather.  smart_run_step drives both
+ * halves per layer (on separate GPUs; ranks sharing one GPU must call them in lockstep, all local
+ * phases before any finish).  Sharding as for smart_attach_exchange. */
+smart_status smart_peer_exchange_bytes(const smart_config* cfg, int nranks, int64_t* bytes);
+smart_status smart_attach_peer_exchange(smart_ctx* ctx, int rank, int nranks, void* const* d_recv_bufs);
+/* CUDA IPC of a device allocation: 64-byte handle out, mapping in (this process), unmapping. */
+smart_status smart_ipc_get_handle(void* d_ptr, uint8_t handle[64]);
+smart_status smart_ipc_open_handle(const uint8_t handle[64], void** d_ptr);
+smart_status smart_ipc_close(void* d_ptr);
+
 smart_status smart_destroy(smart_ctx* ctx);
 
 /* ---- one decode step -------------------------------------------------------------------- */

@@ -56,6 +56,10 @@ struct smart_ctx {
   void* nccl_comm = nullptr;
   bool byo_exchange = false;
   bool owns_exchange = false;
+  // peer exchange (smart_attach_peer_exchange): own send record + device table of receive buffers
+  bool peer_exchange = false;
+  char* peer_xs = nullptr;
+  char** peer_tab = nullptr;
 };
 
 namespace {
@@ -603,10 +607,72 @@ smart_status smart_attach_exchange(smart_ctx* c, int rank, int nranks, void* d_s
   return setup_exchange(c, rank, nranks, d_send, d_recv);
 }
 
+smart_status smart_peer_exchange_bytes(const smart_config* cfg, int nranks, int64_t* bytes) {
+  int64_t rec = 0;
+  smart_status st = smart_exchange_record_bytes(cfg, nranks, &rec);
+  if (st) return st;
+  *bytes = rec * nranks + ((8ll * nranks + 255) & ~255ll);  // records, then one tag word per rank
+  return SMART_OK;
+}
+
+smart_status smart_attach_peer_exchange(smart_ctx* c, int rank, int nranks, void* const* d_recv_bufs) {
+  if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
+  if (!d_recv_bufs) return fail(c, SMART_EINVAL, "null receive-buffer table");
+  for (int g = 0; g < nranks; ++g)
+    if (!d_recv_bufs[g] || (reinterpret_cast<uintptr_t>(d_recv_bufs[g]) & 255))
+      return fail(c, SMART_EINVAL, "receive buffer %d null or not 256-byte aligned", g);
+  smart_status st = check_sharding(c, rank, nranks);
+  if (st) return st;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!c->peer_xs) {
+    int64_t rec = 0;
+    st = smart_exchange_record_bytes(&c->cfg, nranks, &rec);
+    if (st) return st;
+    CUDA_TRY(c, cudaMalloc(&c->peer_xs, (size_t)rec));
+  }
+  st = setup_exchange(c, rank, nranks, c->peer_xs, d_recv_bufs[rank]);
+  if (st) return st;
+  if (c->peer_tab) cudaFree(c->peer_tab);
+  CUDA_TRY(c, cudaMalloc(&c->peer_tab, sizeof(char*) * nranks));
+  CUDA_TRY(c, cudaMemcpy(c->peer_tab, d_recv_bufs, sizeof(char*) * nranks, cudaMemcpyHostToDevice));
+  c->P.xpeer = c->peer_tab;
+  c->P.xtag_off = c->P.xstride * nranks;
+  c->byo_exchange = true;
+  c->peer_exchange = true;
+  return SMART_OK;
+}
+
+smart_status smart_ipc_get_handle(void* d_ptr, uint8_t handle[64]) {
+  if (!d_ptr || !handle) return fail(nullptr, SMART_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, d_ptr);
+  if (e != cudaSuccess) return fail(nullptr, SMART_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle, &h, 64);
+  return SMART_OK;
+}
+
+smart_status smart_ipc_open_handle(const uint8_t handle[64], void** d_ptr) {
+  if (!d_ptr || !handle) return fail(nullptr, SMART_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(nullptr, SMART_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  return SMART_OK;
+}
+
+smart_status smart_ipc_close(void* d_ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  if (e != cudaSuccess) return fail(nullptr, SMART_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return SMART_OK;
+}
+
 smart_status smart_destroy(smart_ctx* c) {
   if (!c) return SMART_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  if (c->peer_xs) cudaFree(c->peer_xs);
+  if (c->peer_tab) cudaFree(c->peer_tab);
   if (c->nccl_comm && g_nccl.h) g_nccl.CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   if (c->owns_exchange) {
     cudaFree(c->P.xs);
@@ -623,6 +689,7 @@ smart_status smart_begin_step(smart_ctx* c, const int32_t* d_root_tok, const int
   int thr = 256, grid = (c->P.b_loc + thr - 1) / thr;
   launch_k(begin_step_kernel, dim3(grid), dim3(thr), 0, s, c->P, d_root_tok, d_root_pos);
   CUDA_TRY(c, cudaGetLastError());
+  ++c->P.xepoch;  // the peer-exchange tags of this step
   c->next_layer = 1;
   c->phase = 0;
   c->masked = false;
@@ -662,8 +729,9 @@ smart_status smart_select(smart_ctx* c, int32_t layer, int32_t* d_frontier, int3
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (c->byo_exchange && c->P.nranks > 1) {
     launch_select(c->P, layer, 1 /* kSelLocal */, c->select_smem, s);
+    if (c->peer_exchange) launch_peer_push(c->P, layer, s);  // the record into every rank's buffer
     CUDA_TRY(c, cudaGetLastError());
-    c->phase = 2;  // awaiting smart_select_finish after the caller's all-gather
+    c->phase = 2;  // awaiting smart_select_finish (after the caller's all-gather, or the peer pushes)
     c->last_stream = s;
     return SMART_OK;
   }
@@ -693,6 +761,7 @@ smart_status smart_select_finish(smart_ctx* c, int32_t layer, int32_t* d_frontie
   if (layer != c->next_layer || c->phase != 2)
     return fail(c, SMART_ESTATE, "select_finish layer %d out of order", layer);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->peer_exchange) launch_peer_wait(c->P, layer, s);  // every rank's record has landed
   launch_select(c->P, layer, 2 /* kSelGlobal */, c->select_smem, s);
   CUDA_TRY(c, cudaGetLastError());
   if (d_frontier || d_frontier_count) launch_export_frontier(c->P, layer & 1, d_frontier, d_frontier_count, s);
@@ -774,7 +843,8 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
   if (!c) return fail(nullptr, SMART_EINVAL, "null ctx");
   if (c->cfg.row_mode == SMART_ROWS_FRONTIER)
     return fail(c, SMART_EINVAL, "smart_run_step needs row_mode NODE or POSITION (pre-filled pools)");
-  if (c->byo_exchange) return fail(c, SMART_ESTATE, "smart_run_step cannot drive a caller-provided exchange");
+  if (c->byo_exchange && !c->peer_exchange)
+    return fail(c, SMART_ESTATE, "smart_run_step cannot drive a caller-provided exchange");
   if (!d_draft) return fail(c, SMART_EINVAL, "null draft logits");
   if (ld < c->cfg.vocab || (d_target && ld_t < c->cfg.vocab)) return fail(c, SMART_EINVAL, "ld < vocab");
   if (c->step_grid > 0 && c->P.nranks <= 1) {
@@ -804,6 +874,7 @@ smart_status smart_run_step(smart_ctx* c, const int32_t* d_root_tok, const int32
   for (int l = 1; !st && l <= c->cfg.max_depth; ++l) {
     st = smart_expand_step(c, l, d_draft, ld, stream);
     if (!st) st = smart_select(c, l, nullptr, nullptr, stream);
+    if (!st && c->phase == 2) st = smart_select_finish(c, l, nullptr, nullptr, stream);  // peer exchange
   }
   c->in_run_step = false;
   if (!st) st = smart_build_mask(c, d_mask, d_pos, d_parent, d_tok, d_tree_len, stream);

@@ -56,6 +56,47 @@ cudaError_t select_set_smem(size_t bytes) {
   return cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// ---- peer exchange (NEXT #4): the local phase's record written straight into every
+// rank's receive buffer, then one tag word per (rank -> receiver) with release semantics at system
+// scope; the receiver polls the tags of all ranks (acquire) before its global phase.  Tags carry
+// (step counter << 32 | layer), so a stale record is never accepted and nothing is reset. ----
+__device__ __forceinline__ unsigned long long peer_tag(const Params& P, int layer) {
+  return (P.xepoch << 32) | (unsigned)layer;
+}
+__global__ void __launch_bounds__(256) peer_push_kernel(Params P, int layer) {
+  const int tid = threadIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(P.xs);
+  const int n16 = (int)(P.xstride / 16);
+  for (int g = 0; g < P.nranks; ++g) {
+    uint4* dst = reinterpret_cast<uint4*>(P.xpeer[g] + (size_t)P.rank * P.xstride);
+    for (int i = tid; i < n16; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (tid < P.nranks) {  // release (cumulative over the barrier): the record before the tag
+    unsigned long long* tg = reinterpret_cast<unsigned long long*>(P.xpeer[tid] + P.xtag_off) + P.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(tg), "l"(peer_tag(P, layer)) : "memory");
+  }
+}
+__global__ void __launch_bounds__(32) peer_wait_kernel(Params P, int layer) {
+  const int g = threadIdx.x;
+  if (g < P.nranks) {
+    const unsigned long long* tg = reinterpret_cast<const unsigned long long*>(P.xr + P.xtag_off) + g;
+    const unsigned long long want = peer_tag(P, layer);
+    for (unsigned it = 0;; ++it) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(tg) : "memory");
+      if (v == want) break;
+      if (it > (1u << 24)) {  // a rank that never pushes: sticky flag instead of a hang
+        atomicOr(P.err, kErrTimeout);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+void launch_peer_push(const Params& P, int layer, cudaStream_t s) { peer_push_kernel<<<1, 256, 0, s>>>(P, layer); }
+void launch_peer_wait(const Params& P, int layer, cudaStream_t s) { peer_wait_kernel<<<1, 32, 0, s>>>(P, layer); }
+
 void launch_select(const Params& P, int layer, int mode, size_t smem, cudaStream_t s) {
   launch_k(select_kernel, dim3(1), dim3(kSelectThreads), smem, s, P, layer, mode);
 }

@@ -142,7 +142,12 @@ struct Params {
   int m_cap;
   long long xstride;  // bytes per rank record
   char* xs;           // send record
-  char* xr;           // [nranks] gathered records
+  char* xr;           // [nranks] gathered records (peer exchange: this rank's receive buffer)
+  // peer exchange (smart_attach_peer_exchange): every rank's receive buffer as seen from here, the
+  // byte offset of the per-rank tag words in a receive buffer, and the step counter of the tags
+  char* const* xpeer;
+  long long xtag_off;
+  unsigned long long xepoch;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -349,6 +354,8 @@ void launch_expand(const Params& P, int layer, const void* logits, long long ld_
 size_t layer_smem_bytes(int cpr, int k);
 int expand_grid(int cpr, int k);
 void launch_select(const Params& P, int layer, int phase, size_t smem, cudaStream_t s);
+void launch_peer_push(const Params& P, int layer, cudaStream_t s);
+void launch_peer_wait(const Params& P, int layer, cudaStream_t s);
 size_t select_smem_bytes(int b_loc, int b_all, int sort_cap, int nc_cap, int nranks, int k);
 size_t select_rec_bytes(int nc_cap);
 cudaError_t select_set_smem(size_t bytes);

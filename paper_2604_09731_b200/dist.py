@@ -49,6 +49,25 @@ def broadcast_bytes(payload: bytes | None, src: int = 0, group=None) -> bytes:
     return obj[0]
 
 
+def attach_peer_exchange(ctx, group=None):
+    """The peer exchange (smart_attach_peer_exchange) across the processes of
+    `group`, one per GPU: each rank allocates its receive buffer, the 64-byte CUDA IPC handles are
+    all-gathered through torch.distributed, every rank maps the others' buffers (peer access over
+    NVLink) and attaches the table.  Returns the list of mapped addresses (close with
+    smart.ipc_close) and the owned buffer (keep it alive)."""
+    import torch
+    import torch.distributed as dist
+    from . import smart as S
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = torch.zeros(ctx.peer_exchange_bytes(world), dtype=torch.uint8, device="cuda")
+    handles = [None] * world
+    dist.all_gather_object(handles, S.ipc_handle(buf.data_ptr()), group=group)
+    ptrs = [buf.data_ptr() if g == rank else S.ipc_open(handles[g]) for g in range(world)]
+    ctx.attach_peer_exchange(rank, world, ptrs, keep=buf)
+    dist.barrier(group)  # every buffer zeroed and mapped before the first push
+    return ptrs, buf
+
+
 class ShardedSmart:
     """One rank's share of a sharded decode step (caller-provided all-gather mode)."""
 

@@ -29,6 +29,8 @@ MAX_DEPTH = 16
 
 EXPORTED = ["smart_query_sizes", "smart_create", "smart_nccl_unique_id", "smart_attach_nccl",
             "smart_exchange_record_bytes", "smart_attach_exchange", "smart_select_finish",
+            "smart_peer_exchange_bytes", "smart_attach_peer_exchange", "smart_ipc_get_handle",
+            "smart_ipc_open_handle", "smart_ipc_close",
             "smart_destroy", "smart_begin_step", "smart_expand_step", "smart_select",
             "smart_build_mask", "smart_verify_accept", "smart_verify_sample", "smart_run_step", "smart_get_stats",
             "smart_get_tree", "smart_get_candidates", "smart_last_error", "smart_status_string"]
@@ -95,6 +97,11 @@ def lib() -> C.CDLL:
         L.smart_exchange_record_bytes.argtypes = [C.POINTER(_Config), C.c_int, C.POINTER(i64)]
         L.smart_attach_exchange.argtypes = [vp, C.c_int, C.c_int, vp, vp]
         L.smart_select_finish.argtypes = [vp, i32, vp, vp, vp]
+        L.smart_peer_exchange_bytes.argtypes = [C.POINTER(_Config), C.c_int, C.POINTER(i64)]
+        L.smart_attach_peer_exchange.argtypes = [vp, C.c_int, C.c_int, C.POINTER(vp)]
+        L.smart_ipc_get_handle.argtypes = [vp, C.c_char_p]
+        L.smart_ipc_open_handle.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.smart_ipc_close.argtypes = [vp]
         L.smart_destroy.argtypes = [vp]
         L.smart_begin_step.argtypes = [vp, vp, vp, vp]
         L.smart_expand_step.argtypes = [vp, i32, vp, i64, vp]
@@ -218,6 +225,19 @@ class Smart:
         self._xbufs = (send, recv)  # keep alive
         _check(lib().smart_attach_exchange(self._h, rank, nranks, _ptr(send), _ptr(recv)), self._h)
 
+    def peer_exchange_bytes(self, nranks: int) -> int:
+        n = C.c_int64()
+        c = self.cfg.c()
+        _check(lib().smart_peer_exchange_bytes(C.byref(c), nranks, C.byref(n)))
+        return n.value
+
+    def attach_peer_exchange(self, rank: int, nranks: int, recv_ptrs, keep=None):
+        """peer exchange (smart_attach_peer_exchange): recv_ptrs[g] = rank g's receive buffer (an int
+        device address valid in this process); `keep` holds the owning tensors alive"""
+        self._xbufs = keep
+        arr = (C.c_void_p * nranks)(*[C.c_void_p(int(p)) for p in recv_ptrs])
+        _check(lib().smart_attach_peer_exchange(self._h, rank, nranks, arr), self._h)
+
     def select_finish(self, layer: int, frontier=None, frontier_count=None, stream=None):
         _check(lib().smart_select_finish(self._h, layer, _ptr(frontier), _ptr(frontier_count), _stream(stream)),
                self._h)
@@ -327,3 +347,21 @@ class Smart:
         n = cnt.value
         return dict(r=ints[:n, 0], parent=ints[:n, 1], tok=ints[:n, 2], c=ints[:n, 3],
                     p=fl[:n, 0], cum=fl[:n, 1], b=fl[:n, 2], admitted=adm[:n].astype(bool))
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (smart_ipc_get_handle)."""
+    buf = C.create_string_buffer(64)
+    _check(lib().smart_ipc_get_handle(C.c_void_p(int(dev_ptr)), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation into this one (smart_ipc_open_handle); returns the address."""
+    p = C.c_void_p()
+    _check(lib().smart_ipc_open_handle(C.c_char_p(bytes(handle)), C.byref(p)))
+    return p.value
+
+
+def ipc_close(dev_ptr: int) -> None:
+    _check(lib().smart_ipc_close(C.c_void_p(int(dev_ptr))))
