@@ -145,7 +145,7 @@ def config_dict(args, wl, world):
          "depth": wl["d"], "top_k": wl["k"], "max_frontier": wl["W"], "B_verify": Bv, "alpha": ALPHA,
          "preset": "HOTPATH (PREFIX, NODE_SUM, omega=1)", "cost_fixture": f"fixtures/cost_b200_{fixture_name(args, wl)}.txt",
          "synth": SYNTH, "scaling": args.scaling,
-         "parallelism": f"requests sharded dp{world}" + (", NCCL all-gather per layer in the step graph" if world > 1 else "")}
+         "parallelism": f"requests sharded dp{world}" + ((", peer exchange per layer (IPC-mapped buffers)" if getattr(args, "exchange", "nccl") == "peer" else ", NCCL all-gather per layer in the step graph") if world > 1 else "")}
     return c
 
 
@@ -277,6 +277,9 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: the workload's batch per GPU; strong: the workload's batch split over the GPUs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: the per-layer exchange through the library's NCCL all-gather, or the peer "
+                         "exchange (records stored straight into every rank's IPC-mapped buffer, DESIGN.md §8)")
     ap.add_argument("--cost", default="default", choices=["default", "roofline", "measured"],
                     help="cost-model fixture: the workload's default, the roofline fit, or measured on a B200 (NEXT #2)")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -315,7 +318,11 @@ def main():
     cost = S.Cost(lam=cost_fx["lam"], beta=cost_fx["beta"], gamma=cost_fx["gamma"], delta=cost_fx["delta"],
                   rho=cost_fx["rho"], eta=cost_fx["eta"], c_T=cost_fx["c_T"])
     ctx = S.Smart(cfg, cost, local)
-    if world > 1:
+    if world > 1 and args.exchange == "peer":
+        # the peer exchange: no collective per layer (the end-of-step C2 sums stay per rank)
+        from paper_2604_09731_b200 import dist as D
+        _peer_keep = D.attach_peer_exchange(ctx)
+    elif world > 1:
         # the library's own NCCL communicator: the per-layer all-gather and the end-of-step
         # all-reduce are enqueued on the step's stream, so the sharded step is one CUDA graph
         uid = S.nccl_unique_id() if rank == 0 else None
