@@ -444,9 +444,9 @@ __device__ inline MergeLayout merge_layout(char* p, int rows_cap) {
 // select_small: A3-A6 of one layer for small batches (one rank, <= 32 requests, NODE_SUM, PREFIX
 // or FROZEN) -- the same decisions, node numbering, fp64 associations and trace as select_layer,
 // computed on the few candidates that can matter, in one warp, with the per-request state in
-// registers (lane r of warp 0 holds request r).  The selection CTA runs once per layer, so its
-// code is always cold in the 32 KB instruction cache: this path is short, straight-line code
-// instead of select_layer's generic phases.
+// registers (lane r of warp 0 holds request r).  Every dependent warp collective costs ~30-50
+// cycles and every block barrier ~40 (profiles/r02c_ubench_latency.txt), so this path is a few
+// warp-wide steps instead of select_layer's barrier-separated block phases.
 //  * theta (known before the layer's candidates arrive): Eq.(16) admits the candidate at sorted
 //    position j only if alpha c_T b_j C(N0+j) > (rhs0 + c_T before_j) dc(N0+j) with before_j >= 0,
 //    so every admitted candidate has b > theta = min_j rhs0 dc(N0+j) / (alpha c_T C(N0+j))
