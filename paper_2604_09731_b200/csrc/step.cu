@@ -723,8 +723,6 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
   if (tid == 0) pb_max(P, layer, kPbMerged);
   const int nA = sh.n_above, ne = sh.ne;
   if (theta < 0.0 || nA > 32 || ne > kA5Par) return false;
-  if (warp == 0 && lane >= nA && lane < ((nA + 3) & ~3)) sh.akeys[lane] = ~0ull;  // padding for the 4-wide loop
-  __syncwarp();
 
   if (warp == 0) {
     const double E0 = sh.E0, th_cut = sh.th_cut, th_arg = sh.th_arg;
@@ -737,22 +735,25 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
     const unsigned c = (unsigned)(key & 0xffffu);
     const int er = __shfl_sync(kFull, e, r);
     unsigned lt = 0u, same = 0u, clo = 0u;
-    // four screened keys per step (two 16-byte broadcast loads issued together); the padding
-    // keys ~0 beyond nA (written with the screen) are never better, same-request or lower-index
+    // all 32 key slots in one unrolled pass: the 16 broadcast 16-byte loads issue back to back,
+    // the slots at or beyond nA masked off
     const ulonglong2* ak2 = reinterpret_cast<const ulonglong2*>(sh.akeys);
-#pragma unroll 1
-    for (int j0 = 0; j0 < nA; j0 += 4) {
-      const ulonglong2 p0 = ak2[j0 >> 1], p1 = ak2[(j0 >> 1) + 1];
-      const unsigned long long kq[4] = {p0.x, p0.y, p1.x, p1.y};
+    const unsigned valid = nA >= 32 ? 0xffffffffu : ((1u << nA) - 1u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned long long kj = kq[u];
-        const unsigned bit = 1u << (j0 + u);
+    for (int j2 = 0; j2 < 16; ++j2) {
+      const ulonglong2 pr = ak2[j2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const unsigned long long kj = u ? pr.y : pr.x;
+        const unsigned bit = 1u << (2 * j2 + u);
         lt |= kj < key ? bit : 0u;
         same |= (((kj ^ key) >> 16) & 0xffffull) == 0ull ? bit : 0u;
         clo |= (unsigned)(kj & 0xffffu) < c ? bit : 0u;
       }
     }
+    lt &= valid;
+    same &= valid;
+    clo &= valid;
     const bool elig = own && __popc(lt & same) < er;
     const unsigned Mq = __ballot_sync(kFull, elig);
     const int g = __popc(lt & Mq);
