@@ -12,7 +12,8 @@ Recipe:
   * rows are keyed by (seed, global request) with numpy's counter-based Philox, so a
     request's rows do not depend on how the batch is sharded across ranks;
   * logits are rounded to bf16 (round-to-nearest-even) and returned as uint16 bit
-    patterns; the fp32 variant is the same values upcast.
+    patterns; the fp32 variant is the same values upcast, and "fp32full" keeps the full fp32
+    mantissa (no bf16 rounding) for the fp32 path's own tests.
 """
 from __future__ import annotations
 
@@ -61,12 +62,15 @@ def draft_pool(seed: int, b: int, T: int, V: int, ld: int | None = None, r_offse
     out = np.empty((b, T, ld), np.uint16 if dtype == "bf16" else np.float32)
     for r in range(b):
         x = draft_rows(seed, r_offset + r, T, V, ld, **kw)
-        out[r] = f32_to_bf16_bits(x) if dtype == "bf16" else bf16_bits_to_f32(f32_to_bf16_bits(x))
+        if dtype == "fp32full":
+            out[r] = x
+        else:
+            out[r] = f32_to_bf16_bits(x) if dtype == "bf16" else bf16_bits_to_f32(f32_to_bf16_bits(x))
     return out
 
 
 def target_pool(draft: np.ndarray, seed: int, sigma_m: float, r_offset: int = 0,
-                V: int | None = None) -> np.ndarray:
+                V: int | None = None, full: bool = False) -> np.ndarray:
     """target(r, u) = draft(r, u) + sigma_m * z' (fresh keyed noise); same dtype as draft."""
     bf = draft.dtype == np.uint16
     out = np.empty_like(draft)
@@ -78,7 +82,7 @@ def target_pool(draft: np.ndarray, seed: int, sigma_m: float, r_offset: int = 0,
             noise = g.standard_normal((draft.shape[1], V), dtype=np.float32) * np.float32(sigma_m)
             base = base.copy()
             base[:, :V] += noise
-        out[r] = f32_to_bf16_bits(base) if bf else bf16_bits_to_f32(f32_to_bf16_bits(base))
+        out[r] = f32_to_bf16_bits(base) if bf else (base if full else bf16_bits_to_f32(f32_to_bf16_bits(base)))
     return out
 
 

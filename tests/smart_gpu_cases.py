@@ -42,7 +42,7 @@ def make_inputs(case: Case, T: int):
     ld = case.V + case.ld_pad
     draft = synth.draft_pool(case.seed, case.b, T, case.V, ld=ld, dtype=case.dtype, a_lo=case.a_lo,
                              a_hi=case.a_hi, sigma_bg=case.sigma_bg)
-    target = synth.target_pool(draft, case.seed + 1000, case.sigma_m, V=case.V)
+    target = synth.target_pool(draft, case.seed + 1000, case.sigma_m, V=case.V, full=case.dtype == "fp32full")
     rng = np.random.default_rng(case.seed)
     root_tok = rng.integers(0, case.V, case.b).astype(np.int32)
     root_pos = rng.integers(0, 4000, case.b).astype(np.int32)

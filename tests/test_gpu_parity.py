@@ -192,6 +192,22 @@ SMALL = {
 }
 
 
+# full-mantissa fp32 logits (the fp32 path otherwise only sees bf16-representable values)
+FP32_FULL = {
+    "cfg3_fp32full": Case(V=128256, k=8, d=6, W=8, b=32, B_verify=200, seed=12, dtype="fp32full",
+                          cost=(0.0117, 0.0, 0.05, 0.02, 1.3, 2.4631, 2.4631)),
+    "mid_fp32full_frozen": Case(V=30000, k=6, d=5, W=6, b=8, B_verify=96, seed=48, dtype="fp32full", selection=1,
+                                a_lo=6.0, a_hi=12.0, sigma_m=0.5, cost=(0.001, 0.0, 0.2, 0.05, 0.7, 1.5, 1.0)),
+}
+
+
+@pytest.mark.parametrize("name", list(FP32_FULL))
+def test_fp32_full_mantissa(name):
+    case = FP32_FULL[name]
+    orc, gpu, layers = _run(case)
+    assert sum(1 for l in range(case.d) if orc.trace[l, 3] > 0) >= 3 and layers == case.d
+
+
 @pytest.mark.parametrize("name", list(SMALL))
 def test_small_selection_paths(name):
     case, want = SMALL[name]
