@@ -474,6 +474,7 @@ struct SmallShared {
   long long N0, N0next;
   int ne, n_above, need_full, bestj;
   int a[32];
+  int nn[32];  // node counts after the last layer (lane r of warp 0), for the verify-row table
   __align__(16) unsigned long long akeys[64];
 };
 
@@ -856,6 +857,7 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       st.nd += a;
       st.cnt = nx;
       st.off = base;
+      sh.nn[lane] = st.nd + 1;
     }
     double Ea = lane < bl ? st.E : 0.0;
 #pragma unroll
@@ -986,6 +988,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   st.E = 0.0;
   bool rows_in_smem = false;  // layer 1: the roots, from the global frontier written above
   if (tid == 0) ssm.N0next = 0;
+  if (tid < bl && tid < 32) ssm.nn[tid] = 1;
   consumer_sync();
 
   for (int layer = 1; layer <= P.d; ++layer) {
@@ -1034,7 +1037,10 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
           P.trace[layer - 1].select_path = 3;
           P.trace[layer - 1].n_screened = ssm.n_above;
         }
-        if (warp == 0) small_state_load(P, layer & 1, lane, st);
+        if (warp == 0) {
+          small_state_load(P, layer & 1, lane, st);
+          if (lane < bl) ssm.nn[lane] = st.nd + 1;
+        }
         if (tid == 0) ssm.N0next = *P.N_glob;
       }
     }
@@ -1071,7 +1077,8 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   int* s_tok = s_dep + (size_t)bl * T;
   int* s_arg = s_tok + (size_t)bl * T;
   int* s_off = s_n + bl + 1;  // exclusive scan of the node counts
-  for (int r = tid; r < bl; r += kConsumers) s_off[r] = s_n[r] = P.n_nodes[r];
+  // node counts: from the small path's shared copy (no round trip through L2), else the global state
+  for (int r = tid; r < bl; r += kConsumers) s_off[r] = s_n[r] = small ? ssm.nn[r] : P.n_nodes[r];
   consumer_sync();
   if (warp == 0) {
     const int tot = warp_excl_scan_smem(s_off, bl, lane);
