@@ -474,6 +474,7 @@ struct SmallShared {
   long long N0, N0next;
   int ne, n_above, need_full, bestj;
   int a[32];
+  int vpub;    // the verify rows are published (select_small, after the last layer)
   int nn[32];  // node counts after the last layer (lane r of warp 0), for the verify-row table
   __align__(16) unsigned long long akeys[64];
 };
@@ -575,7 +576,7 @@ __device__ __forceinline__ void small_trace_full(const Params& P, char* dsm, Sma
 template <class Pub>
 __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, char* dsm, const MergeLayout& M,
                                              const MergeLayout& Mn, bool rows_in_smem, SmallState& st,
-                                             SmallShared& sh, unsigned tag, Pub pub) {
+                                             SmallShared& sh, unsigned tag, Pub pub, bool verify) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = (layer - 1) & 1, npar = layer & 1;
   const int k = P.k, bl = P.b_loc, nct = R * k, T = P.T;
@@ -859,6 +860,30 @@ __device__ __forceinline__ bool select_small(const Params& P, int layer, int R, 
       st.off = base;
       sh.nn[lane] = st.nd + 1;
     }
+    if (layer == P.d || tot == 0) {
+      // the trees are final: warp 0 publishes the verify rows ((request, node), request-major, as
+      // self-validating entries) and their count right away, from its registers
+      const int nr = lane < bl ? st.nd + 1 : 0;
+      int vin = nr;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(kFull, vin, o);
+        if (lane >= o) vin += u;
+      }
+      const int voff = vin - nr, NR = __shfl_sync(kFull, vin, 31);
+      const unsigned vtag = entry_tag(tag, 31);
+      for (int j = 0; j < nr; ++j) {
+        P.vrow_rn[voff + j] = make_int2(lane, j);
+        st_relaxed_u64(&P.fr_tag[voff + j], ((unsigned long long)vtag << 32) | ((unsigned)lane << 10) | (unsigned)j);
+      }
+      if (lane < bl) P.vrow_off[lane] = voff;
+      if (lane == 0) P.vrow_off[bl] = NR;
+      __syncwarp();
+      if (lane == 0) {
+        st_relaxed_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
+        sh.vpub = 1;
+      }
+    }
     double Ea = lane < bl ? st.E : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) Ea += __shfl_xor_sync(kFull, Ea, o);
@@ -987,7 +1012,10 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   st.nd = st.fin = 0;
   st.E = 0.0;
   bool rows_in_smem = false;  // layer 1: the roots, from the global frontier written above
-  if (tid == 0) ssm.N0next = 0;
+  if (tid == 0) {
+    ssm.N0next = 0;
+    ssm.vpub = 0;
+  }
   if (tid < bl && tid < 32) ssm.nn[tid] = 1;
   consumer_sync();
 
@@ -1025,7 +1053,7 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
     bool done = false;
     if (small) {
       done = select_small(P, layer, R, dsm, Mb[layer & 1], Mb[(layer + 1) & 1], rows_in_smem, st, ssm, tag,
-                          StepPub{&P, tag, layer});
+                          StepPub{&P, tag, layer}, verify);
       staged = !done;  // records and row requests are staged for the generic selection
       rows_in_smem = done;
     }
@@ -1087,16 +1115,18 @@ __device__ void select_role(const Params& P, char* dsm, size_t sel_bytes, const 
   consumer_sync();
   const int NR = s_off[bl];
   const unsigned vtag = entry_tag(tag, 31);
-  for (int e = tid; e < bl * T; e += kConsumers) {
+  const bool vdone = small && ssm.vpub;  // already published by select_small's warp 0
+  for (int e = tid; e < bl * T && !vdone; e += kConsumers) {
     const int r = e / T, j = e - r * T;
     if (j < s_n[r]) {
       P.vrow_rn[s_off[r] + j] = make_int2(r, j);
       st_relaxed_u64(&P.fr_tag[s_off[r] + j], ((unsigned long long)vtag << 32) | ((unsigned)r << 10) | (unsigned)j);
     }
   }
-  for (int r = tid; r <= bl; r += kConsumers) P.vrow_off[r] = s_off[r];
+  for (int r = tid; r <= bl && !vdone; r += kConsumers) P.vrow_off[r] = s_off[r];
   if (tid == 0) {
-    st_relaxed_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
+    if (!vdone)
+      st_relaxed_u64(&P.ctl->flag[kVerifySlot], ((unsigned long long)tag << 32) | (unsigned)(verify ? NR : 0));
     pb_max(P, kVerifySlot, kPbPublished);
   }
   if (SMART_PROBES && P.dbg && tid == 0) P.dbg[1001] = gtime();
