@@ -59,13 +59,17 @@ __device__ __forceinline__ float perturbed(float x, float inv_tau, uint32_t rowk
 // pass.  T = max(running best of the segment, exact perturbed value of the warp's largest x).
 // Exact: the winning token passes its own test (the rounding of fma is monotone in the addend).
 constexpr uint32_t kU999 = 8380000u;  // (h >> 9) >= this  <=>  U >= ~0.99898
-__device__ __forceinline__ uint32_t sample_hash(uint32_t rowkey, int v) {
+// the hash before its last xor-shift: that step keeps bits 31..16, so h >= kU999 << 9 = 0xFFBCC000
+// implies (h before it) >= 0xFFBC0000; testing the latter marks a superset of the large-G tokens
+// (the bound stays valid) and saves the last two operations of the per-token hash
+constexpr uint32_t kU999Pre = 0xFFBC0000u;
+static_assert((kU999 << 9) == 0xFFBCC000u, "kU999Pre follows kU999");
+__device__ __forceinline__ uint32_t sample_hash_pre(uint32_t rowkey, int v) {
   uint32_t h = rowkey + (uint32_t)v * 0x9e3779b9u;
   h ^= h >> 16;
   h *= 0x7feb352du;
   h ^= h >> 15;
   h *= 0x846ca68bu;
-  h ^= h >> 16;
   return h;
 }
 template <bool BF16>
@@ -129,9 +133,9 @@ __device__ __forceinline__ void sample_chunk(const uint4 (&raw)[kVecPerThread], 
   for (int n = 0; n < EPT; ++n) {
     const int j = n / EPV, e = n % EPV;
     const int v = cbase + (j * kConsumers + tid) * EPV + e;
-    const uint32_t h = sample_hash(rowkey, v);
-    const float gmax = (h >> 9) >= kU999 ? 16.64f : 6.92f;
-    cm |= (fmaf(xat(raw[j], e), inv_tau, gmax) >= T && v < V) ? (1u << n) : 0u;
+    const uint32_t h = sample_hash_pre(rowkey, v);
+    const float gmax = h >= kU999Pre ? 16.64f : 6.92f;
+    cm |= (fmaf(xat(raw[j], e), inv_tau, gmax) >= T && (!ragged || v < V)) ? (1u << n) : 0u;
   }
   // (3) exact perturbed values of the candidates only (rare), the lane's best, the warp's
   float pv = -INFINITY;
