@@ -174,8 +174,10 @@ struct VerifyShared {
 constexpr int kVStages = 3;
 using VPipe = StreamPipeT<kVStages>;
 
+// the T > 0 variant at 4 CTAs per SM: it is issue and latency bound (the per-token hash), so more
+// resident warps pay more than registers
 template <bool BF16, bool TMA, bool SAMPLE>
-__global__ void __launch_bounds__(kLayerThreads, 2)
+__global__ void __launch_bounds__(kLayerThreads, SAMPLE ? 4 : 2)
 verify_kernel(Params P, const char* __restrict__ target, long long ld_bytes, int32_t* accept_len,
               int32_t* accept_path, int32_t* bonus, float inv_tau, unsigned long long seed) {
   constexpr int EPV = BF16 ? 8 : 4;
