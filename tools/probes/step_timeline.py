@@ -65,7 +65,7 @@ for sidx in range(4096 // 4 - 256):
     if a:
         pc.append(((a - t0) / 1e3, (b_ - a) / 1e3, (c_ - b_) / 1e3, m & 255, (m >> 8) & 255, m >> 16, sidx))
 pc.sort()
-print("layer-2 per-CTA: first-chunk arrival, consume time of chunk 1, rest of slice (us), nch, row, smid, cta")
+print(("A8 per-CTA (SMART_DEBUG_MODE=9): first-chunk arrival, consume time of chunk 1, rest (us), units, first row, smid, cta" if os.environ.get("SMART_DEBUG_MODE") == "9" else "layer-2 per-CTA: first-chunk arrival, consume time of chunk 1, rest of slice (us), nch, row, smid, cta"))
 for x in pc[::max(1, len(pc) // 40)]:
     print("  %7.2f %5.2f %5.2f  nch %d row %d sm %d cta %d" % x)
 import statistics as stt
